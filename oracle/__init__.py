@@ -1,0 +1,148 @@
+"""ORACLE — test infrastructure only.
+
+Plain, slow, obviously-correct CPU implementation of what the hot path computes.
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` leg may import this package.  It shares no code, headers,
+tables or helpers with ``paper_1709_08625_b200`` (the CUDA path) and never imports it.
+
+Functions and the passages they follow (PAPER.md = the paper's LaTeX text):
+
+* ``besselk``, ``matern``  — Eq. (3), PAPER.md:185-191 (C(h;theta)); K_nu from the
+  integral representation (C code in ``matern.c``); half-integer closed forms
+  (read with Eq. (3)'s argument h/ell — DESIGN.md reading R1).
+* ``cov_dense``            — C_ij = C(s_i - s_j; theta) (Eq. (1) text)
+  + nugget tau^2 on the diagonal (listing).
+* ``loglik_dense``         — Eq. (1), PAPER.md:109-114:
+  L = -n/2 log(2 pi) - 1/2 log det C - 1/2 Z^T C^{-1} Z, computed through the Cholesky
+  factor C = L L^T exactly as Eq. (2) / Def. 1 writes it with the
+  exact factor: log det C = 2 sum log L_ii, v = L^{-1} Z, Z^T C^{-1} Z = v^T v.
+  The factorisation and the triangular solve are LAPACK library primitives.
+* ``sample_dense``         — Z = L xi with the exact dense factor (Sec. 5.1, PAPER.md:573-577,
+  with the exact factor in place of the H-factor; configs C1/C2 of BASELINE.json).
+
+Parity pins for every function are in ``tests/test_oracle.py`` (none unpinned).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import scipy.linalg as sla
+from threadpoolctl import threadpool_limits
+
+# Host threads used by the oracle (OpenMP fill + LAPACK). Half the logical CPUs by
+# default: with all logical CPUs OpenBLAS' dpotrf degrades badly on SMT/cgroup hosts.
+THREADS = int(os.environ.get("HCOV_ORACLE_THREADS", max(1, (os.cpu_count() or 2) // 2)))
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "matern.c")
+_SO = os.path.join(_HERE, "_oracle_matern.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile matern.c (gcc -O2 -fopenmp, no fast-math). Returns the .so path."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _SO, _SRC, "-lm"])
+    return _SO
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        # OpenMP threads of matern.c must not spin after their loop and starve the
+        # LAPACK (OpenBLAS) threads of the Cholesky step.
+        os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
+        os.environ.setdefault("OMP_NUM_THREADS", str(THREADS))
+        lib = ctypes.CDLL(_SO)
+        d, i64, p = ctypes.c_double, ctypes.c_int64, ctypes.c_void_p
+        lib.oracle_besselk.restype = d
+        lib.oracle_besselk.argtypes = [d, d]
+        lib.oracle_besselk_scaled.restype = d
+        lib.oracle_besselk_scaled.argtypes = [d, d]
+        lib.oracle_matern.restype = d
+        lib.oracle_matern.argtypes = [d, d, d, d]
+        lib.oracle_matern_integral.restype = d
+        lib.oracle_matern_integral.argtypes = [d, d, d, d]
+        lib.oracle_cov_dense.restype = None
+        lib.oracle_cov_dense.argtypes = [i64, p, d, d, d, d, p]
+        lib.oracle_cov_entries.restype = None
+        lib.oracle_cov_entries.argtypes = [i64, p, d, d, d, d, p, i64, p, i64, p]
+        _lib = lib
+    return _lib
+
+
+def besselk(nu: float, x: float) -> float:
+    """K_nu(x) by the trapezoid rule on DLMF 10.32.9."""
+    return _load().oracle_besselk(float(nu), float(x))
+
+
+def matern(h: float, sigma2: float, ell: float, nu: float, integral: bool = False) -> float:
+    """Eq. (3): sigma^2 / (2^(nu-1) Gamma(nu)) (h/ell)^nu K_nu(h/ell)."""
+    lib = _load()
+    f = lib.oracle_matern_integral if integral else lib.oracle_matern
+    return f(float(h), float(sigma2), float(ell), float(nu))
+
+
+def cov_dense(s: np.ndarray, sigma2: float, ell: float, nu: float, nugget: float) -> np.ndarray:
+    """Dense n x n covariance in external order (Eq. (1) definition + nugget)."""
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    n = s.shape[0]
+    C = np.empty((n, n), dtype=np.float64)
+    _load().oracle_cov_dense(n, s.ctypes.data, sigma2, ell, nu, nugget, C.ctypes.data)
+    return C
+
+
+def cov_entries(s, sigma2, ell, nu, nugget, rows, cols) -> np.ndarray:
+    """C[rows][:, cols] (external indices) without forming C."""
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    out = np.empty((rows.size, cols.size), dtype=np.float64)
+    _load().oracle_cov_entries(s.shape[0], s.ctypes.data, sigma2, ell, nu, nugget,
+                               rows.ctypes.data, rows.size, cols.ctypes.data, cols.size,
+                               out.ctypes.data)
+    return out
+
+
+class NotSPD(Exception):
+    pass
+
+
+def cholesky(C: np.ndarray) -> np.ndarray:
+    """Lower Cholesky factor (LAPACK dpotrf). Raises NotSPD if a pivot is <= 0."""
+    try:
+        with threadpool_limits(THREADS):
+            return sla.cholesky(C, lower=True, check_finite=False)
+    except np.linalg.LinAlgError as e:  # pragma: no cover - message passthrough
+        raise NotSPD(str(e))
+
+
+def loglik_from_factor(L: np.ndarray, Z: np.ndarray):
+    """Eq. (1) through the factor: returns (loglik, logdet, quad)."""
+    n = L.shape[0]
+    logdet = 2.0 * float(np.sum(np.log(np.diag(L))))
+    with threadpool_limits(THREADS):
+        v = sla.solve_triangular(L, np.asarray(Z, dtype=np.float64), lower=True, check_finite=False)
+    quad = float(v @ v)
+    ll = -0.5 * n * np.log(2.0 * np.pi) - 0.5 * logdet - 0.5 * quad
+    return ll, logdet, quad
+
+
+def loglik_dense(s, Z, sigma2, ell, nu, nugget):
+    """Exact Gaussian log-likelihood Eq. (1). Returns (loglik, logdet, quad)."""
+    C = cov_dense(s, sigma2, ell, nu, nugget)
+    L = cholesky(C)
+    del C
+    return loglik_from_factor(L, Z)
+
+
+def sample_dense(s, xi, sigma2, ell, nu, nugget):
+    """Z = L xi with the exact dense Cholesky factor (external order)."""
+    C = cov_dense(s, sigma2, ell, nu, nugget)
+    L = cholesky(C)
+    with threadpool_limits(THREADS):
+        return L @ np.asarray(xi, dtype=np.float64)
