@@ -1,0 +1,150 @@
+/*
+ * hcov.h — C ABI of libhcov.so: the B200-native (sm_100a, fp64) hot path of
+ * Litvinenko, "HLIBCov" (arXiv 1709.08625): evaluate the Gaussian log-likelihood of a
+ * Matern random field with the covariance held as an H-matrix.
+ *
+ *   L(theta) = -n/2 log(2 pi) - 1/2 log det C(theta) - 1/2 Z^T C(theta)^{-1} Z      Eq. (1)
+ *   L~(theta) = -n/2 log(2 pi) - sum_i log L~_ii - 1/2 v^T v,  L~ v = Z              Eq. (2)
+ *
+ * Stages: A1 cluster tree, A2 block tree (hcov_build_tree);
+ * A3-A6 Matern entries, dense leaves, ACA, truncation (hcov_assemble); A7 H-Cholesky
+ * (hcov_cholesky); A8-A10 log det, forward H-solve, L (hcov_loglik).
+ *
+ * Conventions
+ *  - All floating point is IEEE fp64.  Pointers named *_dev are CUDA device pointers,
+ *    *_host are host pointers.  Arrays are owned by the caller; the library copies what it
+ *    keeps into handle-owned device memory.  Handles are owned by the caller and released
+ *    with hcov_*_free.  Streams: every call is ordered on the given stream (0 = legacy default).
+ *  - Index order: "external" = the caller's order of the n locations; "internal" = cluster-tree
+ *    order (perm_e2i / perm_i2e).  Z and sampled vectors are external.
+ *  - Errors: every function returns hcov_status; nothing throws across the ABI.  On error the
+ *    output handle is left NULL and no memory is leaked.
+ *  - Determinism: the same inputs on the same device give bitwise-identical outputs.
+ *  - Thread safety: a handle must not be used from several host threads concurrently.
+ */
+#ifndef HCOV_H
+#define HCOV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HCOV_OK = 0,
+    HCOV_ERR_INVALID_ARG = 1,   /* sigma2, ell, nu <= 0; nugget, eps < 0; leaf < 1; non-finite coordinates; NULL pointer */
+    HCOV_ERR_EMPTY_INPUT = 2,   /* n == 0 */
+    HCOV_ERR_NOT_SPD = 3,       /* a diagonal-leaf pivot <= 0 during the H-Cholesky (fail_leaf reports which) */
+    HCOV_ERR_OUT_OF_MEMORY = 4, /* device allocation failed */
+    HCOV_ERR_CUDA = 5,          /* any other CUDA runtime error */
+    HCOV_ERR_RANK_CAPACITY = 6, /* an epsilon-rank exceeded the rank capacity with kmax == 0 */
+    HCOV_ERR_STATE = 7          /* call order violated (e.g. loglik on an unfactored matrix) */
+} hcov_status;
+
+typedef struct hcov_tree_s *hcov_tree;  /* cluster tree + block tree + theta-independent schedule */
+typedef struct hcov_hmat_s *hcov_hmat;  /* device H-matrix: C~ after hcov_assemble, L~ (in place) after hcov_cholesky */
+typedef void *hcov_stream;              /* a cudaStream_t */
+
+/* Eq. (3):  C(h) = sigma2 / (2^(nu-1) Gamma(nu)) (h/ell)^nu K_nu(h/ell);
+ * nugget tau^2 is added on the diagonal (listing PAPER.md:534). */
+typedef struct {
+    double sigma2, ell, nu, nugget;
+} hcov_theta;
+
+/* Remark 2: per admissible block keep the smallest rank r with
+ * sigma_{r+1} <= eps * sigma_1 (adaptive), and r <= kmax (fixed) when kmax > 0.
+ * kcap = rank capacity of the device pools (0 = default: kmax if kmax > 0 else 64). */
+typedef struct {
+    double eps;
+    int32_t kmax;
+    int32_t kcap;
+} hcov_trunc;
+
+typedef struct {
+    double loglik;        /* L~(theta), Eq. (2) */
+    double logdet;        /* log det C~ = 2 sum log L~_ii */
+    double quad;          /* v^T v, L~ v = P_e2i Z */
+    int64_t n;
+    int32_t max_rank;     /* largest rank of any low-rank block of L~ */
+    int32_t cap_binds;    /* number of truncations where kmax bound below the eps-rank */
+    double min_pivot;     /* smallest L~_ii^2 */
+    int64_t fail_leaf;    /* -1, or the first diagonal leaf whose pivot failed */
+} hcov_result;
+
+typedef struct {
+    int64_t n, n_pad;       /* locations; padded size 32 * 2^depth (phantom identity rows) */
+    int32_t depth, leaf_size;
+    int64_t n_leaves;
+    int64_t n_dense_tiles;  /* 32x32 tiles of the lower triangle incl. diagonal */
+    int64_t n_lowrank;      /* admissible low-rank blocks (lower triangle) */
+    int64_t n_tasks, n_waves;
+    double eta;
+} hcov_tree_info;
+
+/* A1 + A2: cluster tree by median bisection on the longest bounding-box axis (leaves <= leaf_size,
+ * uniform depth), eta-admissible block tree (min(diam) <= eta * dist, dist > 0; PAPER.md:475,
+ * 723-743), and the theta-independent H-Cholesky task schedule.
+ *   s_dev: n x 2 row-major device array of locations (external order).
+ *   leaf_size: 32 (the only supported value).  eta: admissibility parameter (2.0; 0 = all dense).
+ *   dense_below: admissible blocks with cluster size <= dense_below are stored as dense tiles
+ *   (32 = only leaf-level blocks). */
+hcov_status hcov_build_tree(const double *s_dev, int64_t n, int32_t leaf_size, double eta,
+                            int32_t dense_below, hcov_stream stream, hcov_tree *out);
+/* Host-only planning (no device memory is touched; usable without a GPU): same as
+ * hcov_build_tree with s_host a host array.  Device arrays are uploaded on first use. */
+hcov_status hcov_build_tree_host(const double *s_host, int64_t n, int32_t leaf_size, double eta,
+                                 int32_t dense_below, hcov_tree *out);
+hcov_status hcov_tree_get_info(hcov_tree t, hcov_tree_info *info);
+/* Block-tree nodes (lower triangle incl. diagonal), 4 int32 per node: level, i, j, type
+ * (0 = inadmissible/subdivided, 1 = low-rank leaf, 2 = dense 32x32 leaf).  With out4 == NULL
+ * only *count is set; otherwise cap >= *count is required. */
+hcov_status hcov_tree_blocks(hcov_tree t, int32_t *out4, int64_t cap, int64_t *count);
+/* Cluster bounding boxes, 4 doubles per cluster heap id (2^l - 1 + c): lo_x, lo_y, hi_x, hi_y. */
+hcov_status hcov_tree_bbox(hcov_tree t, double *bb, int64_t cap);
+/* perm_i2e: n_pad int64 (host); entry k = external index of internal position k, -1 for phantom rows. */
+hcov_status hcov_tree_perm(hcov_tree t, int64_t *perm_i2e_host);
+
+/* A3-A6: dense leaves filled with Eq. (3) (+nugget), admissible blocks by ACA (Alg. B.1,
+ * PAPER.md:759-787) to eps/10, then QR+SVD truncation to (eps, kmax). */
+hcov_status hcov_assemble(hcov_tree t, const hcov_theta *theta, const hcov_trunc *trunc,
+                          hcov_stream stream, hcov_hmat *out);
+
+/* A7: H-Cholesky C~ = L~ L~^T in place (Eq. (2)).  Synchronises the
+ * stream.  fail_leaf (may be NULL) receives -1 or the first failing diagonal leaf. */
+hcov_status hcov_cholesky(hcov_hmat h, hcov_stream stream, int64_t *fail_leaf);
+
+/* A8-A10: log det = 2 sum log L~_ii, v = L~^{-1} P_e2i Z (forward H-solve), q = v^T v,
+ * L~ = -n/2 log 2pi - logdet/2 - q/2.  Z_dev: n fp64 external order.  Synchronises. */
+hcov_status hcov_loglik(hcov_hmat h, const double *Z_dev, hcov_stream stream, hcov_result *out);
+
+/* A3-A10 in one call (assemble + factor + loglik), handle-free for the caller. */
+hcov_status hcov_eval(hcov_tree t, const hcov_theta *theta, const hcov_trunc *trunc,
+                      const double *Z_dev, hcov_stream stream, hcov_result *out);
+
+/* Theta batch (MLE candidates): evaluates m thetas; loglik_host[i] = -INFINITY and
+ * status_host[i] != HCOV_OK for rejected candidates (not SPD, rank capacity); the batch
+ * continues.  Returns HCOV_OK unless an argument or CUDA error aborts the batch. */
+hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *thetas_host, int32_t m,
+                           const hcov_trunc *trunc, hcov_stream stream, double *loglik_host,
+                           hcov_status *status_host);
+
+/* Support (not timed).  Z = P_i2e L~ xi for a factored matrix (Sec. 5.1);
+ * xi_dev, Z_dev: n fp64 (xi in external order too: xi is permuted to internal first). */
+hcov_status hcov_sample(hcov_hmat h, const double *xi_dev, double *Z_dev, hcov_stream stream);
+/* Columns of the assembled C~ (before hcov_cholesky): out_dev is n x m column-major, external
+ * row order; cols_host are external column indices. */
+hcov_status hcov_columns(hcov_hmat h, const int64_t *cols_host, int32_t m, double *out_dev,
+                         hcov_stream stream);
+/* Diagnostics of an H-matrix: bytes of dense tiles and low-rank factors at actual ranks. */
+hcov_status hcov_hmat_storage(hcov_hmat h, int64_t *dense_bytes, int64_t *lowrank_bytes,
+                              int32_t *max_rank);
+
+void hcov_tree_free(hcov_tree t);
+void hcov_hmat_free(hcov_hmat h);
+const char *hcov_status_string(hcov_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCOV_H */

@@ -1,0 +1,247 @@
+"""paper_1709_08625_b200 — thin Python binding of libhcov.so (include/hcov.h).
+
+Argument marshalling only: every step of the likelihood path runs in the CUDA kernels of
+``csrc/``.  PyTorch supplies device memory and the current stream.  There is no CPU fallback:
+``lib()`` raises if the shared library is missing and every compute entry point requires CUDA
+tensors.  Names follow the C ABI (hcov_build_tree, hcov_assemble, hcov_cholesky, hcov_loglik,
+hcov_eval, hcov_mle_batch, hcov_sample, hcov_columns).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhcov.so")
+
+HCOV_OK = 0
+STATUS = {0: "ok", 1: "invalid argument", 2: "empty input", 3: "not SPD", 4: "out of memory",
+          5: "CUDA error", 6: "rank capacity exceeded", 7: "invalid call order"}
+ND_H, ND_R, ND_T = 0, 1, 2
+
+
+class HcovError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {STATUS.get(code, code)} ({code})")
+        self.code = code
+
+
+class Theta(ctypes.Structure):
+    _fields_ = [("sigma2", ctypes.c_double), ("ell", ctypes.c_double), ("nu", ctypes.c_double),
+                ("nugget", ctypes.c_double)]
+
+
+class Trunc(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_double), ("kmax", ctypes.c_int32), ("kcap", ctypes.c_int32)]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [("loglik", ctypes.c_double), ("logdet", ctypes.c_double), ("quad", ctypes.c_double),
+                ("n", ctypes.c_int64), ("max_rank", ctypes.c_int32), ("cap_binds", ctypes.c_int32),
+                ("min_pivot", ctypes.c_double), ("fail_leaf", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class TreeInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("n_pad", ctypes.c_int64), ("depth", ctypes.c_int32),
+                ("leaf_size", ctypes.c_int32), ("n_leaves", ctypes.c_int64), ("n_dense_tiles", ctypes.c_int64),
+                ("n_lowrank", ctypes.c_int64), ("n_tasks", ctypes.c_int64), ("n_waves", ctypes.c_int64),
+                ("eta", ctypes.c_double)]
+
+
+# name -> (restype, argtypes) ; every symbol declared in include/hcov.h
+_P, _I32, _I64, _D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+_SIGS = {
+    "hcov_build_tree": (_I32, [_P, _I64, _I32, _D, _I32, _P, _P]),
+    "hcov_build_tree_host": (_I32, [_P, _I64, _I32, _D, _I32, _P]),
+    "hcov_tree_get_info": (_I32, [_P, _P]),
+    "hcov_tree_blocks": (_I32, [_P, _P, _I64, _P]),
+    "hcov_tree_bbox": (_I32, [_P, _P, _I64]),
+    "hcov_tree_perm": (_I32, [_P, _P]),
+    "hcov_assemble": (_I32, [_P, _P, _P, _P, _P]),
+    "hcov_cholesky": (_I32, [_P, _P, _P]),
+    "hcov_loglik": (_I32, [_P, _P, _P, _P]),
+    "hcov_eval": (_I32, [_P, _P, _P, _P, _P, _P]),
+    "hcov_mle_batch": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P]),
+    "hcov_sample": (_I32, [_P, _P, _P, _P]),
+    "hcov_columns": (_I32, [_P, _P, _I32, _P, _P]),
+    "hcov_hmat_storage": (_I32, [_P, _P, _P, _P]),
+    "hcov_tree_free": (None, [_P]),
+    "hcov_hmat_free": (None, [_P]),
+    "hcov_status_string": (ctypes.c_char_p, [_I32]),
+}
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libhcov.so (built in-tree by build.py / __graft_entry__.build()). Fails loudly."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libhcov.so not built ({LIB_PATH}); run `python -m paper_1709_08625_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(code: int, where: str):
+    if code != HCOV_OK:
+        raise HcovError(code, where)
+
+
+def _stream(stream=None):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_f64(x, n=None, name="array"):
+    import torch
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+    if n is not None and x.numel() != n:
+        raise ValueError(f"{name}: expected {n} elements, got {x.numel()}")
+    return ctypes.c_void_p(x.data_ptr())
+
+
+class Tree:
+    """Cluster tree + block tree + theta-independent schedule (hcov_tree)."""
+
+    def __init__(self, s, eta: float = 2.0, dense_below: int = 32, leaf_size: int = 32, stream=None):
+        L = lib()
+        h = ctypes.c_void_p()
+        if isinstance(s, np.ndarray):
+            a = np.ascontiguousarray(s, dtype=np.float64)
+            self.n = a.shape[0]
+            _check(L.hcov_build_tree_host(a.ctypes.data, self.n, leaf_size, eta, dense_below, ctypes.byref(h)),
+                   "hcov_build_tree_host")
+        else:
+            self.n = s.shape[0]
+            _check(L.hcov_build_tree(_dev_f64(s, 2 * self.n, "s"), self.n, leaf_size, eta, dense_below,
+                                     _stream(stream), ctypes.byref(h)), "hcov_build_tree")
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.hcov_tree_free(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> dict:
+        i = TreeInfo()
+        _check(lib().hcov_tree_get_info(self._h, ctypes.byref(i)), "hcov_tree_get_info")
+        return {k: getattr(i, k) for k, _ in i._fields_}
+
+    def perm_i2e(self) -> np.ndarray:
+        npad = self.info()["n_pad"]
+        p = np.empty(npad, dtype=np.int64)
+        _check(lib().hcov_tree_perm(self._h, p.ctypes.data), "hcov_tree_perm")
+        return p
+
+    def blocks(self) -> np.ndarray:
+        cnt = ctypes.c_int64()
+        _check(lib().hcov_tree_blocks(self._h, None, 0, ctypes.byref(cnt)), "hcov_tree_blocks")
+        out = np.empty((cnt.value, 4), dtype=np.int32)
+        _check(lib().hcov_tree_blocks(self._h, out.ctypes.data, cnt.value, ctypes.byref(cnt)), "hcov_tree_blocks")
+        return out
+
+    def bbox(self) -> np.ndarray:
+        d = self.info()["depth"]
+        nc = (2 << d) - 1
+        out = np.empty((nc, 4), dtype=np.float64)
+        _check(lib().hcov_tree_bbox(self._h, out.ctypes.data, out.size), "hcov_tree_bbox")
+        return out
+
+
+def build_tree(s, eta: float = 2.0, dense_below: int = 32, stream=None) -> Tree:
+    return Tree(s, eta=eta, dense_below=dense_below, stream=stream)
+
+
+class HMatrix:
+    """Device H-matrix (hcov_hmat): C~ after assemble, L~ after cholesky."""
+
+    def __init__(self, tree: Tree, theta, eps: float, kmax: int = 0, kcap: int = 0, stream=None):
+        self.tree = tree
+        h = ctypes.c_void_p()
+        th = Theta(*theta)
+        tr = Trunc(eps, kmax, kcap)
+        _check(lib().hcov_assemble(tree.handle, ctypes.byref(th), ctypes.byref(tr), _stream(stream), ctypes.byref(h)),
+               "hcov_assemble")
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.hcov_hmat_free(self._h)
+            self._h = None
+
+    def cholesky(self, stream=None) -> int:
+        fl = ctypes.c_int64(-1)
+        code = lib().hcov_cholesky(self._h, _stream(stream), ctypes.byref(fl))
+        _check(code, "hcov_cholesky")
+        return fl.value
+
+    def loglik(self, Z, stream=None) -> dict:
+        r = Result()
+        _check(lib().hcov_loglik(self._h, _dev_f64(Z, self.tree.n, "Z"), _stream(stream), ctypes.byref(r)),
+               "hcov_loglik")
+        return r.as_dict()
+
+    def sample(self, xi, stream=None):
+        import torch
+        Z = torch.empty_like(xi)
+        _check(lib().hcov_sample(self._h, _dev_f64(xi, self.tree.n, "xi"), _dev_f64(Z), _stream(stream)),
+               "hcov_sample")
+        return Z
+
+    def columns(self, cols: Sequence[int], stream=None):
+        import torch
+        c = np.ascontiguousarray(cols, dtype=np.int64)
+        out = torch.empty((len(c), self.tree.n), dtype=torch.float64, device="cuda")
+        _check(lib().hcov_columns(self._h, c.ctypes.data, len(c), _dev_f64(out), _stream(stream)), "hcov_columns")
+        return out.T   # n x m, external rows
+
+    def storage(self) -> dict:
+        d, l, m = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        _check(lib().hcov_hmat_storage(self._h, ctypes.byref(d), ctypes.byref(l), ctypes.byref(m)), "hcov_hmat_storage")
+        return {"dense_bytes": d.value, "lowrank_bytes": l.value, "max_rank": m.value}
+
+
+def eval_loglik(tree: Tree, theta, Z, eps: float, kmax: int = 0, kcap: int = 0, stream=None) -> dict:
+    """hcov_eval: assemble + H-Cholesky + log det + forward solve. Raises HcovError(3) if not SPD."""
+    r = Result()
+    th = Theta(*theta)
+    tr = Trunc(eps, kmax, kcap)
+    code = lib().hcov_eval(tree.handle, ctypes.byref(th), ctypes.byref(tr), _dev_f64(Z, tree.n, "Z"),
+                           _stream(stream), ctypes.byref(r))
+    d = r.as_dict()
+    d["status"] = code
+    if code not in (HCOV_OK, 3, 6):
+        raise HcovError(code, "hcov_eval")
+    return d
+
+
+def mle_batch(tree: Tree, Z, thetas, eps: float, kmax: int = 0, kcap: int = 0, stream=None):
+    """hcov_mle_batch: returns (loglik[m], status[m]); rejected candidates get -inf."""
+    m = len(thetas)
+    arr = (Theta * m)(*[Theta(*t) for t in thetas])
+    tr = Trunc(eps, kmax, kcap)
+    ll = np.empty(m, dtype=np.float64)
+    st = np.empty(m, dtype=np.int32)
+    _check(lib().hcov_mle_batch(tree.handle, _dev_f64(Z, tree.n, "Z"), ctypes.cast(arr, ctypes.c_void_p), m,
+                                ctypes.byref(tr), _stream(stream), ll.ctypes.data, st.ctypes.data), "hcov_mle_batch")
+    return ll, st

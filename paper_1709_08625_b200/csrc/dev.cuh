@@ -1,0 +1,62 @@
+// CTA-level helpers: reductions with deterministic ordering.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define NT 128          // threads per CTA for every task kernel
+#define NWARP (NT / 32)
+
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block sum; result broadcast to all threads.  red: >= NWARP doubles of shared memory.
+__device__ __forceinline__ double block_sum(double v, double *red)
+{
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < NWARP; ++k) t += red[k];
+    return t;
+}
+
+// argmax |v| with ties -> lowest index; returns (value, index) to all threads.
+struct ValIdx { double v; int64_t i; };
+__device__ __forceinline__ bool vi_better(double av, int64_t ai, double bv, int64_t bi)
+{
+    return (av > bv) || (av == bv && ai < bi);
+}
+__device__ __forceinline__ ValIdx warp_argmax(double v, int64_t i)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+        if (vi_better(ov, oi, v, i)) { v = ov; i = oi; }
+    }
+    return ValIdx{v, i};
+}
+__device__ __forceinline__ ValIdx block_argmax(double v, int64_t i, double *redv, int64_t *redi)
+{
+    ValIdx r = warp_argmax(v, i);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) { redv[w] = r.v; redi[w] = r.i; }
+    __syncthreads();
+    ValIdx b{redv[0], redi[0]};
+#pragma unroll
+    for (int k = 1; k < NWARP; ++k)
+        if (vi_better(redv[k], redi[k], b.v, b.i)) { b.v = redv[k]; b.i = redi[k]; }
+    return b;
+}
+
+// Loads that bypass L1 (data written by other CTAs in earlier launches/waves is always in
+// L2; within a launch no task reads data another task of the same launch writes).
+__device__ __forceinline__ double ldg_cg(const double *p) { return __ldcg(p); }

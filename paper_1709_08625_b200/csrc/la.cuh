@@ -1,0 +1,398 @@
+// CTA-level fp64 linear algebra used by the task kernels (NT = 128 threads per CTA).
+//   * 32x32 tile POTRF / TRSM / GEMM (dense leaves, A7)
+//   * Householder QR of tall-skinny panels and application of Q (A6)
+//   * one-sided Jacobi SVD of the small core (A6)
+//   * truncation  X Y^T -> U V^T  with sigma_{r+1} <= eps sigma_1, r <= kmax   (Remark 2)
+//   * partially pivoted ACA on the Matern kernel (Alg. B.1)
+//   * fully pivoted cross approximation of a dense Schur block (recompression)
+// All matrices are column-major.
+#pragma once
+#include "dev.cuh"
+#include "matern.cuh"
+
+// ------------------------------------------------------------------------------------------
+// tiles (shared memory, 32 x 32 col-major)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void tile_load(double *s, const double *g)
+{
+    for (int e = threadIdx.x; e < HCOV_TILE; e += NT) s[e] = ldg_cg(g + e);
+}
+__device__ __forceinline__ void tile_store(double *g, const double *s)
+{
+    for (int e = threadIdx.x; e < HCOV_TILE; e += NT) g[e] = s[e];
+}
+
+// In-place lower Cholesky. Returns 0, or k+1 for the first non-positive pivot k.
+// On success the strict upper triangle is zeroed; *logsum = sum_k log L_kk, *minpiv = min L_kk^2.
+__device__ int tile_potrf(double *A, double *logsum, double *minpiv)
+{
+    __shared__ int s_fail;
+    if (threadIdx.x == 0) s_fail = 0;
+    __syncthreads();
+    for (int k = 0; k < 32; ++k) {
+        if (threadIdx.x == 0) {
+            double d = A[k + 32 * k];
+            if (!(d > 0.0) || !isfinite(d)) s_fail = k + 1;
+            else A[k + 32 * k] = sqrt(d);
+        }
+        __syncthreads();
+        if (s_fail) break;
+        const double dk = A[k + 32 * k];
+        if (threadIdx.x > k && threadIdx.x < 32) A[threadIdx.x + 32 * k] /= dk;
+        __syncthreads();
+        for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
+            int i = e & 31, j = e >> 5;
+            if (j > k && i >= j) A[i + 32 * j] -= A[i + 32 * k] * A[j + 32 * k];
+        }
+        __syncthreads();
+    }
+    int f = s_fail;
+    if (f) return f;
+    for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
+        int i = e & 31, j = e >> 5;
+        if (i < j) A[e] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+        double ls = 0.0, mp = INFINITY;
+        for (int k = 0; k < 32; ++k) {
+            double d = A[k + 32 * k];
+            ls += log(d);
+            mp = fmin(mp, d * d);
+        }
+        *logsum = ls;
+        *minpiv = mp;
+    }
+    __syncthreads();
+    return 0;
+}
+
+// X <- X L^{-T}  (L lower 32x32), both in shared memory.
+__device__ __forceinline__ void tile_trsm_rt(double *X, const double *L)
+{
+    if (threadIdx.x < 32) {
+        const int i = threadIdx.x;
+        for (int k = 0; k < 32; ++k) {
+            double s = X[i + 32 * k];
+            for (int j = 0; j < k; ++j) s -= X[i + 32 * j] * L[k + 32 * j];
+            X[i + 32 * k] = s / L[k + 32 * k];
+        }
+    }
+    __syncthreads();
+}
+
+// S -= A B^T  (all 32x32 shared)
+__device__ __forceinline__ void tile_gemm_nt_sub(double *S, const double *A, const double *B)
+{
+    for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
+        int i = e & 31, j = e >> 5;
+        double s = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) s += A[i + 32 * k] * B[j + 32 * k];
+        S[e] -= s;
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------
+// Householder QR of a tall-skinny panel in global memory: A (m x R, lda), R <= m.
+// Reflector j: v_j = [1; A[j+1:m, j]], H_j = I - tau_j v_j v_j^T; R in the upper triangle.
+// ------------------------------------------------------------------------------------------
+__device__ void qr_house(double *A, int64_t lda, int64_t m, int R, double *tau, double *red)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = 0; j < R; ++j) {
+        double *aj = A + lda * j;
+        double s = 0.0;
+        for (int64_t i = j + 1 + threadIdx.x; i < m; i += NT) { double v = aj[i]; s += v * v; }
+        s = block_sum(s, red);
+        const double alpha = aj[j];
+        double t = 0.0, beta = alpha, scale = 0.0;
+        if (s > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + s), alpha);
+            t = (beta - alpha) / beta;
+            scale = 1.0 / (alpha - beta);
+        }
+        __syncthreads();
+        if (s > 0.0) {
+            for (int64_t i = j + 1 + threadIdx.x; i < m; i += NT) aj[i] *= scale;
+        }
+        if (threadIdx.x == 0) { aj[j] = beta; tau[j] = t; }
+        __syncthreads();
+        if (t != 0.0) {
+            for (int k = j + 1 + warp; k < R; k += NWARP) {
+                double *ak = A + lda * k;
+                double w = 0.0;
+                for (int64_t i = j + 1 + lane; i < m; i += 32) w += aj[i] * ak[i];
+                w = warp_sum(w) + ak[j];
+                w *= t;
+                if (lane == 0) ak[j] -= w;
+                for (int64_t i = j + 1 + lane; i < m; i += 32) ak[i] -= aj[i] * w;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// B <- Q B with Q = H_0 H_1 ... H_{R-1} stored by qr_house in A.  B: m x r (ldb).
+__device__ void qr_apply_q(const double *A, int64_t lda, int64_t m, int R, const double *tau,
+                           double *B, int64_t ldb, int r)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = R - 1; j >= 0; --j) {
+        const double t = tau[j];
+        if (t == 0.0) continue;
+        const double *aj = A + lda * j;
+        for (int c = warp; c < r; c += NWARP) {
+            double *bc = B + ldb * c;
+            double w = 0.0;
+            for (int64_t i = j + 1 + lane; i < m; i += 32) w += aj[i] * bc[i];
+            w = warp_sum(w) + bc[j];
+            w *= t;
+            if (lane == 0) bc[j] -= w;
+            for (int64_t i = j + 1 + lane; i < m; i += 32) bc[i] -= aj[i] * w;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// One-sided Jacobi SVD of M (R x R, ld R, global scratch): on return M <- M J (columns
+// mutually orthogonal, ||col_i|| = sigma_i) and J orthogonal, so M_in = (M J) J^T.
+// Round-robin parallel ordering (R/2 disjoint pairs per round, one warp per pair).
+// ------------------------------------------------------------------------------------------
+__device__ void jacobi_svd(double *M, double *J, int R)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ int s_rot;
+    for (int e = threadIdx.x; e < R * R; e += NT) J[e] = ((e % R) == (e / R)) ? 1.0 : 0.0;
+    __syncthreads();
+    const int Rp = R + (R & 1);
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        if (threadIdx.x == 0) s_rot = 0;
+        __syncthreads();
+        for (int round = 0; round < Rp - 1; ++round) {
+            for (int t = warp; t < Rp / 2; t += NWARP) {
+                int a = t, b = Rp - 1 - t;
+                int p = (a == 0) ? 0 : 1 + ((a - 1 + round) % (Rp - 1));
+                int q = (b == 0) ? 0 : 1 + ((b - 1 + round) % (Rp - 1));
+                if (p >= R || q >= R) continue;
+                double *mp = M + (int64_t)R * p, *mq = M + (int64_t)R * q;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = lane; i < R; i += 32) {
+                    double x = mp[i], y = mq[i];
+                    al += x * x; be += y * y; ga += x * y;
+                }
+                al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+                if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+                    double zeta = (be - al) / (2.0 * ga);
+                    double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+                    for (int i = lane; i < R; i += 32) {
+                        double x = mp[i], y = mq[i];
+                        mp[i] = c * x - s * y;
+                        mq[i] = s * x + c * y;
+                    }
+                    double *jp = J + (int64_t)R * p, *jq = J + (int64_t)R * q;
+                    for (int i = lane; i < R; i += 32) {
+                        double x = jp[i], y = jq[i];
+                        jp[i] = c * x - s * y;
+                        jq[i] = s * x + c * y;
+                    }
+                    if (lane == 0) s_rot = 1;
+                }
+            }
+            __syncthreads();
+        }
+        if (!s_rot) break;
+        __syncthreads();
+    }
+    __syncthreads();
+}
+
+// Truncation workspace for R columns of m rows.
+struct CompressWs {
+    double *X, *Y;      // m x R each (ld m): inputs, destroyed
+    double *M, *J;      // R x R each
+    double *tx, *ty;    // R each
+    double *sig;        // R
+    int *ord;           // R
+};
+
+// Truncate X Y^T (m x m, rank <= R) to U V^T with the smallest r such that
+// sigma_{r+1} <= eps * sigma_1, then r <= kmax (if kmax > 0), r <= kcap.
+// U, V: m x kcap (ld ldo).  Returns r; *cap_bound = 1 if kmax cut below the eps-rank,
+// *overflow = 1 if the eps-rank exceeded kcap with kmax == 0 (result truncated to kcap).
+__device__ int compress(const CompressWs &w, int64_t m, int R, double eps, int kmax, int kcap,
+                        double *U, double *V, int64_t ldo, int *cap_bound, int *overflow, double *red)
+{
+    if (R == 0) { if (threadIdx.x == 0) { *cap_bound = 0; *overflow = 0; } __syncthreads(); return 0; }
+    qr_house(w.X, m, m, R, w.tx, red);
+    qr_house(w.Y, m, m, R, w.ty, red);
+    // M = R_X R_Y^T   (R_X[i,k] != 0 for k >= i)
+    for (int e = threadIdx.x; e < R * R; e += NT) {
+        int i = e % R, j = e / R;
+        double s = 0.0;
+        for (int k = max(i, j); k < R; ++k) s += w.X[i + m * k] * w.Y[j + m * k];
+        w.M[e] = s;
+    }
+    __syncthreads();
+    jacobi_svd(w.M, w.J, R);
+    for (int i = threadIdx.x; i < R; i += NT) {
+        double s = 0.0;
+        for (int k = 0; k < R; ++k) { double x = w.M[k + R * i]; s += x * x; }
+        w.sig[i] = sqrt(s);
+    }
+    __syncthreads();
+    // rank of each singular value in descending order (ties -> lower index first)
+    for (int i = threadIdx.x; i < R; i += NT) {
+        int pos = 0;
+        double si = w.sig[i];
+        for (int j = 0; j < R; ++j) {
+            double sj = w.sig[j];
+            if (sj > si || (sj == si && j < i)) ++pos;
+        }
+        w.ord[pos] = i;
+    }
+    __syncthreads();
+    __shared__ int s_r, s_cb, s_of;
+    if (threadIdx.x == 0) {
+        double s1 = w.sig[w.ord[0]];
+        int r = 0;
+        if (s1 > 0.0)
+            while (r < R && w.sig[w.ord[r]] > eps * s1) ++r;
+        int cb = 0, of = 0;
+        if (kmax > 0 && r > kmax) { r = kmax; cb = 1; }
+        if (r > kcap) { r = kcap; of = (kmax == 0); }
+        s_r = r; s_cb = cb; s_of = of;
+    }
+    __syncthreads();
+    const int r = s_r;
+    // U = Q_X [ (M J)_r ; 0 ],  V = Q_Y [ J_r ; 0 ]
+    for (int64_t e = threadIdx.x; e < (int64_t)m * r; e += NT) {
+        int64_t i = e % m;
+        int c = (int)(e / m);
+        int src = w.ord[c];
+        U[i + ldo * c] = (i < R) ? w.M[i + R * src] : 0.0;
+        V[i + ldo * c] = (i < R) ? w.J[i + R * src] : 0.0;
+    }
+    __syncthreads();
+    qr_apply_q(w.X, m, m, R, w.tx, U, ldo, r);
+    qr_apply_q(w.Y, m, m, R, w.ty, V, ldo, r);
+    if (threadIdx.x == 0) { *cap_bound = s_cb; *overflow = s_of; }
+    __syncthreads();
+    return r;
+}
+
+// ------------------------------------------------------------------------------------------
+// Fully pivoted cross approximation of a dense m x m block S (global, ld m), destroyed.
+// Appends up to Kmax columns to X, Y (ld m): S ~= X Y^T.  Stops when max |residual| <= tol.
+// ------------------------------------------------------------------------------------------
+__device__ int aca_full(double *S, int64_t m, double *X, double *Y, int Kmax, double rel_tol,
+                        double *redv, int64_t *redi)
+{
+    const int64_t mm = m * m;
+    double bv = 0.0; int64_t bi = 0;
+    for (int64_t e = threadIdx.x; e < mm; e += NT) {
+        double a = fabs(S[e]);
+        if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
+    }
+    ValIdx b = block_argmax(bv, bi, redv, redi);
+    const double tol = rel_tol * b.v;
+    int k = 0;
+    while (k < Kmax && b.v > tol && b.v > 0.0) {
+        const int64_t is = b.i % m, js = b.i / m;
+        const double p = S[is + m * js];
+        for (int64_t i = threadIdx.x; i < m; i += NT) {
+            X[i + m * k] = S[i + m * js];
+            Y[i + m * k] = S[is + m * i] / p;
+        }
+        __syncthreads();
+        bv = 0.0; bi = 0;
+        const double *xk = X + m * k, *yk = Y + m * k;
+        for (int64_t e = threadIdx.x; e < mm; e += NT) {
+            int64_t i = e % m, j = e / m;
+            double v = S[e] - xk[i] * yk[j];
+            S[e] = v;
+            double a = fabs(v);
+            if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
+        }
+        b = block_argmax(bv, bi, redv, redi);
+        ++k;
+    }
+    __syncthreads();
+    return k;
+}
+
+// ------------------------------------------------------------------------------------------
+// Partially pivoted ACA (Alg. B.1) of the Matern block with rows at internal
+// positions r0.., columns c0.. (m x m).  U, V: m x Kmax (ld m).  Reading R4:
+// first row i* = 0; ties -> lowest index; column scaled by 1/pivot; a zero residual row is
+// skipped (next unused row); stop after adding term k when ||u_k|| ||v_k|| <= eps_aca ||u_1|| ||v_1||.
+// ------------------------------------------------------------------------------------------
+__device__ int aca_partial(const MaternParams &mp, const double *xs, const double *ys, int64_t r0,
+                           int64_t c0, int64_t m, double *U, double *V, int Kmax, double eps_aca,
+                           uint8_t *used, double *red, double *redv, int64_t *redi)
+{
+    for (int64_t i = threadIdx.x; i < m; i += NT) used[i] = 0;
+    __syncthreads();
+    int64_t istar = 0;
+    int k = 0;
+    double n1 = 0.0;
+    int64_t guard = 0;
+    while (k < Kmax && guard++ < m + Kmax) {
+        // row residual -> V[:,k]
+        const double xi = xs[r0 + istar], yi = ys[r0 + istar];
+        double bv = 0.0; int64_t bi = 0;
+        double *vk = V + m * k;
+        for (int64_t j = threadIdx.x; j < m; j += NT) {
+            double a = hcov_cov_entry(mp, xi, yi, xs[c0 + j], ys[c0 + j], (r0 + istar) == (c0 + j));
+            for (int l = 0; l < k; ++l) a -= U[istar + m * l] * V[j + m * l];
+            vk[j] = a;
+            double aa = fabs(a);
+            if (vi_better(aa, j, bv, bi)) { bv = aa; bi = j; }
+        }
+        ValIdx b = block_argmax(bv, bi, redv, redi);
+        if (threadIdx.x == 0) used[istar] = 1;
+        __syncthreads();
+        if (!(b.v > 0.0)) {
+            // zero residual row: next unused row (lowest index)
+            int64_t cand = m;
+            for (int64_t i = threadIdx.x; i < m; i += NT)
+                if (!used[i] && i < cand) cand = i;
+            ValIdx c = block_argmax(-(double)cand, cand, redv, redi);  // min index
+            if (c.i >= m) break;
+            istar = c.i;
+            continue;
+        }
+        const int64_t js = b.i;
+        const double piv = vk[js];
+        const double xj = xs[c0 + js], yj = ys[c0 + js];
+        double *uk = U + m * k;
+        bv = -1.0; bi = m;
+        double su = 0.0, sv = 0.0;
+        for (int64_t i = threadIdx.x; i < m; i += NT) {
+            double c = hcov_cov_entry(mp, xs[r0 + i], ys[r0 + i], xj, yj, (r0 + i) == (c0 + js));
+            for (int l = 0; l < k; ++l) c -= U[i + m * l] * V[js + m * l];
+            double u = c / piv;
+            uk[i] = u;
+            su += u * u;
+            double vv = vk[i];
+            sv += vv * vv;
+            if (!used[i]) {
+                double aa = fabs(c);
+                if (vi_better(aa, i, bv, bi)) { bv = aa; bi = i; }
+            }
+        }
+        su = block_sum(su, red);
+        sv = block_sum(sv, red);
+        ValIdx nb = block_argmax(bv, bi, redv, redi);
+        ++k;
+        const double nn = sqrt(su) * sqrt(sv);
+        if (k == 1) n1 = nn;
+        else if (nn <= eps_aca * n1) break;
+        if (nb.i >= m || nb.v < 0.0) break;   // all rows used
+        istar = nb.i;
+    }
+    __syncthreads();
+    return k;
+}

@@ -1,0 +1,159 @@
+"""Host-side logic of libhcov (no GPU): symbol exports, cluster tree (A1) and block tree (A2)
+against an independent Python mirror of the rules (R5, R6), partition invariants."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1709_08625_b200 as H
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "hcov.h")).read()
+    names = set(re.findall(r"\b(hcov_[a-z_0-9]+)\s*\(", hdr))
+    assert len(names) >= 17
+    L = H.lib()
+    for nm in sorted(names):
+        assert hasattr(L, nm), nm
+    assert set(H._SIGS) == names
+
+
+def _mirror_tree(s, leaf=32):
+    """Python re-statement of A1: longest bbox axis (ties -> x), stable cardinality median,
+    left = ceil(m/2), uniform depth L = ceil(log2(n/32))."""
+    n = len(s)
+    L = 0
+    while (leaf << L) < n:
+        L += 1
+    ranges = [list(range(n))]
+    for _ in range(L):
+        nxt = []
+        for idx in ranges:
+            P = s[idx]
+            ext = P.max(0) - P.min(0)
+            ax = 0 if ext[0] >= ext[1] else 1
+            order = sorted(range(len(idx)), key=lambda k: (P[k, ax], k))
+            idx = [idx[k] for k in order]
+            m1 = (len(idx) + 1) // 2
+            nxt += [idx[:m1], idx[m1:]]
+        ranges = nxt
+    perm = []
+    for idx in ranges:
+        perm += idx + [-1] * (leaf - len(idx))
+    return L, np.array(perm, dtype=np.int64)
+
+
+def _mirror_blocks(s, perm, L, eta=2.0, leaf=32, dense_below=32):
+    npad = leaf << L
+    def box(l, c):
+        m = npad >> l
+        idx = perm[c * m:(c + 1) * m]
+        P = s[idx[idx >= 0]]
+        return P.min(0), P.max(0)
+    def adm(l, i, j):
+        (a0, a1), (b0, b1) = box(l, i), box(l, j)
+        gap = np.maximum(0, np.maximum(a0 - b1, b0 - a1))
+        d = math.hypot(*gap)
+        return eta > 0 and d > 0 and min(math.hypot(*(a1 - a0)), math.hypot(*(b1 - b0))) <= eta * d
+    out = set()
+    def rec(l, i, j, forced):
+        if i == j:
+            if l == L:
+                out.add((l, i, j, H.ND_T)); return
+            out.add((l, i, j, H.ND_H))
+            rec(l + 1, 2 * i, 2 * j, forced); rec(l + 1, 2 * i + 1, 2 * j, forced); rec(l + 1, 2 * i + 1, 2 * j + 1, forced)
+            return
+        a = (not forced) and adm(l, i, j)
+        if a and l < L and (npad >> l) > dense_below:
+            out.add((l, i, j, H.ND_R)); return
+        if l == L:
+            out.add((l, i, j, H.ND_T)); return
+        out.add((l, i, j, H.ND_H))
+        for x in (0, 1):
+            for y in (0, 1):
+                rec(l + 1, 2 * i + x, 2 * j + y, forced or a)
+    rec(0, 0, 0, False)
+    return out
+
+
+@pytest.mark.parametrize("n,seed,geom", [(1, 1, "u"), (31, 2, "u"), (33, 3, "u"), (500, 4, "u"),
+                                         (2000, 1001, "u"), (4096, 5, "c"), (1000, 6, "line")])
+def test_tree_and_blocks_match_mirror(n, seed, geom):
+    if geom == "u":
+        s = synth.uniform_points(n, seed)
+    elif geom == "c":
+        s = synth.clustered_points(n, seed, seed + 1, frac=0.2)
+    else:
+        s = synth.collinear_points(n, seed)
+    T = H.Tree(s)
+    info = T.info()
+    L, perm = _mirror_tree(s)
+    assert info["depth"] == L and info["n_pad"] == 32 << L
+    got = T.perm_i2e()
+    assert np.array_equal(got, perm)
+    real = got[got >= 0]
+    assert np.array_equal(np.sort(real), np.arange(n))       # bijection on the real points
+    assert np.all((got.reshape(-1, 32) >= 0).sum(1) <= 32)
+    blocks = {tuple(int(v) for v in b) for b in T.blocks()}
+    assert blocks == _mirror_blocks(s, perm, L)
+
+
+@pytest.mark.parametrize("eta,dense_below", [(2.0, 32), (2.0, 128), (0.0, 32), (0.7, 32)])
+def test_block_partition_covers_lower_triangle(eta, dense_below):
+    n = 3000
+    s = synth.uniform_points(n, 77)
+    T = H.Tree(s, eta=eta, dense_below=dense_below)
+    info = T.info()
+    L, npad = info["depth"], info["n_pad"]
+    b = T.blocks()
+    leaves = b[b[:, 3] != H.ND_H]
+    m = npad >> leaves[:, 0].astype(np.int64)
+    off = leaves[:, 1] != leaves[:, 2]
+    # lower + diagonal leaves mirrored cover I x I exactly once
+    assert int(np.sum(m[off] ** 2)) * 2 + int(np.sum(m[~off] ** 2)) == npad * npad
+    assert np.all(leaves[:, 1] >= leaves[:, 2])
+    assert np.all(leaves[~off, 0] == L)                        # diagonal leaves are 32x32 tiles
+    assert np.all(leaves[leaves[:, 3] == H.ND_T, 0] == L)
+    r = leaves[leaves[:, 3] == H.ND_R]
+    assert np.all((npad >> r[:, 0].astype(np.int64)) > dense_below)
+    if eta == 0.0:
+        assert len(r) == 0 and info["n_dense_tiles"] == (npad // 32) * (npad // 32 + 1) // 2
+    # no overlaps: paint a leaf-level occupancy grid
+    N = npad // 32
+    grid = np.zeros((N, N), dtype=np.int32)
+    for l, i, j, t in leaves:
+        sp = 1 << (L - l)
+        grid[i * sp:(i + 1) * sp, j * sp:(j + 1) * sp] += 1
+    assert np.array_equal(grid, np.tril(np.ones((N, N), dtype=np.int32)))
+
+
+def test_admissibility_is_symmetric_and_eta_monotone():
+    s = synth.uniform_points(4096, 9)
+    c1 = np.bincount(H.Tree(s, eta=1.0).blocks()[:, 3], minlength=3)
+    c2 = np.bincount(H.Tree(s, eta=2.0).blocks()[:, 3], minlength=3)
+    c4 = np.bincount(H.Tree(s, eta=4.0).blocks()[:, 3], minlength=3)
+    # larger eta admits coarser blocks -> fewer dense tiles
+    assert c1[H.ND_T] >= c2[H.ND_T] >= c4[H.ND_T]
+
+
+def test_invalid_inputs():
+    with pytest.raises(H.HcovError) as e:
+        H.Tree(np.zeros((0, 2)))
+    assert e.value.code == 2
+    bad = synth.uniform_points(10, 1)
+    bad[3, 1] = np.nan
+    with pytest.raises(H.HcovError) as e:
+        H.Tree(bad)
+    assert e.value.code == 1
+
+
+def test_schedule_depth_is_linear_in_leaves():
+    # critical path of the lazy column schedule: ~2 waves per diagonal leaf
+    for n in (2048, 16384):
+        info = H.Tree(synth.uniform_points(n, 3)).info()
+        assert info["n_waves"] <= 2.5 * info["n_leaves"] + 40
