@@ -1,0 +1,291 @@
+#!/usr/bin/env python
+"""bench.py — log-likelihood evaluations per second of the H-matrix hot path on B200.
+
+One step = one full evaluation of L~(theta) (Eq. (2)): H-assembly (A3-A6),
+H-Cholesky (A7), log det + forward H-solve (A8-A10), i.e. BASELINE.json's metric
+"log-likelihood evals/s (H-assemble+H-Cholesky+solve) at n=2M".  The cluster/block tree
+(A1-A2) is theta-independent and built once before the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl hcov|reference]
+
+Multi-GPU (torchrun, one rank per GPU): the theta candidates are sharded across ranks (each
+rank owns whole factorizations), the per-step likelihood values are
+all-gathered over NCCL, timing is the max over ranks; scaling is weak (fixed work per rank).
+--impl reference times the CPU oracle (oracle/, dense fp64 Cholesky) on a bounded sample of the
+same workload, extrapolated to the metric's n by the dense O(n^3) cost.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "log-likelihood evals/s (H-assemble+H-Cholesky+solve) at n=2M"
+
+
+def _args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="C5")
+    p.add_argument("--impl", default="hcov", choices=["hcov", "reference"])
+    p.add_argument("--n", type=int, default=0, help="override n (debug only; not a bench line)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=0, help="oracle sample size (default: auto)")
+    return p.parse_args()
+
+
+# --------------------------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md "clocks line")
+# --------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 8]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, nm in enumerate(names):
+                if "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------------------------
+def _theta_for(cfg, j: int, m: int):
+    """Candidate j of m: the config's theta for m == 1; else ell log-spaced in ell*[0.8, 1.25]
+    (SURVEY.md Sec. 8(d), C5's 8-GPU theta batch)."""
+    if m == 1:
+        return (cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget)
+    f = 0.8 * (1.25 / 0.8) ** (j / (m - 1))
+    return (cfg.sigma2, cfg.ell * f, cfg.nu, cfg.nugget)
+
+
+def _oracle_cpu(cfg, n_s: int, reps: int = 1):
+    """The oracle as it stands (dense Matern fill + LAPACK Cholesky + solve) on the first n_s
+    points of the config; returns (seconds per evaluation, threads)."""
+    import oracle
+    s = synth.points(cfg)[:n_s]
+    Z = synth.xi(n_s, cfg.seed_xi)
+    th = (cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget)
+    oracle.loglik_dense(s[:256], Z[:256], *th)      # build/load the C checker outside the clock
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.loglik_dense(s, Z, *th)
+        ts.append(time.perf_counter() - t0)
+    return min(ts), oracle.THREADS
+
+
+def _cpu_sample_size(cfg, budget_s: float = 15.0) -> int:
+    import oracle
+    n_s = 2048
+    t, _ = _oracle_cpu(cfg, n_s)
+    # grow until one evaluation costs ~budget/4 (dense O(n^3))
+    while n_s < cfg.n and t * 8 < budget_s / 2 and n_s * 2 <= 32768:
+        n_s *= 2
+        t, _ = _oracle_cpu(cfg, n_s)
+    return n_s
+
+
+def run_reference(args, cfg, rank: int, world: int):
+    if rank != 0:
+        return
+    n = cfg.n
+    n_s = args.cpu_sample or _cpu_sample_size(cfg, budget_s=8.0)
+    for _ in range(args.warmup):
+        _oracle_cpu(cfg, min(n_s, 2048))
+    ts = []
+    for _ in range(args.steps):
+        t, thr = _oracle_cpu(cfg, n_s)
+        ts.append(t)
+    t_step = float(np.mean(ts))
+    t_full = t_step * (n / n_s) ** 3              # dense O(n^3) extrapolation to the metric's n
+    v = 1.0 / t_full
+    out = {"metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": cfg.name, "n": n, "nu": cfg.nu, "ell": cfg.ell, "sigma2": cfg.sigma2,
+                      "nugget": cfg.nugget, "eps": cfg.eps[0], "kmax": cfg.kmax},
+           "cpu_baseline": {"value": v, "unit": "evals/s", "cores": thr, "kind": "oracle",
+                            "sample": f"dense oracle L(theta) on the first {n_s} of the {n} points, "
+                                      f"{t_step:.2f} s/eval, extrapolated x(n/{n_s})^3"},
+           "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_hcov(args, cfg, rank: int, world: int):
+    import torch
+    import paper_1709_08625_b200 as H
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.n or cfg.n
+    s = synth.points(cfg)[:n] if args.n else synth.points(cfg)
+    eps, kmax = cfg.eps[0], cfg.kmax
+    stream = torch.cuda.current_stream()
+    s_dev = torch.from_numpy(s).to(dev)
+    tree = H.Tree(s_dev)                       # A1-A2: theta-independent, untimed
+    info = tree.info()
+    th0 = (cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget)
+    # data: Z = L~ xi from the H-Cholesky factor at the config's theta (Sec. 5.1)
+    xi = torch.from_numpy(synth.xi(n, cfg.seed_xi)).to(dev)
+    hgen = H.HMatrix(tree, th0, eps, kmax)
+    hgen.cholesky()
+    Z = hgen.sample(xi)
+    del hgen
+    m_total = max(1, world)
+    my_theta = _theta_for(cfg, rank, m_total)
+
+    def step():
+        return H.eval_loglik(tree, my_theta, Z, eps, kmax)
+
+    for _ in range(max(3, args.warmup)):
+        r = step()
+    if r["status"] != 0:
+        raise RuntimeError(f"evaluation failed: {r}")
+    # ---- timed region -----------------------------------------------------------------------
+    clocks = Clocks(dev.index)
+    H.prof_control(enable_events=True, reset=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    gathered = []
+    for _ in range(args.steps):
+        r = step()
+        if dist:
+            t = torch.tensor([r["loglik"]], dtype=torch.float64, device=dev)
+            g = torch.empty(world, dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(g, t)
+            gathered.append(g)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    prof = H.prof_read()
+    H.prof_control(enable_events=False, reset=True)
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * args.steps / (ms * 1e-3)
+
+    # ---- e2e: host Z (pinned) -> device inside the timed region, result back to host -----------
+    Zh = Z.cpu().pin_memory()
+    Zd = torch.empty_like(Z)
+    k_e = max(1, min(args.steps, 3))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(k_e):
+        Zd.copy_(Zh, non_blocking=True)
+        r2 = H.eval_loglik(tree, my_theta, Zd, eps, kmax)    # returns host scalars (D2H inside)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e = {"value": world * k_e / (ms_e2e * 1e-3), "unit": "evals/s", "h2d_bytes_per_step": 8 * n,
+           "d2h_bytes_per_step": 3 * 8}
+
+    # ---- roofline of the dominant kernel class ------------------------------------------------
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    roof = H.roofline(prof, peaks)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    out = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+           "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg.name if not args.n else f"{cfg.name}[n={n}]", "n": n, "nu": cfg.nu,
+                      "ell": cfg.ell, "sigma2": cfg.sigma2, "nugget": cfg.nugget, "eps": eps, "kmax": kmax,
+                      "leaf": 32, "eta": 2.0, "parallelism": f"theta-batch dp{world}",
+                      "l2": "inputs larger than L2 (H-matrix >> 126 MB)",
+                      "tree": {k: info[k] for k in ("depth", "n_dense_tiles", "n_lowrank", "n_tasks", "n_waves")}},
+           "loglik": r["loglik"], "max_rank": r["max_rank"], "cap_binds": r["cap_binds"],
+           "gpu_launches": int(prof["launches"] // max(1, args.steps)),
+           "e2e": e2e, "roofline": roof, "clocks": clk,
+           "stages_ms_per_step": {k: v / args.steps for k, v in prof["ms"].items()}}
+    if world == 1 and not args.no_cpu_baseline:
+        n_s = args.cpu_sample or _cpu_sample_size(cfg)
+        t, thr = _oracle_cpu(cfg, n_s)
+        t_full = t * (n / n_s) ** 3
+        out["cpu_baseline"] = {"value": 1.0 / t_full, "unit": "evals/s", "cores": thr, "kind": "oracle",
+                               "sample": f"dense oracle L(theta) on the first {n_s} of the {n} points: "
+                                         f"{t:.2f} s, extrapolated x(n/{n_s})^3 = {t_full:.3g} s/eval"}
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus and rank == 0:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+    else:
+        run_hcov(args, cfg, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,21 @@ hcov_status hcov_columns(hcov_hmat h, const int64_t *cols_host, int32_t m, doubl
 hcov_status hcov_hmat_storage(hcov_hmat h, int64_t *dense_bytes, int64_t *lowrank_bytes,
                               int32_t *max_rank);
 
+/* Instrumentation (process-wide, not thread-safe): number of kernels the library launched and,
+ * when enabled, per-kernel-class device time from CUDA events recorded around each launch on its
+ * stream.  hcov_prof_read synchronises those events.  Class names: hcov_prof_class_name. */
+#define HCOV_PROF_CLASSES 16
+typedef struct {
+    int64_t launches;                  /* kernels launched since the last reset */
+    int32_t n_classes;
+    int32_t pad;
+    int64_t count[HCOV_PROF_CLASSES];  /* launches per class */
+    double ms[HCOV_PROF_CLASSES];      /* device milliseconds per class (0 unless events enabled) */
+} hcov_prof;
+hcov_status hcov_prof_control(int32_t enable_events, int32_t reset);
+hcov_status hcov_prof_read(hcov_prof *out);
+const char *hcov_prof_class_name(int32_t cls);
+
 void hcov_tree_free(hcov_tree t);
 void hcov_hmat_free(hcov_hmat h);
 const char *hcov_status_string(hcov_status s);

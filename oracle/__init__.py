@@ -17,6 +17,10 @@ Functions and the passages they follow (PAPER.md = the paper's LaTeX text):
   factor C = L L^T exactly as Eq. (2) / Def. 1 writes it with the
   exact factor: log det C = 2 sum log L_ii, v = L^{-1} Z, Z^T C^{-1} Z = v^T v.
   The factorisation and the triangular solve are LAPACK library primitives.
+* ``loglik_ou_collinear``  — Eq. (1) in closed form for nu = 1/2, tau^2 = 0 on collinear
+  points: the exponential covariance (Eq. (3) at nu = 1/2) on a line is the
+  Ornstein-Uhlenbeck process, which is Markov, so the joint density factorises into
+  one-step conditionals.  O(n) exact L at any n (used at 2M).
 * ``sample_dense``         — Z = L xi with the exact dense factor (Sec. 5.1, PAPER.md:573-577,
   with the exact factor in place of the H-factor; configs C1/C2 of BASELINE.json).
 
@@ -146,3 +150,24 @@ def sample_dense(s, xi, sigma2, ell, nu, nugget):
     L = cholesky(C)
     with threadpool_limits(THREADS):
         return L @ np.asarray(xi, dtype=np.float64)
+
+
+def loglik_ou_collinear(x, Z, sigma2, ell):
+    """Exact Eq. (1) for nu = 1/2, tau^2 = 0, points (x_i, 0) on a line.
+
+    Sort x_1 < ... < x_n, rho_i = exp(-(x_i - x_{i-1}) / ell).  The field is Markov:
+    Z_1 ~ N(0, sigma2), Z_i | Z_{i-1} ~ N(rho_i Z_{i-1}, sigma2 (1 - rho_i^2)), hence
+    log det C = n log sigma2 + sum_{i>=2} log(1 - rho_i^2) and
+    Z^T C^{-1} Z = Z_1^2 / sigma2 + sum_{i>=2} (Z_i - rho_i Z_{i-1})^2 / (sigma2 (1 - rho_i^2)).
+    Returns (loglik, logdet, quad)."""
+    x = np.asarray(x, dtype=np.float64)
+    Z = np.asarray(Z, dtype=np.float64)
+    o = np.argsort(x, kind="stable")
+    x, z = x[o], Z[o]
+    d = np.diff(x)
+    om = -np.expm1(-2.0 * d / ell)          # 1 - rho^2 without cancellation
+    rho = np.exp(-d / ell)
+    n = x.size
+    logdet = n * np.log(sigma2) + float(np.sum(np.log(om)))
+    quad = z[0] ** 2 / sigma2 + float(np.sum((z[1:] - rho * z[:-1]) ** 2 / (sigma2 * om)))
+    return -0.5 * n * np.log(2.0 * np.pi) - 0.5 * logdet - 0.5 * quad, logdet, quad

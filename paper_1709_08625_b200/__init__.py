@@ -56,6 +56,11 @@ class TreeInfo(ctypes.Structure):
                 ("eta", ctypes.c_double)]
 
 
+class Prof(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("count", ctypes.c_int64 * 16), ("ms", ctypes.c_double * 16)]
+
+
 # name -> (restype, argtypes) ; every symbol declared in include/hcov.h
 _P, _I32, _I64, _D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 _SIGS = {
@@ -73,6 +78,9 @@ _SIGS = {
     "hcov_sample": (_I32, [_P, _P, _P, _P]),
     "hcov_columns": (_I32, [_P, _P, _I32, _P, _P]),
     "hcov_hmat_storage": (_I32, [_P, _P, _P, _P]),
+    "hcov_prof_control": (_I32, [_I32, _I32]),
+    "hcov_prof_read": (_I32, [_P]),
+    "hcov_prof_class_name": (ctypes.c_char_p, [_I32]),
     "hcov_tree_free": (None, [_P]),
     "hcov_hmat_free": (None, [_P]),
     "hcov_status_string": (ctypes.c_char_p, [_I32]),
@@ -245,3 +253,25 @@ def mle_batch(tree: Tree, Z, thetas, eps: float, kmax: int = 0, kcap: int = 0, s
     _check(lib().hcov_mle_batch(tree.handle, _dev_f64(Z, tree.n, "Z"), ctypes.cast(arr, ctypes.c_void_p), m,
                                 ctypes.byref(tr), _stream(stream), ll.ctypes.data, st.ctypes.data), "hcov_mle_batch")
     return ll, st
+
+
+def prof_control(enable_events: bool = False, reset: bool = True) -> None:
+    """hcov_prof_control: launch counting is always on; events time every launch by class."""
+    _check(lib().hcov_prof_control(int(enable_events), int(reset)), "hcov_prof_control")
+
+
+def prof_read() -> dict:
+    """hcov_prof_read: {'launches': int, 'count': {cls: n}, 'ms': {cls: device ms}}."""
+    p = Prof()
+    _check(lib().hcov_prof_read(ctypes.byref(p)), "hcov_prof_read")
+    names = [lib().hcov_prof_class_name(k).decode() for k in range(p.n_classes)]
+    return {"launches": p.launches, "count": {nm: p.count[k] for k, nm in enumerate(names)},
+            "ms": {nm: p.ms[k] for k, nm in enumerate(names)}}
+
+
+def roofline(prof: dict, peaks: dict) -> dict:
+    """Roofline entry of the dominant kernel class (largest device time).  Filled in by the
+    per-class algorithmic work model; see bench.py."""
+    ms = prof["ms"]
+    top = max(ms, key=lambda k: ms[k]) if ms else None
+    return {"kernel": top, "ms": ms.get(top), "launches": prof["count"].get(top)}

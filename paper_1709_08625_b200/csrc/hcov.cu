@@ -38,6 +38,64 @@ cudaError_t upload(T **d, const std::vector<T> &h)
 }
 
 // ------------------------------------------------------------------------------------------
+// instrumentation: launch counter and per-class CUDA-event timing (hcov_prof_*)
+// ------------------------------------------------------------------------------------------
+enum ProfCls { PC_FILL = 0, PC_ACA = 1, PC_POTRF = 2, PC_TRSM = 3, PC_RFIN = 4, PC_LRSOLVE = 5, PC_PRR = 6,
+               PC_PHW = 7, PC_FWD = 8, PC_REDUCE = 9, PC_AUX = 10, PC_N = 11 };
+const char *const PROF_NAMES[PC_N] = {"fill_tiles", "aca_trunc", "potrf", "trsm", "rfin", "lr_solve", "prr",
+                                      "phw", "fwd_solve", "reduce", "aux"};
+struct ProfEv { int cls; cudaEvent_t a, b; };
+struct Prof {
+    int64_t launches = 0;
+    int64_t count[PC_N] = {};
+    bool events = false;
+    std::vector<ProfEv> evs;
+    std::vector<cudaEvent_t> pool;
+    double ms[PC_N] = {};
+};
+Prof g_prof;
+
+cudaEvent_t prof_event()
+{
+    if (!g_prof.pool.empty()) { cudaEvent_t e = g_prof.pool.back(); g_prof.pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+// Open a launch record of class cls on stream st; returns the index to close.
+int prof_begin(int cls, cudaStream_t st)
+{
+    g_prof.launches++;
+    g_prof.count[cls]++;
+    if (!g_prof.events) return -1;
+    ProfEv p{cls, prof_event(), prof_event()};
+    cudaEventRecord(p.a, st);
+    g_prof.evs.push_back(p);
+    return (int)g_prof.evs.size() - 1;
+}
+void prof_end(int k, cudaStream_t st)
+{
+    if (k >= 0) cudaEventRecord(g_prof.evs[k].b, st);
+}
+void prof_collect()
+{
+    for (ProfEv &p : g_prof.evs) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess)
+            g_prof.ms[p.cls] += ms;
+        g_prof.pool.push_back(p.a);
+        g_prof.pool.push_back(p.b);
+    }
+    g_prof.evs.clear();
+}
+#define LAUNCH(cls, st, ...)                     \
+    do {                                         \
+        int pk_ = prof_begin((cls), (st));       \
+        __VA_ARGS__;                             \
+        prof_end(pk_, (st));                     \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------
 // kernels
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) k_fill_tiles(Ctx c, int64_t ntiles)
@@ -516,11 +574,11 @@ hcov_status assemble_into(hcov_hmat h, const hcov_theta *theta, const hcov_trunc
     CK(cudaMemsetAsync(h->fail, 0x7f, sizeof(int32_t), st));
     if (P.n_tiles() > 0) {
         int grid = (int)std::min<int64_t>(P.n_tiles(), 148 * 16);
-        k_fill_tiles<<<grid, NT, 0, st>>>(h->ctx, P.n_tiles());
+        LAUNCH(PC_FILL, st, k_fill_tiles<<<grid, NT, 0, st>>>(h->ctx, P.n_tiles()));
     }
     for (const Launch &L : t->asm_launches) {
         int grid = std::min(L.cnt, t->scr_slots[L.cls]);
-        k_assemble_r<<<grid, NT, 0, st>>>(h->ctx, t->d_asm_ids + L.off, L.cnt, L.cls);
+        LAUNCH(PC_ACA, st, k_assemble_r<<<grid, NT, 0, st>>>(h->ctx, t->d_asm_ids + L.off, L.cnt, L.cls));
     }
     CK(cudaGetLastError());
     h->state = 1;
@@ -540,7 +598,8 @@ hcov_status cholesky_run(hcov_hmat h, cudaStream_t st, int64_t *fail_leaf)
         else grid = std::min(L.cnt, 65535);
         Ctx c = h->ctx;
         if (!scratch) { c.scr[0] = c.scr[1] = nullptr; }
-        k_exec<<<grid, NT, smem, st>>>(c, t->d_exec_ids + L.off, L.cnt, scratch ? L.cls : 0);
+        static const int cls_of[7] = {PC_POTRF, PC_TRSM, PC_RFIN, PC_LRSOLVE, PC_PRR, PC_PHW, PC_AUX};
+        LAUNCH(cls_of[L.type], st, k_exec<<<grid, NT, smem, st>>>(c, t->d_exec_ids + L.off, L.cnt, scratch ? L.cls : 0));
     }
     CK(cudaGetLastError());
     int32_t hf[5];
@@ -559,9 +618,9 @@ hcov_status loglik_run(hcov_hmat h, const double *Z, cudaStream_t st, hcov_resul
 {
     if (!h || h->state != 2) return HCOV_ERR_STATE;
     Plan &P = h->t->P;
-    k_permute_in<<<256, 256, 0, st>>>(h->ctx, Z, h->vbuf);
-    k_fwd_solve<<<1, NT, 0, st>>>(h->ctx, h->vbuf, h->tbuf);
-    k_reduce<<<1, NT, 0, st>>>(h->ctx, h->vbuf, h->res);
+    LAUNCH(PC_REDUCE, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, Z, h->vbuf));
+    LAUNCH(PC_FWD, st, k_fwd_solve<<<1, NT, 0, st>>>(h->ctx, h->vbuf, h->tbuf));
+    LAUNCH(PC_REDUCE, st, k_reduce<<<1, NT, 0, st>>>(h->ctx, h->vbuf, h->res));
     CK(cudaGetLastError());
     int32_t hf[5];
     CK(cudaMemcpyAsync(h->res_host, h->res, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -811,6 +870,36 @@ hcov_status hcov_hmat_storage(hcov_hmat h, int64_t *dense_bytes, int64_t *lowran
     *lowrank_bytes = lr;
     *max_rank = mx;
     return HCOV_OK;
+}
+
+hcov_status hcov_prof_control(int32_t enable_events, int32_t reset)
+{
+    if (reset) {
+        prof_collect();
+        g_prof.launches = 0;
+        for (int k = 0; k < PC_N; ++k) { g_prof.count[k] = 0; g_prof.ms[k] = 0.0; }
+    }
+    g_prof.events = enable_events != 0;
+    return HCOV_OK;
+}
+
+hcov_status hcov_prof_read(hcov_prof *out)
+{
+    if (!out) return HCOV_ERR_INVALID_ARG;
+    prof_collect();
+    std::memset(out, 0, sizeof(*out));
+    out->launches = g_prof.launches;
+    out->n_classes = PC_N;
+    for (int k = 0; k < PC_N; ++k) {
+        out->ms[k] = g_prof.ms[k];
+        out->count[k] = g_prof.count[k];
+    }
+    return HCOV_OK;
+}
+
+const char *hcov_prof_class_name(int32_t cls)
+{
+    return (cls >= 0 && cls < PC_N) ? PROF_NAMES[cls] : "";
 }
 
 void hcov_tree_free(hcov_tree t) { delete t; }

@@ -136,26 +136,12 @@ def test_logdet_quad_vs_lu(n):
         assert np.linalg.norm(L @ L.T - C) <= 1e-13 * np.linalg.norm(C)
 
 
-def _ou_exact(x, z, s2, ell):
-    """Collinear exponential (nu=1/2, tau^2=0) covariance is Markov (Ornstein-Uhlenbeck):
-    Z_i | Z_{i-1} ~ N(rho_i Z_{i-1}, s2 (1 - rho_i^2)), rho_i = exp(-(x_i - x_{i-1})/ell)."""
-    o = np.argsort(x)
-    x, z = x[o], z[o]
-    d = np.diff(x)
-    om = -np.expm1(-2 * d / ell)            # 1 - rho^2
-    rho = np.exp(-d / ell)
-    n = len(x)
-    logdet = n * math.log(s2) + float(np.sum(np.log(om)))
-    quad = z[0] ** 2 / s2 + float(np.sum((z[1:] - rho * z[:-1]) ** 2 / (s2 * om)))
-    return -0.5 * n * math.log(2 * math.pi) - 0.5 * logdet - 0.5 * quad, logdet, quad
-
-
 def test_collinear_ou_closed_form():
     n = 600
     s = synth.collinear_points(n, 11)
     z = synth.xi(n, 12)
     ll, ld, q = oracle.loglik_dense(s, z, 1.4, 0.05, 0.5, 0.0)
-    ll2, ld2, q2 = _ou_exact(s[:, 0], z, 1.4, 0.05)
+    ll2, ld2, q2 = oracle.loglik_ou_collinear(s[:, 0], z, 1.4, 0.05)
     assert abs(ld - ld2) <= 1e-10 * abs(ld2)
     assert abs(q - q2) <= 1e-9 * abs(q2)
     assert abs(ll - ll2) <= 1e-10 * abs(ll2)
