@@ -78,7 +78,7 @@ typedef struct {
     int64_t n_leaves;
     int64_t n_dense_tiles;  /* 32x32 tiles of the lower triangle incl. diagonal */
     int64_t n_lowrank;      /* admissible low-rank blocks (lower triangle) */
-    int64_t n_tasks, n_waves;
+    int64_t n_tasks, n_waves;   /* n_waves: longest dependency chain of the task DAG (tasks) */
     double eta;
 } hcov_tree_info;
 
@@ -100,6 +100,10 @@ hcov_status hcov_tree_get_info(hcov_tree t, hcov_tree_info *info);
  * (0 = inadmissible/subdivided, 1 = low-rank leaf, 2 = dense 32x32 leaf).  With out4 == NULL
  * only *count is set; otherwise cap >= *count is required. */
 hcov_status hcov_tree_blocks(hcov_tree t, int32_t *out4, int64_t cap, int64_t *count);
+/* Schedule introspection (diagnostics): 6 int32 per task of the DAG in generation order:
+ * type (0 FILL, 1 ACA, 2 TAPP, 3 POTRF, 4 TRSM, 5 RAPP, 6 SEG, 7 PROJ, 8 PRR, 9 PHWP, 10 PHWR,
+ * 11 NOP), phase (0 assembly, 1 H-Cholesky, 2 forward solve), and the task arguments a, b, c, d. */
+hcov_status hcov_tree_tasks(hcov_tree t, int32_t *out6, int64_t cap, int64_t *count);
 /* Cluster bounding boxes, 4 doubles per cluster heap id (2^l - 1 + c): lo_x, lo_y, hi_x, hi_y. */
 hcov_status hcov_tree_bbox(hcov_tree t, double *bb, int64_t cap);
 /* perm_i2e: n_pad int64 (host); entry k = external index of internal position k, -1 for phantom rows. */
@@ -140,20 +144,26 @@ hcov_status hcov_columns(hcov_hmat h, const int64_t *cols_host, int32_t m, doubl
 hcov_status hcov_hmat_storage(hcov_hmat h, int64_t *dense_bytes, int64_t *lowrank_bytes,
                               int32_t *max_rank);
 
-/* Instrumentation (process-wide, not thread-safe): number of kernels the library launched and,
- * when enabled, per-kernel-class device time from CUDA events recorded around each launch on its
- * stream.  hcov_prof_read synchronises those events.  Class names: hcov_prof_class_name. */
+/* Instrumentation (process-wide, not thread-safe).  launches/count: kernels the library launched
+ * (always counted).  With events enabled: ms = device time per launch class from CUDA events
+ * recorded around each launch on its stream, and the engine's per-task-type busy time (sum over
+ * CTAs of globaltimer spans), task counts and algorithmic flop per flop class
+ * (0 assembly [kernel evaluations], 1 tile updates, 2 truncation, 3 solves, 4 products).
+ * hcov_prof_read synchronises those events.  Names: hcov_prof_class_name / hcov_prof_task_name. */
 #define HCOV_PROF_CLASSES 16
 typedef struct {
     int64_t launches;                  /* kernels launched since the last reset */
-    int32_t n_classes;
-    int32_t pad;
+    int32_t n_classes, n_task_types;
     int64_t count[HCOV_PROF_CLASSES];  /* launches per class */
     double ms[HCOV_PROF_CLASSES];      /* device milliseconds per class (0 unless events enabled) */
+    double task_busy_ms[HCOV_PROF_CLASSES];
+    double task_count[HCOV_PROF_CLASSES];
+    double flop[8];
 } hcov_prof;
 hcov_status hcov_prof_control(int32_t enable_events, int32_t reset);
 hcov_status hcov_prof_read(hcov_prof *out);
 const char *hcov_prof_class_name(int32_t cls);
+const char *hcov_prof_task_name(int32_t type);
 
 void hcov_tree_free(hcov_tree t);
 void hcov_hmat_free(hcov_hmat h);

@@ -57,8 +57,10 @@ class TreeInfo(ctypes.Structure):
 
 
 class Prof(ctypes.Structure):
-    _fields_ = [("launches", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("pad", ctypes.c_int32),
-                ("count", ctypes.c_int64 * 16), ("ms", ctypes.c_double * 16)]
+    _fields_ = [("launches", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("n_task_types", ctypes.c_int32),
+                ("count", ctypes.c_int64 * 16), ("ms", ctypes.c_double * 16),
+                ("task_busy_ms", ctypes.c_double * 16), ("task_count", ctypes.c_double * 16),
+                ("flop", ctypes.c_double * 8)]
 
 
 # name -> (restype, argtypes) ; every symbol declared in include/hcov.h
@@ -69,6 +71,7 @@ _SIGS = {
     "hcov_tree_get_info": (_I32, [_P, _P]),
     "hcov_tree_blocks": (_I32, [_P, _P, _I64, _P]),
     "hcov_tree_bbox": (_I32, [_P, _P, _I64]),
+    "hcov_tree_tasks": (_I32, [_P, _P, _I64, _P]),
     "hcov_tree_perm": (_I32, [_P, _P]),
     "hcov_assemble": (_I32, [_P, _P, _P, _P, _P]),
     "hcov_cholesky": (_I32, [_P, _P, _P]),
@@ -81,6 +84,7 @@ _SIGS = {
     "hcov_prof_control": (_I32, [_I32, _I32]),
     "hcov_prof_read": (_I32, [_P]),
     "hcov_prof_class_name": (ctypes.c_char_p, [_I32]),
+    "hcov_prof_task_name": (ctypes.c_char_p, [_I32]),
     "hcov_tree_free": (None, [_P]),
     "hcov_hmat_free": (None, [_P]),
     "hcov_status_string": (ctypes.c_char_p, [_I32]),
@@ -166,6 +170,14 @@ class Tree:
         _check(lib().hcov_tree_blocks(self._h, None, 0, ctypes.byref(cnt)), "hcov_tree_blocks")
         out = np.empty((cnt.value, 4), dtype=np.int32)
         _check(lib().hcov_tree_blocks(self._h, out.ctypes.data, cnt.value, ctypes.byref(cnt)), "hcov_tree_blocks")
+        return out
+
+    def tasks(self) -> np.ndarray:
+        """hcov_tree_tasks: (n_tasks, 6) int32 = type, phase, a, b, c, d."""
+        cnt = ctypes.c_int64()
+        _check(lib().hcov_tree_tasks(self._h, None, 0, ctypes.byref(cnt)), "hcov_tree_tasks")
+        out = np.empty((cnt.value, 6), dtype=np.int32)
+        _check(lib().hcov_tree_tasks(self._h, out.ctypes.data, cnt.value, ctypes.byref(cnt)), "hcov_tree_tasks")
         return out
 
     def bbox(self) -> np.ndarray:
@@ -261,12 +273,20 @@ def prof_control(enable_events: bool = False, reset: bool = True) -> None:
 
 
 def prof_read() -> dict:
-    """hcov_prof_read: {'launches': int, 'count': {cls: n}, 'ms': {cls: device ms}}."""
+    """hcov_prof_read: launches, per-class device ms, engine busy ms / counts per task type,
+    algorithmic flop per flop class."""
     p = Prof()
     _check(lib().hcov_prof_read(ctypes.byref(p)), "hcov_prof_read")
     names = [lib().hcov_prof_class_name(k).decode() for k in range(p.n_classes)]
+    tnames = [lib().hcov_prof_task_name(k).decode() for k in range(p.n_task_types)]
     return {"launches": p.launches, "count": {nm: p.count[k] for k, nm in enumerate(names)},
-            "ms": {nm: p.ms[k] for k, nm in enumerate(names)}}
+            "ms": {nm: p.ms[k] for k, nm in enumerate(names)},
+            "task_busy_ms": {nm: p.task_busy_ms[k] for k, nm in enumerate(tnames)},
+            "task_count": {nm: int(p.task_count[k]) for k, nm in enumerate(tnames)},
+            "flop": {nm: p.flop[k] for k, nm in enumerate(FLOP_CLASSES)}}
+
+
+FLOP_CLASSES = ["assembly_evals", "tile", "truncation", "solve", "products"]
 
 
 def roofline(prof: dict, peaks: dict) -> dict:

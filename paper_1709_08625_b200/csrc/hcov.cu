@@ -1,17 +1,22 @@
-// libhcov: C ABI (include/hcov.h) + kernels + wave executor.
+// libhcov: C ABI (include/hcov.h), the persistent DAG engine and its auxiliary kernels.
+//
+// One evaluation of L~(theta) (hcov_eval) is: a reset kernel, the permutation of Z, ONE
+// persistent engine launch that executes the whole task DAG of the plan (assembly A3-A6,
+// H-Cholesky A7, forward H-solve A9; plan.cpp), and a fixed-order reduction (A8, A10).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
 #include <vector>
 
 #include "../../include/hcov.h"
+#include "engine.cuh"
 #include "plan.h"
-#include "tasks.cuh"
 
 namespace {
 
@@ -38,12 +43,12 @@ cudaError_t upload(T **d, const std::vector<T> &h)
 }
 
 // ------------------------------------------------------------------------------------------
-// instrumentation: launch counter and per-class CUDA-event timing (hcov_prof_*)
+// instrumentation: launch counter, per-class CUDA-event timing, engine counters (hcov_prof_*)
 // ------------------------------------------------------------------------------------------
-enum ProfCls { PC_FILL = 0, PC_ACA = 1, PC_POTRF = 2, PC_TRSM = 3, PC_RFIN = 4, PC_LRSOLVE = 5, PC_PRR = 6,
-               PC_PHW = 7, PC_FWD = 8, PC_REDUCE = 9, PC_AUX = 10, PC_N = 11 };
-const char *const PROF_NAMES[PC_N] = {"fill_tiles", "aca_trunc", "potrf", "trsm", "rfin", "lr_solve", "prr",
-                                      "phw", "fwd_solve", "reduce", "aux"};
+enum ProfCls { PC_ENGINE = 0, PC_RESET = 1, PC_PERM = 2, PC_REDUCE = 3, PC_AUX = 4, PC_N = 5 };
+const char *const PROF_NAMES[PC_N] = {"engine", "reset", "permute", "reduce", "aux"};
+const char *const TASK_NAMES[TK_NTYPES] = {"fill", "aca", "tapp", "potrf", "trsm", "rapp",
+                                           "seg", "proj", "prr", "phwp", "phwr", "nop"};
 struct ProfEv { int cls; cudaEvent_t a, b; };
 struct Prof {
     int64_t launches = 0;
@@ -52,6 +57,9 @@ struct Prof {
     std::vector<ProfEv> evs;
     std::vector<cudaEvent_t> pool;
     double ms[PC_N] = {};
+    double busy_ns[TK_NTYPES] = {};
+    double tasks[TK_NTYPES] = {};
+    double flop[FC_N] = {};
 };
 Prof g_prof;
 
@@ -62,7 +70,6 @@ cudaEvent_t prof_event()
     cudaEventCreate(&e);
     return e;
 }
-// Open a launch record of class cls on stream st; returns the index to close.
 int prof_begin(int cls, cudaStream_t st)
 {
     g_prof.launches++;
@@ -96,59 +103,136 @@ void prof_collect()
     } while (0)
 
 // ------------------------------------------------------------------------------------------
-// kernels
+// engine
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_fill_tiles(Ctx c, int64_t ntiles)
+struct EngineStats {
+    unsigned long long busy_ns[TK_NTYPES];
+    unsigned long long tasks[TK_NTYPES];
+    double flop[FC_N];
+};
+
+__device__ __forceinline__ unsigned long long gtimer()
 {
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const DNode x = c.nodes[c.tile_node[t]];
-        const int64_t r0 = (int64_t)x.i * HCOV_LEAF, c0 = (int64_t)x.j * HCOV_LEAF;
-        double *T = c.tiles + t * HCOV_TILE;
-        for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
-            int i = e & 31, j = e >> 5;
-            int64_t a = r0 + i, b = c0 + j;
-            T[e] = hcov_cov_entry(c.mp, c.xs[a], c.ys[a], c.xs[b], c.ys[b], a == b);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ int ld_volatile(const int32_t *p) { return *(volatile const int32_t *)p; }
+
+__device__ __forceinline__ void push_ready(const Ctx &c, int32_t s)
+{
+    const int q = c.tasks[s].qcls;
+    const uint32_t pos = atomicAdd(c.qctl + 2 + q, 1u);
+    atomicExch(c.queue[q] + pos, s);
+}
+
+// Release the successors of task t (all threads of the CTA; NOP joins complete inline).
+__device__ void release(const Ctx &c, int32_t t, int mask, const int8_t *phase)
+{
+    const int b = c.succ_off[t], e = c.succ_off[t + 1];
+    for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
+        int32_t s = c.succ[k];
+        if (!(mask & (1 << phase[s]))) continue;
+        if (atomicSub(c.indeg + s, 1) != 1) continue;
+        int32_t stack[24];
+        int sp = 0;
+        stack[sp++] = s;
+        while (sp > 0) {
+            int32_t u = stack[--sp];
+            if (c.tasks[u].type != TK_NOP) { push_ready(c, u); continue; }
+            __threadfence();
+            for (int z = c.succ_off[u]; z < c.succ_off[u + 1]; ++z) {
+                int32_t v = c.succ[z];
+                if (!(mask & (1 << phase[v]))) continue;
+                if (atomicSub(c.indeg + v, 1) == 1) {
+                    if (sp < 24) stack[sp++] = v;
+                    else push_ready(c, v);
+                }
+            }
         }
     }
 }
 
-__global__ void __launch_bounds__(NT) k_assemble_r(Ctx c, const int32_t *list, int cnt, int cls)
-{
-    __shared__ double red[NWARP], redv[NWARP];
-    __shared__ int64_t redi[NWARP];
-    double *scr = c.scr[cls] + c.scr_stride[cls] * blockIdx.x;
-    for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
-        const int r = list[q];
-        const DRBlk b = c.rblk[r];
-        const int64_t m = b.m;
-        const int K = aca_kmax(m, c.kcap);
-        CompressWs w = make_ws(scr, m, K);
-        uint8_t *used = (uint8_t *)(w.ord + K + 2);
-        int k = aca_partial(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, K, 0.1 * c.eps, used, red, redv, redi);
-        int cb = 0, of = 0;
-        int rk = compress(w, m, k, c.eps, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m, &cb, &of, red);
-        record_rank(c, r, rk, cb, of);
-    }
-}
-
-__global__ void __launch_bounds__(NT) k_exec(Ctx c, const int32_t *ids, int cnt, int cls)
+__global__ void __launch_bounds__(NT) k_engine(Ctx c, int mask, const int8_t *phase, EngineStats *stats)
 {
     extern __shared__ double smem[];
     __shared__ double red[NWARP], redv[NWARP];
     __shared__ int64_t redi[NWARP];
-    double *scr = c.scr[cls] ? c.scr[cls] + c.scr_stride[cls] * blockIdx.x : nullptr;
-    for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
-        const DTask tk = c.tasks[ids[q]];
-        switch (tk.type) {
-        case TK_POTRF: task_potrf(c, tk, smem); break;
-        case TK_TRSM: task_trsm(c, tk, smem); break;
-        case TK_RFIN: task_rfin(c, tk, scr, red, redv, redi); break;
-        case TK_SOLVE: task_solve(c, tk, scr, smem); break;
-        case TK_PRR: task_prr(c, tk); break;
-        case TK_PHW: task_phw(c, tk, smem, smem + HCOV_TILE); break;
-        default: break;
+    __shared__ int32_t s_task;
+    const int q = (blockIdx.x < c.nbig) ? 1 : 0;
+    double *scr = q ? c.bscr + (int64_t)blockIdx.x * c.bscr_stride
+                    : c.scr + (int64_t)(blockIdx.x - c.nbig) * c.scr_stride;
+    double fl[FC_N] = {0, 0, 0, 0, 0};
+    unsigned long long busy[TK_NTYPES] = {}, cnt[TK_NTYPES] = {};
+    while (true) {
+        if (threadIdx.x == 0) {
+            int32_t t = -1;
+            const uint32_t pos = atomicAdd(c.qctl + q, 1u);
+            if (pos < (uint32_t)c.nq[q]) {
+                const unsigned long long t0 = gtimer();
+                unsigned ns = 32;
+                while ((t = ld_volatile(c.queue[q] + pos)) < 0) {
+                    if (ld_volatile((const int32_t *)c.qctl + 4)) { t = -1; break; }
+                    __nanosleep(ns);
+                    if (ns < 256) ns <<= 1;
+                    if (gtimer() - t0 > c.timeout_ns) { atomicExch(c.qctl + 4, 1u); t = -1; break; }
+                }
+                __threadfence();
+            }
+            s_task = t;
         }
         __syncthreads();
+        const int32_t t = s_task;
+        if (t < 0) break;
+        const DTask tk = c.tasks[t];
+        const unsigned long long t0 = gtimer();
+        switch (tk.type) {
+        case TK_FILL: task_fill(c, tk, fl[FC_ASM]); break;
+        case TK_ACA: task_aca(c, tk, scr, red, redv, redi, fl[FC_ASM], fl[FC_TRUNC]); break;
+        case TK_TAPP:
+        case TK_POTRF:
+        case TK_TRSM: task_tile(c, tk, smem, fl[FC_TILE]); break;
+        case TK_RAPP: task_rapp(c, tk, scr, red, redv, redi, fl[FC_TRUNC]); break;
+        case TK_SEG: task_seg(c, tk, smem, fl[FC_SOLVE]); break;
+        case TK_PROJ: task_proj(c, tk, smem, fl[FC_SOLVE]); break;
+        case TK_PRR: task_prr(c, tk, fl[FC_PROD]); break;
+        case TK_PHWP: task_phwp(c, tk, fl[FC_PROD]); break;
+        case TK_PHWR: task_phwr(c, tk, smem, fl[FC_PROD]); break;
+        default: break;
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            busy[tk.type] += gtimer() - t0;
+            cnt[tk.type] += 1;
+        }
+        release(c, t, mask, phase);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && stats) {
+        for (int k = 0; k < TK_NTYPES; ++k) {
+            if (cnt[k]) {
+                atomicAdd(stats->busy_ns + k, busy[k]);
+                atomicAdd(stats->tasks + k, cnt[k]);
+            }
+        }
+        for (int k = 0; k < FC_N; ++k)
+            if (fl[k] != 0.0) atomicAdd(stats->flop + k, fl[k]);
+    }
+}
+
+__global__ void k_reset(Ctx c, const int32_t *indeg_mode, int64_t ntasks, const int32_t *roots0, int32_t nr0,
+                        const int32_t *roots1, int32_t nr1, int64_t qcap0, int64_t qcap1)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int64_t k = tid; k < ntasks; k += stride) c.indeg[k] = indeg_mode[k];
+    for (int64_t k = tid; k < qcap0; k += stride) c.queue[0][k] = (k < nr0) ? roots0[k] : -1;
+    for (int64_t k = tid; k < qcap1; k += stride) c.queue[1][k] = (k < nr1) ? roots1[k] : -1;
+    if (tid == 0) {
+        c.qctl[0] = 0; c.qctl[1] = 0;
+        c.qctl[2] = (uint32_t)nr0; c.qctl[3] = (uint32_t)nr1;
+        c.qctl[4] = 0;
     }
 }
 
@@ -167,24 +251,19 @@ __global__ void k_permute_out(Ctx c, const double *y, double *Zext)
     }
 }
 
-// Forward solve v = L^{-1} y over the whole matrix (root program), one CTA.
-__global__ void __launch_bounds__(NT) k_fwd_solve(Ctx c, double *y, double *tscr)
-{
-    __shared__ double smL[HCOV_TILE];
-    run_solve_program(c, 0, 0, c.n_pad, y, 1, tscr, smL);
-}
-
 // out[0] = log det, out[1] = quad, out[2] = min pivot (fixed-order reductions, one CTA)
-__global__ void __launch_bounds__(NT) k_reduce(Ctx c, const double *v, double *out)
+__global__ void __launch_bounds__(NT) k_reduce(Ctx c, double *out)
 {
     __shared__ double red[NWARP];
+    __shared__ double mred[NT];
     double ld = 0.0, q = 0.0, mp = INFINITY;
-    for (int64_t k = threadIdx.x; k < c.n_leaves; k += NT) { ld += c.logdet_part[k]; mp = fmin(mp, c.minpiv_part[k]); }
-    for (int64_t k = threadIdx.x; k < c.n_pad; k += NT) q += v[k] * v[k];
+    for (int64_t k = threadIdx.x; k < c.n_leaves; k += NT) {
+        ld += c.logdet_part[k];
+        q += c.quad_part[k];
+        mp = fmin(mp, c.minpiv_part[k]);
+    }
     ld = block_sum(ld, red);
     q = block_sum(q, red);
-    // min
-    __shared__ double mred[NT];
     mred[threadIdx.x] = mp;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -212,14 +291,15 @@ __global__ void __launch_bounds__(NT) k_sample_t(Ctx c, const double *x, double 
         }
     }
 }
-// y_seg = sum over the row's blocks (T: tile x_cols; R: U[seg rows] t_b)
-__global__ void __launch_bounds__(32) k_sample_rows(Ctx c, const double *x, const double *t, double *y)
+// y_seg = sum over the row's lower-triangular leaves (T: tile x_cols; R: U[seg rows] t_b)
+__global__ void __launch_bounds__(32) k_sample_rows(Ctx c, const int32_t *row_off, const int32_t *row_nodes,
+                                                    const double *x, const double *t, double *y)
 {
     for (int64_t seg = blockIdx.x; seg < c.n_leaves; seg += gridDim.x) {
         const int i = threadIdx.x;
         double s = 0.0;
-        for (int k = c.row_off[seg]; k < c.row_off[seg + 1]; ++k) {
-            const DNode nd = c.nodes[c.row_nodes[k]];
+        for (int k = row_off[seg]; k < row_off[seg + 1]; ++k) {
+            const DNode nd = c.nodes[row_nodes[k]];
             if (nd.type == ND_T) {
                 const double *T = c.tiles + (int64_t)nd.idx * HCOV_TILE;
                 const int64_t c0 = (int64_t)nd.j * HCOV_LEAF;
@@ -236,9 +316,9 @@ __global__ void __launch_bounds__(32) k_sample_rows(Ctx c, const double *x, cons
     }
 }
 
-// hcov_columns: out (n_pad x m internal rows) for internal columns pc[k].
-__global__ void __launch_bounds__(NT) k_columns(Ctx c, const int32_t *leafnodes, int nleafnodes, const int64_t *pc, int mcols,
-                                                double *out)
+// hcov_columns: out (n_pad x m internal rows) for internal columns pc[k] of the assembled C~.
+__global__ void __launch_bounds__(NT) k_columns(Ctx c, const int32_t *leafnodes, int nleafnodes, const int64_t *pc,
+                                                int mcols, double *out)
 {
     for (int q = blockIdx.x; q < nleafnodes; q += gridDim.x) {
         const DNode nd = c.nodes[leafnodes[q]];
@@ -247,7 +327,7 @@ __global__ void __launch_bounds__(NT) k_columns(Ctx c, const int32_t *leafnodes,
         for (int k = 0; k < mcols; ++k) {
             const int64_t p = pc[k];
             double *o = out + c.n_pad * (int64_t)k;
-            if (p >= c0 && p < c0 + mb) {   // column part: rows r0..r0+mb
+            if (p >= c0 && p < c0 + mb) {
                 const int64_t jj = p - c0;
                 for (int64_t i = threadIdx.x; i < mb; i += NT) {
                     double v;
@@ -261,7 +341,7 @@ __global__ void __launch_bounds__(NT) k_columns(Ctx c, const int32_t *leafnodes,
                     o[r0 + i] = v;
                 }
             }
-            if (nd.i != nd.j && p >= r0 && p < r0 + mb) {   // transposed part: rows c0..c0+mb
+            if (nd.i != nd.j && p >= r0 && p < r0 + mb) {
                 const int64_t ii = p - r0;
                 for (int64_t j = threadIdx.x; j < mb; j += NT) {
                     double v;
@@ -293,41 +373,35 @@ __global__ void k_columns_perm(Ctx c, const double *in, int mcols, double *out)
 // ------------------------------------------------------------------------------------------
 // handles
 // ------------------------------------------------------------------------------------------
-struct Launch {
-    int32_t type, cls, off, cnt;
-};
-
 struct hcov_tree_s {
     Plan P;
     bool uploaded = false;
-    // device plan arrays
     DNode *d_nodes = nullptr;
-    int32_t *d_children = nullptr;
-    DTerm *d_terms = nullptr;
-    DTask *d_tasks = nullptr;
-    DRBlk *d_rblk = nullptr;
     int32_t *d_tile_node = nullptr;
-    DPhw *d_phw = nullptr;
-    int32_t *d_phw_part = nullptr, *d_hleaf = nullptr, *d_col_r_off = nullptr, *d_col_r = nullptr;
-    DOp *d_ops = nullptr;
-    int32_t *d_op_beg = nullptr, *d_op_end = nullptr;
+    DRBlk *d_rblk = nullptr;
+    DTerm *d_terms = nullptr;
+    int32_t *d_xterm = nullptr;
     int64_t *d_fac_row0 = nullptr;
     int32_t *d_fac_nrows = nullptr, *d_fac_rank_src = nullptr;
     int64_t *d_fac_off = nullptr;
     int8_t *d_fac_pool = nullptr;
-    int32_t *d_row_off = nullptr, *d_row_nodes = nullptr;
+    DSolve *d_solves = nullptr;
+    int32_t *d_solve_rhs = nullptr;
+    DSlot *d_slots = nullptr;
+    DCtr *d_ctr = nullptr;
+    DPhw *d_phw = nullptr;
+    int32_t *d_col_r = nullptr;
+    DTask *d_tasks = nullptr;
+    int8_t *d_phase = nullptr;
+    int32_t *d_succ_off = nullptr, *d_succ = nullptr;
+    int32_t *d_indeg[4] = {nullptr, nullptr, nullptr, nullptr};
+    int32_t *d_roots[4][2] = {};
+    int32_t *d_diag_tile = nullptr;
     double *d_xs = nullptr, *d_ys = nullptr;
     int64_t *d_perm_i2e = nullptr;
-    int32_t *d_exec_ids = nullptr;
-    int32_t *d_asm_ids = nullptr;
     int32_t *d_leafnodes = nullptr;
     int32_t n_leafnodes = 0;
-    // schedule, computed for a given kcap
-    int32_t sched_kcap = -1;
-    std::vector<Launch> launches;
-    std::vector<Launch> asm_launches;
-    int64_t scr_need[2] = {0, 0};
-    int32_t scr_slots[2] = {0, 0};
+    int32_t *d_row_off = nullptr, *d_row_nodes = nullptr;
     hcov_hmat cached = nullptr;
     ~hcov_tree_s();
 };
@@ -337,154 +411,109 @@ struct hcov_hmat_s {
     Ctx ctx{};
     hcov_theta theta{};
     hcov_trunc trunc{};
-    int state = 0;   // 1 assembled, 2 factored
-    double *tiles = nullptr, *U = nullptr, *V = nullptr, *cores = nullptr, *W = nullptr;
-    double *logdet_part = nullptr, *minpiv_part = nullptr;
+    int state = 0;   // 1 assembled, 2 factored, 3 solved
+    int kcap_alloc = -1;
+    int grid = 0;
+    int64_t smem = 0;
+    double *tiles = nullptr, *U = nullptr, *V = nullptr, *cores = nullptr, *W = nullptr, *P = nullptr;
+    double *vbuf = nullptr, *logdet_part = nullptr, *minpiv_part = nullptr, *quad_part = nullptr;
     int32_t *rank = nullptr, *fail = nullptr, *flags = nullptr;
-    double *scr[2] = {nullptr, nullptr};
-    double *vbuf = nullptr, *tbuf = nullptr, *res = nullptr, *res_host = nullptr;
+    int32_t *indeg = nullptr, *q0 = nullptr, *q1 = nullptr;
+    uint32_t *qctl = nullptr;
+    double *scr = nullptr, *bscr = nullptr, *res = nullptr, *res_host = nullptr;
+    EngineStats *stats = nullptr, *stats_host = nullptr;
+    void release_all()
+    {
+        void *ps[] = {tiles, U, V, cores, W, P, vbuf, logdet_part, minpiv_part, quad_part, rank, fail, flags,
+                      indeg, q0, q1, qctl, scr, bscr, res, stats};
+        for (void *p : ps) cudaFree(p);
+        tiles = U = V = cores = W = P = vbuf = logdet_part = minpiv_part = quad_part = nullptr;
+        rank = fail = flags = indeg = q0 = q1 = nullptr;
+        qctl = nullptr;
+        scr = bscr = res = nullptr;
+        stats = nullptr;
+        kcap_alloc = -1;
+    }
     ~hcov_hmat_s()
     {
-        cudaFree(tiles); cudaFree(U); cudaFree(V); cudaFree(cores); cudaFree(W);
-        cudaFree(logdet_part); cudaFree(minpiv_part); cudaFree(rank); cudaFree(fail); cudaFree(flags);
-        cudaFree(scr[0]); cudaFree(scr[1]); cudaFree(vbuf); cudaFree(tbuf); cudaFree(res);
+        release_all();
         if (res_host) cudaFreeHost(res_host);
+        if (stats_host) cudaFreeHost(stats_host);
     }
 };
 
 hcov_tree_s::~hcov_tree_s()
 {
     if (cached) delete cached;
-    void *ps[] = {d_nodes, d_children, d_terms, d_tasks, d_rblk, d_tile_node, d_phw, d_phw_part, d_hleaf,
-                  d_col_r_off, d_col_r, d_ops, d_op_beg, d_op_end, d_fac_row0, d_fac_nrows, d_fac_rank_src,
-                  d_fac_off, d_fac_pool, d_row_off, d_row_nodes, d_xs, d_ys, d_perm_i2e, d_exec_ids, d_asm_ids,
-                  d_leafnodes};
+    void *ps[] = {d_nodes, d_tile_node, d_rblk, d_terms, d_xterm, d_fac_row0, d_fac_nrows, d_fac_rank_src,
+                  d_fac_off, d_fac_pool, d_solves, d_solve_rhs, d_slots, d_ctr, d_phw, d_col_r, d_tasks, d_phase,
+                  d_succ_off, d_succ, d_diag_tile, d_xs, d_ys, d_perm_i2e, d_leafnodes, d_row_off, d_row_nodes};
     for (void *p : ps) cudaFree(p);
+    for (int m = 0; m < 4; ++m) {
+        cudaFree(d_indeg[m]);
+        cudaFree(d_roots[m][0]);
+        cudaFree(d_roots[m][1]);
+    }
 }
 
 namespace {
 
-const int SMALL_SLOTS = 296;
-const int BIG_SLOTS_MAX = 8;
-const int64_t SMALL_LIMIT = (int64_t)3 << 20;   // doubles (24 MB) per small slot at most
+const int NBIG = 8;   // CTAs serving the big-block queue
 
 hcov_status tree_upload(hcov_tree t)
 {
     if (t->uploaded) return HCOV_OK;
     Plan &P = t->P;
     CK(upload(&t->d_nodes, P.nodes));
-    CK(upload(&t->d_children, P.children));
-    CK(upload(&t->d_terms, P.terms));
-    CK(upload(&t->d_tasks, P.tasks));
-    CK(upload(&t->d_rblk, P.rblk));
     CK(upload(&t->d_tile_node, P.tile_node));
-    CK(upload(&t->d_phw, P.phw));
-    CK(upload(&t->d_phw_part, P.phw_part));
-    CK(upload(&t->d_hleaf, P.hleaf));
-    CK(upload(&t->d_col_r_off, P.col_r_off));
-    CK(upload(&t->d_col_r, P.col_r));
-    CK(upload(&t->d_ops, P.ops));
-    CK(upload(&t->d_op_beg, P.op_beg));
-    CK(upload(&t->d_op_end, P.op_end));
+    CK(upload(&t->d_rblk, P.rblk));
+    CK(upload(&t->d_terms, P.terms));
+    CK(upload(&t->d_xterm, P.xterm));
     CK(upload(&t->d_fac_row0, P.fac_row0));
     CK(upload(&t->d_fac_nrows, P.fac_nrows));
     CK(upload(&t->d_fac_rank_src, P.fac_rank_src));
     CK(upload(&t->d_fac_off, P.fac_off));
     CK(upload(&t->d_fac_pool, P.fac_pool));
-    CK(upload(&t->d_row_off, P.row_off));
-    CK(upload(&t->d_row_nodes, P.row_nodes));
+    CK(upload(&t->d_solves, P.solves));
+    CK(upload(&t->d_solve_rhs, P.solve_rhs));
+    CK(upload(&t->d_slots, P.slots));
+    CK(upload(&t->d_ctr, P.ctr));
+    CK(upload(&t->d_phw, P.phw));
+    CK(upload(&t->d_col_r, P.col_r));
+    CK(upload(&t->d_tasks, P.tasks));
+    CK(upload(&t->d_phase, P.phase));
+    CK(upload(&t->d_succ_off, P.succ_off));
+    CK(upload(&t->d_succ, P.succ));
+    for (int m = 0; m < 4; ++m) {
+        CK(upload(&t->d_indeg[m], P.indeg[m]));
+        CK(upload(&t->d_roots[m][0], P.roots[m][0]));
+        CK(upload(&t->d_roots[m][1], P.roots[m][1]));
+    }
+    CK(upload(&t->d_diag_tile, P.diag_tile));
     CK(upload(&t->d_xs, P.xs));
     CK(upload(&t->d_ys, P.ys));
     CK(upload(&t->d_perm_i2e, P.perm_i2e));
     std::vector<int32_t> leafnodes;
-    for (size_t k = 0; k < P.nodes.size(); ++k)
-        if (P.nodes[k].type != ND_H) leafnodes.push_back((int32_t)k);
+    std::vector<std::vector<int32_t>> rows(P.n_leaves);
+    for (size_t k = 0; k < P.nodes.size(); ++k) {
+        const DNode &x = P.nodes[k];
+        if (x.type == ND_H) continue;
+        leafnodes.push_back((int32_t)k);
+        int64_t span = (int64_t)1 << (P.depth - x.level);
+        for (int64_t seg = (int64_t)x.i * span; seg < (int64_t)(x.i + 1) * span; ++seg) rows[seg].push_back((int32_t)k);
+    }
     t->n_leafnodes = (int32_t)leafnodes.size();
     CK(upload(&t->d_leafnodes, leafnodes));
+    std::vector<int32_t> ro(P.n_leaves + 1, 0), rn;
+    for (int64_t s = 0; s < P.n_leaves; ++s) {
+        ro[s] = (int32_t)rn.size();
+        rn.insert(rn.end(), rows[s].begin(), rows[s].end());
+    }
+    ro[P.n_leaves] = (int32_t)rn.size();
+    CK(upload(&t->d_row_off, ro));
+    CK(upload(&t->d_row_nodes, rn));
     t->uploaded = true;
     return HCOV_OK;
-}
-
-// Group the tasks of every wave by (type, scratch class) for a given rank capacity.
-hcov_status tree_schedule(hcov_tree t, int kcap)
-{
-    if (t->sched_kcap == kcap) return HCOV_OK;
-    Plan &P = t->P;
-    const size_t nt = P.tasks.size();
-    std::vector<int64_t> need(nt, 0);
-    for (size_t k = 0; k < nt; ++k) {
-        const DTask &tk = P.tasks[k];
-        if (tk.type == TK_RFIN) {
-            const DRBlk &b = P.rblk[P.nodes[tk.a].idx];
-            need[k] = rfin_scratch(b.m, kcap);
-        } else if (tk.type == TK_SOLVE) {
-            int level = 0;
-            while ((((int64_t)2 << level) - 1) <= tk.a) ++level;
-            int64_t msig = P.cluster_size(level);
-            int cnt = P.col_r_off[tk.a + 1] - P.col_r_off[tk.a];
-            need[k] = solve_scratch(msig, cnt * kcap, kcap);
-        }
-    }
-    int64_t nsmall = 0, nbig = 0;
-    std::vector<int8_t> cls(nt, 0);
-    for (size_t k = 0; k < nt; ++k) {
-        if (need[k] == 0) continue;
-        if (need[k] <= SMALL_LIMIT) { cls[k] = 0; nsmall = std::max(nsmall, need[k]); }
-        else { cls[k] = 1; nbig = std::max(nbig, need[k]); }
-    }
-    // assembly requirements
-    std::vector<int32_t> asm_small, asm_big;
-    for (size_t r = 0; r < P.rblk.size(); ++r) {
-        int64_t nd = assemble_scratch(P.rblk[r].m, kcap);
-        if (nd <= SMALL_LIMIT) { asm_small.push_back((int32_t)r); nsmall = std::max(nsmall, nd); }
-        else { asm_big.push_back((int32_t)r); nbig = std::max(nbig, nd); }
-    }
-    t->scr_need[0] = nsmall;
-    t->scr_need[1] = nbig;
-    // exec order: by wave, then type, then class, then generation order
-    std::vector<int32_t> ids(P.wave_tasks);
-    std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) {
-        if (P.task_wave[a] != P.task_wave[b]) return P.task_wave[a] < P.task_wave[b];
-        if (P.tasks[a].type != P.tasks[b].type) return P.tasks[a].type < P.tasks[b].type;
-        return cls[a] < cls[b];
-    });
-    t->launches.clear();
-    int32_t maxbig = 0, maxsmall = 0;
-    for (size_t k = 0; k < ids.size();) {
-        size_t e = k;
-        const int32_t w = P.task_wave[ids[k]], ty = P.tasks[ids[k]].type, c = cls[ids[k]];
-        while (e < ids.size() && P.task_wave[ids[e]] == w && P.tasks[ids[e]].type == ty && cls[ids[e]] == c) ++e;
-        t->launches.push_back(Launch{ty, c, (int32_t)k, (int32_t)(e - k)});
-        if (need[ids[k]] > 0) {
-            if (c == 1) maxbig = std::max(maxbig, (int32_t)(e - k));
-            else maxsmall = std::max(maxsmall, (int32_t)(e - k));
-        }
-        k = e;
-    }
-    std::vector<int32_t> asm_ids(asm_small);
-    asm_ids.insert(asm_ids.end(), asm_big.begin(), asm_big.end());
-    t->asm_launches.clear();
-    if (!asm_small.empty()) t->asm_launches.push_back(Launch{-1, 0, 0, (int32_t)asm_small.size()});
-    if (!asm_big.empty()) t->asm_launches.push_back(Launch{-1, 1, (int32_t)asm_small.size(), (int32_t)asm_big.size()});
-    maxsmall = std::max(maxsmall, (int32_t)asm_small.size());
-    maxbig = std::max(maxbig, (int32_t)asm_big.size());
-    t->scr_slots[0] = nsmall ? std::min(SMALL_SLOTS, std::max(1, maxsmall)) : 0;
-    t->scr_slots[1] = nbig ? std::min(BIG_SLOTS_MAX, std::max(1, maxbig)) : 0;
-    cudaFree(t->d_exec_ids);
-    cudaFree(t->d_asm_ids);
-    t->d_exec_ids = nullptr;
-    t->d_asm_ids = nullptr;
-    CK(upload(&t->d_exec_ids, ids));
-    CK(upload(&t->d_asm_ids, asm_ids));
-    t->sched_kcap = kcap;
-    return HCOV_OK;
-}
-
-int64_t exec_smem_bytes(int kcap)
-{
-    int64_t a = tile_smem_doubles(kcap);
-    int64_t b = HCOV_TILE + (int64_t)kcap * kcap + 64;
-    return std::max(a, b) * (int64_t)sizeof(double);
 }
 
 hcov_status check_theta(const hcov_theta *th, const hcov_trunc *tr)
@@ -493,7 +522,7 @@ hcov_status check_theta(const hcov_theta *th, const hcov_trunc *tr)
     if (!(th->sigma2 > 0) || !(th->ell > 0) || !(th->nu > 0) || !(th->nugget >= 0)) return HCOV_ERR_INVALID_ARG;
     if (!std::isfinite(th->sigma2) || !std::isfinite(th->ell) || !std::isfinite(th->nu) || !std::isfinite(th->nugget))
         return HCOV_ERR_INVALID_ARG;
-    if (!(tr->eps >= 0) || tr->kmax < 0 || tr->kcap < 0 || tr->kcap > 256) return HCOV_ERR_INVALID_ARG;
+    if (!(tr->eps >= 0) || tr->kmax < 0 || tr->kcap < 0 || tr->kcap > 96) return HCOV_ERR_INVALID_ARG;
     if (tr->kmax > 0 && tr->kcap > 0 && tr->kmax > tr->kcap) return HCOV_ERR_INVALID_ARG;
     return HCOV_OK;
 }
@@ -505,34 +534,63 @@ int eff_kcap(const hcov_trunc *tr)
     return 64;
 }
 
+int64_t qcap(const Plan &P, int cls)
+{
+    int64_t q = 1;
+    for (int m = 0; m < 4; ++m) q = std::max<int64_t>(q, P.n_q[m][cls]);
+    return q;
+}
+
 // (Re)allocate the numeric buffers of h for the tree's plan and capacity kcap.
 hcov_status hmat_alloc(hcov_hmat h, int kcap)
 {
     hcov_tree t = h->t;
     Plan &P = t->P;
-    if (h->tiles && h->ctx.kcap == kcap) return HCOV_OK;
-    cudaFree(h->tiles); cudaFree(h->U); cudaFree(h->V); cudaFree(h->cores); cudaFree(h->W);
-    cudaFree(h->logdet_part); cudaFree(h->minpiv_part); cudaFree(h->rank); cudaFree(h->fail); cudaFree(h->flags);
-    cudaFree(h->scr[0]); cudaFree(h->scr[1]); cudaFree(h->vbuf); cudaFree(h->tbuf); cudaFree(h->res);
-    h->tiles = h->U = h->V = h->cores = h->W = h->logdet_part = h->minpiv_part = nullptr;
-    h->rank = h->fail = h->flags = nullptr;
-    h->scr[0] = h->scr[1] = h->vbuf = h->tbuf = h->res = nullptr;
+    if (h->tiles && h->kcap_alloc == kcap) return HCOV_OK;
+    h->release_all();
+    const int64_t kc = kcap;
     CK(cudaMalloc(&h->tiles, std::max<int64_t>(1, P.n_tiles()) * HCOV_TILE * sizeof(double)));
-    CK(cudaMalloc(&h->U, std::max<int64_t>(1, P.uv_elems * kcap) * sizeof(double)));
-    CK(cudaMalloc(&h->V, std::max<int64_t>(1, P.uv_elems * kcap) * sizeof(double)));
-    CK(cudaMalloc(&h->cores, std::max<int64_t>(1, (int64_t)P.n_cores * kcap * kcap) * sizeof(double)));
-    CK(cudaMalloc(&h->W, std::max<int64_t>(1, P.w_elems * kcap) * sizeof(double)));
+    CK(cudaMalloc(&h->U, std::max<int64_t>(1, P.uv_elems * kc) * sizeof(double)));
+    CK(cudaMalloc(&h->V, std::max<int64_t>(1, P.uv_elems * kc) * sizeof(double)));
+    CK(cudaMalloc(&h->cores, std::max<int64_t>(1, (int64_t)P.n_cores * kc * kc) * sizeof(double)));
+    CK(cudaMalloc(&h->W, std::max<int64_t>(1, P.w_elems * kc) * sizeof(double)));
+    CK(cudaMalloc(&h->P, std::max<int64_t>(1, P.slot_a * kc * kc + P.slot_b * kc) * sizeof(double)));
+    CK(cudaMalloc(&h->vbuf, P.n_pad * sizeof(double)));
     CK(cudaMalloc(&h->logdet_part, P.n_leaves * sizeof(double)));
     CK(cudaMalloc(&h->minpiv_part, P.n_leaves * sizeof(double)));
+    CK(cudaMalloc(&h->quad_part, P.n_leaves * sizeof(double)));
     CK(cudaMalloc(&h->rank, std::max<int64_t>(1, P.n_r()) * sizeof(int32_t)));
     CK(cudaMalloc(&h->fail, sizeof(int32_t)));
     CK(cudaMalloc(&h->flags, 4 * sizeof(int32_t)));
-    for (int k = 0; k < 2; ++k)
-        if (t->scr_slots[k] > 0) CK(cudaMalloc(&h->scr[k], t->scr_need[k] * t->scr_slots[k] * sizeof(double)));
-    CK(cudaMalloc(&h->vbuf, P.n_pad * sizeof(double)));
-    CK(cudaMalloc(&h->tbuf, std::max<int64_t>((int64_t)kcap * kcap + 64, std::max<int64_t>(1, P.n_r()) * kcap) * sizeof(double)));
+    const int64_t ntk = (int64_t)P.tasks.size();
+    CK(cudaMalloc(&h->indeg, std::max<int64_t>(1, ntk) * sizeof(int32_t)));
+    CK(cudaMalloc(&h->q0, qcap(P, 0) * sizeof(int32_t)));
+    CK(cudaMalloc(&h->q1, qcap(P, 1) * sizeof(int32_t)));
+    CK(cudaMalloc(&h->qctl, 8 * sizeof(uint32_t)));
     CK(cudaMalloc(&h->res, 8 * sizeof(double)));
+    CK(cudaMalloc(&h->stats, sizeof(EngineStats)));
     if (!h->res_host) CK(cudaMallocHost(&h->res_host, 8 * sizeof(double)));
+    if (!h->stats_host) CK(cudaMallocHost(&h->stats_host, sizeof(EngineStats)));
+    h->smem = engine_smem_doubles(kcap) * (int64_t)sizeof(double);
+    CK(cudaFuncSetAttribute(k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
+    int dev = 0, nsm = 0, occ = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engine, NT, (size_t)h->smem));
+    occ = std::max(1, std::min(occ, 4));
+    h->grid = nsm * occ;
+    const int64_t med_m = std::min<int64_t>(P.opt.big_m, std::max<int64_t>(P.max_rm, 32));
+    const int64_t scr_stride = task_scratch(med_m, kcap);
+    const int nnorm = h->grid - NBIG;
+    CK(cudaMalloc(&h->scr, scr_stride * nnorm * sizeof(double)));
+    int64_t bscr_stride = 0;
+    if (P.max_rm > P.opt.big_m) {
+        bscr_stride = task_scratch(P.max_rm, kcap);
+        CK(cudaMalloc(&h->bscr, bscr_stride * NBIG * sizeof(double)));
+    }
+    h->ctx.scr_stride = scr_stride;
+    h->ctx.bscr_stride = bscr_stride;
+    h->kcap_alloc = kcap;
     return HCOV_OK;
 }
 
@@ -541,93 +599,99 @@ void fill_ctx(hcov_hmat h)
     hcov_tree t = h->t;
     Plan &P = t->P;
     Ctx &c = h->ctx;
-    c.nodes = t->d_nodes; c.children = t->d_children; c.terms = t->d_terms; c.tasks = t->d_tasks;
-    c.rblk = t->d_rblk; c.tile_node = t->d_tile_node; c.phw = t->d_phw; c.phw_part = t->d_phw_part;
-    c.hleaf = t->d_hleaf; c.col_r_off = t->d_col_r_off; c.col_r = t->d_col_r; c.ops = t->d_ops;
-    c.op_beg = t->d_op_beg; c.op_end = t->d_op_end; c.fac_row0 = t->d_fac_row0; c.fac_nrows = t->d_fac_nrows;
+    c.nodes = t->d_nodes; c.tile_node = t->d_tile_node; c.rblk = t->d_rblk; c.terms = t->d_terms;
+    c.xterm = t->d_xterm; c.fac_row0 = t->d_fac_row0; c.fac_nrows = t->d_fac_nrows;
     c.fac_rank_src = t->d_fac_rank_src; c.fac_off = t->d_fac_off; c.fac_pool = t->d_fac_pool;
-    c.row_off = t->d_row_off; c.row_nodes = t->d_row_nodes; c.xs = t->d_xs; c.ys = t->d_ys;
-    c.perm_i2e = t->d_perm_i2e;
-    c.depth = P.depth; c.n_r = (int32_t)P.n_r(); c.n_pad = P.n_pad; c.n_leaves = P.n_leaves; c.n_real = P.n;
-    c.tiles = h->tiles; c.U = h->U; c.V = h->V; c.rank = h->rank; c.cores = h->cores; c.W = h->W;
-    c.logdet_part = h->logdet_part; c.minpiv_part = h->minpiv_part; c.fail_leaf = h->fail; c.flags = h->flags;
-    c.kmax = h->trunc.kmax; c.eps = h->trunc.eps;
+    c.solves = t->d_solves; c.solve_rhs = t->d_solve_rhs; c.slots = t->d_slots; c.ctr = t->d_ctr;
+    c.phw = t->d_phw; c.col_r = t->d_col_r; c.tasks = t->d_tasks; c.succ_off = t->d_succ_off; c.succ = t->d_succ;
+    c.diag_tile = t->d_diag_tile; c.xs = t->d_xs; c.ys = t->d_ys; c.perm_i2e = t->d_perm_i2e;
+    c.depth = P.depth; c.n_r = (int32_t)P.n_r(); c.root_solve = P.root_solve;
+    c.n_pad = P.n_pad; c.n_leaves = P.n_leaves; c.n_real = P.n; c.n_tiles = P.n_tiles();
+    c.tiles = h->tiles; c.U = h->U; c.V = h->V; c.rank = h->rank; c.cores = h->cores; c.W = h->W; c.P = h->P;
+    c.vbuf = h->vbuf; c.logdet_part = h->logdet_part; c.minpiv_part = h->minpiv_part; c.quad_part = h->quad_part;
+    c.fail_leaf = h->fail; c.flags = h->flags;
+    c.kcap = h->kcap_alloc; c.kmax = h->trunc.kmax; c.eps = h->trunc.eps;
     c.mp = hcov_matern_params(h->theta.sigma2, h->theta.ell, h->theta.nu, h->theta.nugget);
-    for (int k = 0; k < 2; ++k) { c.scr[k] = h->scr[k]; c.scr_stride[k] = t->scr_need[k]; }
+    c.indeg = h->indeg; c.queue[0] = h->q0; c.queue[1] = h->q1; c.qctl = h->qctl;
+    c.nbig = NBIG;
+    c.scr = h->scr; c.bscr = h->bscr;
+    c.flop = nullptr;
+    const char *wd = std::getenv("HCOV_WATCHDOG_S");
+    double wds = wd ? std::atof(wd) : 300.0;
+    if (!(wds > 0)) wds = 300.0;
+    c.timeout_ns = (unsigned long long)(wds * 1e9);
 }
 
-hcov_status assemble_into(hcov_hmat h, const hcov_theta *theta, const hcov_trunc *trunc, cudaStream_t st)
+// Run the engine in mode md (0 all, 1 assembly, 2 Cholesky, 3 solve) on stream st.
+hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
+{
+    hcov_tree t = h->t;
+    Plan &P = t->P;
+    static const int mask[4] = {7, 1, 2, 4};
+    const int64_t ntk = (int64_t)P.tasks.size();
+    Ctx c = h->ctx;
+    c.nq[0] = P.n_q[md][0];
+    c.nq[1] = P.n_q[md][1];
+    if (c.nq[0] + c.nq[1] == 0) return HCOV_OK;
+    LAUNCH(PC_RESET, st, k_reset<<<296, 256, 0, st>>>(c, t->d_indeg[md], ntk, t->d_roots[md][0],
+                                                     (int32_t)P.roots[md][0].size(), t->d_roots[md][1],
+                                                     (int32_t)P.roots[md][1].size(), qcap(P, 0), qcap(P, 1)));
+    EngineStats *stats = g_prof.events ? h->stats : nullptr;
+    if (stats) CK(cudaMemsetAsync(h->stats, 0, sizeof(EngineStats), st));
+    LAUNCH(PC_ENGINE, st, k_engine<<<h->grid, NT, h->smem, st>>>(c, mask[md], t->d_phase, stats));
+    CK(cudaGetLastError());
+    if (stats) {
+        CK(cudaMemcpyAsync(h->stats_host, h->stats, sizeof(EngineStats), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int k = 0; k < TK_NTYPES; ++k) {
+            g_prof.busy_ns[k] += (double)h->stats_host->busy_ns[k];
+            g_prof.tasks[k] += (double)h->stats_host->tasks[k];
+        }
+        for (int k = 0; k < FC_N; ++k) g_prof.flop[k] += h->stats_host->flop[k];
+    }
+    return HCOV_OK;
+}
+
+hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trunc *trunc, cudaStream_t st)
 {
     hcov_tree t = h->t;
     const int kcap = eff_kcap(trunc);
     hcov_status s = tree_upload(t);
     if (s) return s;
-    if ((s = tree_schedule(t, kcap))) return s;
-    if ((s = hmat_alloc(h, kcap))) return s;
     h->theta = *theta;
     h->trunc = *trunc;
-    h->ctx.kcap = kcap;
+    if ((s = hmat_alloc(h, kcap))) return s;
     fill_ctx(h);
     Plan &P = t->P;
     CK(cudaMemsetAsync(h->rank, 0, std::max<int64_t>(1, P.n_r()) * sizeof(int32_t), st));
     CK(cudaMemsetAsync(h->flags, 0, 4 * sizeof(int32_t), st));
     CK(cudaMemsetAsync(h->fail, 0x7f, sizeof(int32_t), st));
-    if (P.n_tiles() > 0) {
-        int grid = (int)std::min<int64_t>(P.n_tiles(), 148 * 16);
-        LAUNCH(PC_FILL, st, k_fill_tiles<<<grid, NT, 0, st>>>(h->ctx, P.n_tiles()));
-    }
-    for (const Launch &L : t->asm_launches) {
-        int grid = std::min(L.cnt, t->scr_slots[L.cls]);
-        LAUNCH(PC_ACA, st, k_assemble_r<<<grid, NT, 0, st>>>(h->ctx, t->d_asm_ids + L.off, L.cnt, L.cls));
-    }
-    CK(cudaGetLastError());
-    h->state = 1;
+    CK(cudaMemsetAsync(h->quad_part, 0, P.n_leaves * sizeof(double), st));
     return HCOV_OK;
 }
 
-hcov_status cholesky_run(hcov_hmat h, cudaStream_t st, int64_t *fail_leaf)
+hcov_status check_abort(hcov_hmat h, cudaStream_t st, int32_t *hf)
 {
-    if (!h || h->state != 1) return HCOV_ERR_STATE;
-    hcov_tree t = h->t;
-    const int64_t smem = exec_smem_bytes(h->ctx.kcap);
-    CK(cudaFuncSetAttribute(k_exec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    for (const Launch &L : t->launches) {
-        int grid;
-        const bool scratch = (L.type == TK_RFIN || L.type == TK_SOLVE);
-        if (scratch) grid = std::min(L.cnt, t->scr_slots[L.cls]);
-        else grid = std::min(L.cnt, 65535);
-        Ctx c = h->ctx;
-        if (!scratch) { c.scr[0] = c.scr[1] = nullptr; }
-        static const int cls_of[7] = {PC_POTRF, PC_TRSM, PC_RFIN, PC_LRSOLVE, PC_PRR, PC_PHW, PC_AUX};
-        LAUNCH(cls_of[L.type], st, k_exec<<<grid, NT, smem, st>>>(c, t->d_exec_ids + L.off, L.cnt, scratch ? L.cls : 0));
-    }
-    CK(cudaGetLastError());
-    int32_t hf[5];
+    uint32_t ab = 0;
+    CK(cudaMemcpyAsync(&ab, h->qctl + 4, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf, h->fail, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf + 1, h->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    h->state = 2;
-    int64_t fl = (hf[0] == 0x7f7f7f7f) ? -1 : hf[0];
-    if (fail_leaf) *fail_leaf = fl;
-    if (fl >= 0) return HCOV_ERR_NOT_SPD;
-    if (hf[2] > 0 && h->trunc.kmax == 0) return HCOV_ERR_RANK_CAPACITY;
+    if (ab) return HCOV_ERR_CUDA;
     return HCOV_OK;
 }
 
-hcov_status loglik_run(hcov_hmat h, const double *Z, cudaStream_t st, hcov_result *out)
+hcov_status finish_result(hcov_hmat h, cudaStream_t st, hcov_result *out)
 {
-    if (!h || h->state != 2) return HCOV_ERR_STATE;
     Plan &P = h->t->P;
-    LAUNCH(PC_REDUCE, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, Z, h->vbuf));
-    LAUNCH(PC_FWD, st, k_fwd_solve<<<1, NT, 0, st>>>(h->ctx, h->vbuf, h->tbuf));
-    LAUNCH(PC_REDUCE, st, k_reduce<<<1, NT, 0, st>>>(h->ctx, h->vbuf, h->res));
+    LAUNCH(PC_REDUCE, st, k_reduce<<<1, NT, 0, st>>>(h->ctx, h->res));
     CK(cudaGetLastError());
     int32_t hf[5];
     CK(cudaMemcpyAsync(h->res_host, h->res, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hf, h->fail, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hf + 1, h->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    hcov_status s = check_abort(h, st, hf);
+    if (s) return s;
     const double ld = h->res_host[0], q = h->res_host[1];
+    std::memset(out, 0, sizeof(*out));
     out->n = P.n;
     out->logdet = ld;
     out->quad = q;
@@ -636,6 +700,8 @@ hcov_status loglik_run(hcov_hmat h, const double *Z, cudaStream_t st, hcov_resul
     out->fail_leaf = (hf[0] == 0x7f7f7f7f) ? -1 : hf[0];
     out->cap_binds = hf[1];
     out->max_rank = hf[3];
+    if (out->fail_leaf >= 0) { out->loglik = -INFINITY; return HCOV_ERR_NOT_SPD; }
+    if (hf[2] > 0 && h->trunc.kmax == 0) { out->loglik = -INFINITY; return HCOV_ERR_RANK_CAPACITY; }
     return HCOV_OK;
 }
 
@@ -670,7 +736,10 @@ hcov_status hcov_build_tree_host(const double *s_host, int64_t n, int32_t leaf_s
     if (!s_host || n < 0 || leaf_size != HCOV_LEAF || !(eta >= 0) || dense_below < 0) return HCOV_ERR_INVALID_ARG;
     std::unique_ptr<hcov_tree_s> t(new (std::nothrow) hcov_tree_s());
     if (!t) return HCOV_ERR_OUT_OF_MEMORY;
-    int rc = plan_build(t->P, s_host, n, eta, dense_below);
+    PlanOpts o;
+    o.eta = eta;
+    o.dense_below = dense_below;
+    int rc = plan_build(t->P, s_host, n, o);
     if (rc == 2) return HCOV_ERR_EMPTY_INPUT;
     if (rc) return HCOV_ERR_INVALID_ARG;
     *out = t.release();
@@ -702,7 +771,7 @@ hcov_status hcov_tree_get_info(hcov_tree t, hcov_tree_info *info)
     const Plan &P = t->P;
     info->n = P.n; info->n_pad = P.n_pad; info->depth = P.depth; info->leaf_size = HCOV_LEAF;
     info->n_leaves = P.n_leaves; info->n_dense_tiles = P.n_tiles(); info->n_lowrank = P.n_r();
-    info->n_tasks = (int64_t)P.tasks.size(); info->n_waves = P.n_waves; info->eta = P.eta;
+    info->n_tasks = (int64_t)P.tasks.size(); info->n_waves = P.crit_len; info->eta = P.opt.eta;
     return HCOV_OK;
 }
 
@@ -729,6 +798,21 @@ hcov_status hcov_tree_blocks(hcov_tree t, int32_t *out4, int64_t cap, int64_t *c
     return HCOV_OK;
 }
 
+hcov_status hcov_tree_tasks(hcov_tree t, int32_t *out6, int64_t cap, int64_t *count)
+{
+    if (!t || !count) return HCOV_ERR_INVALID_ARG;
+    const Plan &P = t->P;
+    *count = (int64_t)P.tasks.size();
+    if (!out6) return HCOV_OK;
+    if (cap < *count) return HCOV_ERR_INVALID_ARG;
+    for (size_t k = 0; k < P.tasks.size(); ++k) {
+        const DTask &tk = P.tasks[k];
+        int32_t *o = out6 + 6 * k;
+        o[0] = tk.type; o[1] = P.phase[k]; o[2] = tk.a; o[3] = tk.b; o[4] = tk.c; o[5] = tk.d;
+    }
+    return HCOV_OK;
+}
+
 hcov_status hcov_tree_bbox(hcov_tree t, double *bb, int64_t cap)
 {
     if (!t || !bb || cap < (int64_t)t->P.bb.size()) return HCOV_ERR_INVALID_ARG;
@@ -747,8 +831,15 @@ hcov_status hcov_assemble(hcov_tree t, const hcov_theta *theta, const hcov_trunc
     hcov_hmat h = new (std::nothrow) hcov_hmat_s();
     if (!h) return HCOV_ERR_OUT_OF_MEMORY;
     h->t = t;
-    s = assemble_into(h, theta, trunc, (cudaStream_t)stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    s = assemble_setup(h, theta, trunc, st);
+    if (!s) s = engine_run(h, 1, st);
+    if (!s) {
+        int32_t hf[5];
+        s = check_abort(h, st, hf);
+    }
     if (s) { delete h; return s; }
+    h->state = 1;
     *out = h;
     return HCOV_OK;
 }
@@ -756,13 +847,30 @@ hcov_status hcov_assemble(hcov_tree t, const hcov_theta *theta, const hcov_trunc
 hcov_status hcov_cholesky(hcov_hmat h, hcov_stream stream, int64_t *fail_leaf)
 {
     if (!h) return HCOV_ERR_INVALID_ARG;
-    return cholesky_run(h, (cudaStream_t)stream, fail_leaf);
+    if (h->state != 1) return HCOV_ERR_STATE;
+    cudaStream_t st = (cudaStream_t)stream;
+    hcov_status s = engine_run(h, 2, st);
+    if (s) return s;
+    int32_t hf[5];
+    if ((s = check_abort(h, st, hf))) return s;
+    h->state = 2;
+    int64_t fl = (hf[0] == 0x7f7f7f7f) ? -1 : hf[0];
+    if (fail_leaf) *fail_leaf = fl;
+    if (fl >= 0) return HCOV_ERR_NOT_SPD;
+    if (hf[2] > 0 && h->trunc.kmax == 0) return HCOV_ERR_RANK_CAPACITY;
+    return HCOV_OK;
 }
 
 hcov_status hcov_loglik(hcov_hmat h, const double *Z_dev, hcov_stream stream, hcov_result *out)
 {
     if (!h || !Z_dev || !out) return HCOV_ERR_INVALID_ARG;
-    return loglik_run(h, Z_dev, (cudaStream_t)stream, out);
+    if (h->state < 2) return HCOV_ERR_STATE;
+    cudaStream_t st = (cudaStream_t)stream;
+    LAUNCH(PC_PERM, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, Z_dev, h->vbuf));
+    hcov_status s = engine_run(h, 3, st);
+    if (s) return s;
+    h->state = 3;
+    return finish_result(h, st, out);
 }
 
 hcov_status hcov_eval(hcov_tree t, const hcov_theta *theta, const hcov_trunc *trunc, const double *Z_dev,
@@ -778,18 +886,11 @@ hcov_status hcov_eval(hcov_tree t, const hcov_theta *theta, const hcov_trunc *tr
     }
     hcov_hmat h = t->cached;
     cudaStream_t st = (cudaStream_t)stream;
-    if ((s = assemble_into(h, theta, trunc, st))) return s;
-    int64_t fl = -1;
-    s = cholesky_run(h, st, &fl);
-    if (s == HCOV_ERR_NOT_SPD || s == HCOV_ERR_RANK_CAPACITY) {
-        std::memset(out, 0, sizeof(*out));
-        out->n = t->P.n;
-        out->loglik = -INFINITY;
-        out->fail_leaf = fl;
-        return s;
-    }
-    if (s) return s;
-    return loglik_run(h, Z_dev, st, out);
+    if ((s = assemble_setup(h, theta, trunc, st))) return s;
+    LAUNCH(PC_PERM, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, Z_dev, h->vbuf));
+    if ((s = engine_run(h, 0, st))) return s;
+    h->state = 3;
+    return finish_result(h, st, out);
 }
 
 hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *thetas, int32_t m,
@@ -811,17 +912,18 @@ hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *t
 hcov_status hcov_sample(hcov_hmat h, const double *xi_dev, double *Z_dev, hcov_stream stream)
 {
     if (!h || !xi_dev || !Z_dev) return HCOV_ERR_INVALID_ARG;
-    if (h->state != 2) return HCOV_ERR_STATE;
+    if (h->state < 2) return HCOV_ERR_STATE;
     cudaStream_t st = (cudaStream_t)stream;
     Plan &P = h->t->P;
     double *x = nullptr, *y = nullptr, *tt = nullptr;
     CK(cudaMalloc(&x, P.n_pad * sizeof(double)));
     CK(cudaMalloc(&y, P.n_pad * sizeof(double)));
     CK(cudaMalloc(&tt, std::max<int64_t>(1, P.n_r()) * h->ctx.kcap * sizeof(double)));
-    k_permute_in<<<256, 256, 0, st>>>(h->ctx, xi_dev, x);
-    if (P.n_r() > 0) k_sample_t<<<(int)std::min<int64_t>(P.n_r(), 65535), NT, 0, st>>>(h->ctx, x, tt);
-    k_sample_rows<<<(int)std::min<int64_t>(P.n_leaves, 65535), 32, 0, st>>>(h->ctx, x, tt, y);
-    k_permute_out<<<256, 256, 0, st>>>(h->ctx, y, Z_dev);
+    LAUNCH(PC_AUX, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, xi_dev, x));
+    if (P.n_r() > 0) LAUNCH(PC_AUX, st, k_sample_t<<<(int)std::min<int64_t>(P.n_r(), 65535), NT, 0, st>>>(h->ctx, x, tt));
+    LAUNCH(PC_AUX, st, k_sample_rows<<<(int)std::min<int64_t>(P.n_leaves, 65535), 32, 0, st>>>(
+                           h->ctx, h->t->d_row_off, h->t->d_row_nodes, x, tt, y));
+    LAUNCH(PC_AUX, st, k_permute_out<<<256, 256, 0, st>>>(h->ctx, y, Z_dev));
     cudaError_t e = cudaStreamSynchronize(st);
     cudaFree(x); cudaFree(y); cudaFree(tt);
     if (e != cudaSuccess) return map_err(e);
@@ -849,8 +951,9 @@ hcov_status hcov_columns(hcov_hmat h, const int64_t *cols_host, int32_t m, doubl
     CK(cudaMalloc(&d_pc, std::max(1, m) * sizeof(int64_t)));
     CK(cudaMalloc(&tmp, std::max<int64_t>(1, P.n_pad * m) * sizeof(double)));
     CK(cudaMemcpyAsync(d_pc, pc.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    k_columns<<<std::min(t->n_leafnodes, 65535), NT, 0, st>>>(h->ctx, t->d_leafnodes, t->n_leafnodes, d_pc, m, tmp);
-    k_columns_perm<<<512, 256, 0, st>>>(h->ctx, tmp, m, out_dev);
+    LAUNCH(PC_AUX, st, k_columns<<<std::min(t->n_leafnodes, 65535), NT, 0, st>>>(h->ctx, t->d_leafnodes,
+                                                                                 t->n_leafnodes, d_pc, m, tmp));
+    LAUNCH(PC_AUX, st, k_columns_perm<<<512, 256, 0, st>>>(h->ctx, tmp, m, out_dev));
     cudaError_t e = cudaStreamSynchronize(st);
     cudaFree(d_pc); cudaFree(tmp);
     if (e != cudaSuccess) return map_err(e);
@@ -878,6 +981,8 @@ hcov_status hcov_prof_control(int32_t enable_events, int32_t reset)
         prof_collect();
         g_prof.launches = 0;
         for (int k = 0; k < PC_N; ++k) { g_prof.count[k] = 0; g_prof.ms[k] = 0.0; }
+        for (int k = 0; k < TK_NTYPES; ++k) { g_prof.busy_ns[k] = 0; g_prof.tasks[k] = 0; }
+        for (int k = 0; k < FC_N; ++k) g_prof.flop[k] = 0;
     }
     g_prof.events = enable_events != 0;
     return HCOV_OK;
@@ -894,12 +999,23 @@ hcov_status hcov_prof_read(hcov_prof *out)
         out->ms[k] = g_prof.ms[k];
         out->count[k] = g_prof.count[k];
     }
+    out->n_task_types = TK_NTYPES;
+    for (int k = 0; k < TK_NTYPES; ++k) {
+        out->task_busy_ms[k] = g_prof.busy_ns[k] * 1e-6;
+        out->task_count[k] = g_prof.tasks[k];
+    }
+    for (int k = 0; k < FC_N; ++k) out->flop[k] = g_prof.flop[k];
     return HCOV_OK;
 }
 
 const char *hcov_prof_class_name(int32_t cls)
 {
     return (cls >= 0 && cls < PC_N) ? PROF_NAMES[cls] : "";
+}
+
+const char *hcov_prof_task_name(int32_t type)
+{
+    return (type >= 0 && type < TK_NTYPES) ? TASK_NAMES[type] : "";
 }
 
 void hcov_tree_free(hcov_tree t) { delete t; }

@@ -1,5 +1,5 @@
-// Internal data structures shared by the host planner (plan.cpp) and the device kernels.
-// POD only; device arrays are copies of the host vectors built in plan.cpp.
+// Internal data structures shared by the host planner (plan.cpp) and the device engine
+// (engine.cuh, hcov.cu).  POD only; the device arrays are copies of the host vectors.
 #pragma once
 #include <stdint.h>
 
@@ -14,42 +14,59 @@ struct DNode {
     int32_t type;          // NodeType
     int32_t parent;        // node id of the parent, -1 for the root
     int32_t idx;           // tile id (ND_T) or low-rank block id (ND_R); -1 for ND_H
-    int32_t term_off, term_cnt;  // pending-update terms attached to this node (lazy Schur updates)
-    int32_t leaf_off, leaf_cnt;  // ND_H only: flattened list of leaf nodes (T/R) inside, for H x X
 };
 
-// A pending Schur-complement term  A * K * B^T  (K = I if core < 0) or a dense tile product
-// A * B^T (kind TT).  Rows of A / B are global internal indices starting at fac_row0.
+// A pending Schur-complement term (lazy left-looking H-Cholesky):
+//   TT: tile_a * tile_b^T (32 x 32 dense product);
+//   LR: A * K * B^T with A, B factors (fac ids) and K a core (or I if core < 0).
+// Rows of A / B are global internal indices starting at fac_row0.
 enum TermKind : int32_t { TM_TT = 0, TM_LR = 1 };
 struct DTerm {
     int32_t kind;
-    int32_t a, b;   // TT: tile ids.  LR: factor ids.
-    int32_t core;   // LR: core id or -1
+    int32_t a, b;
+    int32_t core;
 };
 
+// Tasks of the DAG executed by the persistent engine (one CTA per task).
 enum TaskType : int32_t {
-    TK_POTRF = 0,  // a = diag T node: finalise (apply terms) + dense Cholesky + log det partial
-    TK_TRSM = 1,   // a = off-diag T node, b = diag tile id of its column: finalise + X <- S L^-T
-    TK_RFIN = 2,   // a = R node: finalise S = U V^T - terms, recompress to (eps, kmax)
-    TK_SOLVE = 3,  // a = cluster heap id s: V <- L_ss^-1 V for all R entries of column s
-    TK_PRR = 4,    // a, b = R nodes (same column), c = core id:  K = V_a^T V_b
-    TK_PHW = 5,    // a = H node, b = phw id: W = H * [V of partners]
-    TK_NOP = 6
+    TK_FILL = 0,   // a = first tile, b = count: dense tiles of C~ (A4)
+    TK_ACA = 1,    // a = R id: ACA + truncation of an admissible block of C~ (A5, A6)
+    TK_TAPP = 2,   // a = tile, [b, c) = range of xterm[]: apply pending terms to the tile
+    TK_POTRF = 3,  // a = diag tile, [b, c) terms: apply, then Cholesky + L^{-1} + log det partial (A7, A8)
+    TK_TRSM = 4,   // a = tile, [b, c) terms, d = diag tile of its column: apply, then X <- X L^{-T}
+    TK_RAPP = 5,   // a = R id, [b, c) terms: append the terms' factors, recompress (A6 inside A7)
+    TK_SEG = 6,    // a = solve id, b = leaf row segment, [c, d) = ctr[] contributions: forward solve rows
+    TK_PROJ = 7,   // a = solve id, b = R id, c = proj slot: P = V_b^T Y[cols of b]
+    TK_PRR = 8,    // a, b = R ids, c = core id: K = V_a^T V_b
+    TK_PHWP = 9,   // a = phw id, b = R id (leaf of the H block), c = q slot: Q = V_x^T V_partners[cols of x]
+    TK_PHWR = 10,  // a = phw id, b = leaf row segment, [c, d) = ctr[]: W rows = H(rows, :) V_partners
+    TK_NOP = 11,   // join (completed inline by the engine, never occupies a CTA)
+    TK_NTYPES = 12
 };
 struct DTask {
     int32_t type;
-    int32_t a, b, c;
+    int32_t a, b, c, d;
+    int32_t qcls;      // queue class: 0 = normal, 1 = big (needs a big scratch slot)
 };
 
-// Forward-solve program op (post-order over the cluster tree).
-enum OpKind : int32_t { OP_TRSM = 0, OP_UPD_T = 1, OP_UPD_R = 2 };
-struct DOp {
-    int32_t kind;
-    int32_t id;        // tile id (TRSM, UPD_T) or R id (UPD_R)
-    int32_t m;         // rows / cols of the block (32 for tiles)
-    int32_t pad;
-    int64_t row0;      // first internal row of the block
-    int64_t col0;      // first internal column of the block
+// Contribution of one block-tree leaf to a row segment in a SEG / PHWR task.
+//   kind 0: dense tile `id` (column segment aux);  kind 1: low-rank block `id`, product slot aux.
+struct DCtr {
+    int32_t kind, id, aux, pad;
+};
+
+// A forward-solve problem  Y <- L_ss^{-1} Y  on the diagonal block of cluster s.  The right-hand
+// sides are the V factors of the low-rank entries of column s (rhs_cnt R ids in solve_rhs[]),
+// or the permuted data vector z for the root solve (rhs_cnt = 0).
+struct DSolve {
+    int32_t level, c;        // cluster
+    int32_t rhs_off, rhs_cnt;
+    int64_t row0, m;
+};
+
+// Product slots (PROJ / PHWP results): doubles at  offa * kcap * kcap + offb * kcap.
+struct DSlot {
+    int64_t offa, offb;
 };
 
 // Low-rank block static description.
@@ -57,17 +74,17 @@ struct DRBlk {
     int32_t node;      // node id
     int32_t level;
     int32_t m;         // block size (rows = cols)
-    int32_t pad;
+    int32_t solve;     // solve id of its column (the solve that finalises V)
     int64_t row0, col0;
-    int64_t uv_off;    // offset (elements) of U and V in the U / V pools; each m x kcap col-major
+    int64_t uv_off;    // offset (elements per unit kcap) of U and V in the pools; each m x kcap col-major
 };
 
-// Product H x [V_partners] bookkeeping.
+// W = H * [V_partners] bookkeeping for an H entry of a column with low-rank entries.
 struct DPhw {
-    int32_t hnode;     // H node id (rows rho, cols sigma)
-    int32_t part_off, part_cnt;  // partner R ids in phw_part[]
-    int32_t fac_base;  // factor ids fac_base .. fac_base+part_cnt-1 are its W slices
-    int64_t w_off;     // offset (elements) of W in the W pool, m x (kcap * part_cnt)
+    int32_t hnode;               // H node id (rows rho, cols sigma)
+    int32_t part_off, part_cnt;  // partner R ids in col_r[]
+    int32_t fac_base;            // factor ids fac_base .. fac_base+part_cnt-1 are its W slices
+    int64_t w_off;               // offset (elements per unit kcap) of W: m x (kcap * part_cnt)
     int32_t m;
     int32_t pad;
 };

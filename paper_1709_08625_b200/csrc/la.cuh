@@ -156,18 +156,18 @@ __device__ void qr_apply_q(const double *A, int64_t lda, int64_t m, int R, const
 }
 
 // ------------------------------------------------------------------------------------------
-// One-sided Jacobi SVD of M (R x R, ld R, global scratch): on return M <- M J (columns
-// mutually orthogonal, ||col_i|| = sigma_i) and J orthogonal, so M_in = (M J) J^T.
-// Round-robin parallel ordering (R/2 disjoint pairs per round, one warp per pair).
+// One-sided Jacobi SVD of G (K x nc, ld K, global scratch): on return G <- G J (columns mutually
+// orthogonal, ||col_i|| = sigma_i) and J (nc x nc, ld nc) orthogonal, so G_in = (G J) J^T.
+// Round-robin parallel ordering (nc/2 disjoint pairs per round, one warp per pair).
 // ------------------------------------------------------------------------------------------
-__device__ void jacobi_svd(double *M, double *J, int R)
+__device__ void jacobi_svd(double *G, int64_t K, double *J, int nc)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ int s_rot;
-    for (int e = threadIdx.x; e < R * R; e += NT) J[e] = ((e % R) == (e / R)) ? 1.0 : 0.0;
+    for (int e = threadIdx.x; e < nc * nc; e += NT) J[e] = ((e % nc) == (e / nc)) ? 1.0 : 0.0;
     __syncthreads();
-    const int Rp = R + (R & 1);
-    for (int sweep = 0; sweep < 60; ++sweep) {
+    const int Rp = nc + (nc & 1);
+    for (int sweep = 0; sweep < 40; ++sweep) {
         if (threadIdx.x == 0) s_rot = 0;
         __syncthreads();
         for (int round = 0; round < Rp - 1; ++round) {
@@ -175,11 +175,11 @@ __device__ void jacobi_svd(double *M, double *J, int R)
                 int a = t, b = Rp - 1 - t;
                 int p = (a == 0) ? 0 : 1 + ((a - 1 + round) % (Rp - 1));
                 int q = (b == 0) ? 0 : 1 + ((b - 1 + round) % (Rp - 1));
-                if (p >= R || q >= R) continue;
-                double *mp = M + (int64_t)R * p, *mq = M + (int64_t)R * q;
+                if (p >= nc || q >= nc) continue;
+                double *gp = G + K * p, *gq = G + K * q;
                 double al = 0.0, be = 0.0, ga = 0.0;
-                for (int i = lane; i < R; i += 32) {
-                    double x = mp[i], y = mq[i];
+                for (int64_t i = lane; i < K; i += 32) {
+                    double x = gp[i], y = gq[i];
                     al += x * x; be += y * y; ga += x * y;
                 }
                 al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
@@ -187,13 +187,13 @@ __device__ void jacobi_svd(double *M, double *J, int R)
                     double zeta = (be - al) / (2.0 * ga);
                     double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                     double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
-                    for (int i = lane; i < R; i += 32) {
-                        double x = mp[i], y = mq[i];
-                        mp[i] = c * x - s * y;
-                        mq[i] = s * x + c * y;
+                    for (int64_t i = lane; i < K; i += 32) {
+                        double x = gp[i], y = gq[i];
+                        gp[i] = c * x - s * y;
+                        gq[i] = s * x + c * y;
                     }
-                    double *jp = J + (int64_t)R * p, *jq = J + (int64_t)R * q;
-                    for (int i = lane; i < R; i += 32) {
+                    double *jp = J + (int64_t)nc * p, *jq = J + (int64_t)nc * q;
+                    for (int i = lane; i < nc; i += 32) {
                         double x = jp[i], y = jq[i];
                         jp[i] = c * x - s * y;
                         jq[i] = s * x + c * y;
@@ -209,73 +209,180 @@ __device__ void jacobi_svd(double *M, double *J, int R)
     __syncthreads();
 }
 
+// Householder QR with column pivoting of the K x K matrix M (ld K, in place), stopped at the
+// first step whose largest remaining column norm is <= tol * (largest initial column norm) or
+// at rmax steps.  On return: reflectors below the diagonal of the first r columns (tau[0..r)),
+// R in the upper trapezoid of rows 0..r-1, piv[k] = original column of column k.  Returns r.
+__device__ int qrcp_trunc(double *M, int K, double tol, int rmax, double *tau, int *piv, double *cn,
+                          double *redv, int64_t *redi, double *red)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k = threadIdx.x; k < K; k += NT) piv[k] = k;
+    __shared__ double s_n1;
+    __shared__ int s_stop;
+    int j = 0;
+    for (; j < min(K, rmax); ++j) {
+        // exact remaining column norms (rows j..K-1) of columns j..K-1
+        for (int k = j + warp; k < K; k += NWARP) {
+            const double *mk = M + (int64_t)K * k;
+            double s = 0.0;
+            for (int i = j + lane; i < K; i += 32) s += mk[i] * mk[i];
+            s = warp_sum(s);
+            if (lane == 0) cn[k] = s;
+        }
+        __syncthreads();
+        double bv = -1.0;
+        int64_t bi = K;
+        for (int k = j + threadIdx.x; k < K; k += NT)
+            if (vi_better(cn[k], k, bv, bi)) { bv = cn[k]; bi = k; }
+        ValIdx b = block_argmax(bv, bi, redv, redi);
+        if (threadIdx.x == 0) {
+            const double nrm = sqrt(fmax(b.v, 0.0));
+            if (j == 0) s_n1 = nrm;
+            s_stop = !(nrm > tol * s_n1) || !(nrm > 0.0);
+        }
+        __syncthreads();
+        if (s_stop) break;
+        const int p = (int)b.i;
+        if (p != j) {   // swap columns j and p
+            double *mj = M + (int64_t)K * j, *mp = M + (int64_t)K * p;
+            for (int i = threadIdx.x; i < K; i += NT) { double t = mj[i]; mj[i] = mp[i]; mp[i] = t; }
+            if (threadIdx.x == 0) { int t = piv[j]; piv[j] = piv[p]; piv[p] = t; }
+            __syncthreads();
+        }
+        // Householder reflector of column j, rows j..K-1
+        double *aj = M + (int64_t)K * j;
+        double s = 0.0;
+        for (int i = j + 1 + threadIdx.x; i < K; i += NT) s += aj[i] * aj[i];
+        s = block_sum(s, red);
+        const double alpha = aj[j];
+        double t = 0.0, beta = alpha, scale = 0.0;
+        if (s > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + s), alpha);
+            t = (beta - alpha) / beta;
+            scale = 1.0 / (alpha - beta);
+        }
+        __syncthreads();
+        if (s > 0.0)
+            for (int i = j + 1 + threadIdx.x; i < K; i += NT) aj[i] *= scale;
+        if (threadIdx.x == 0) { aj[j] = beta; tau[j] = t; }
+        __syncthreads();
+        if (t != 0.0) {
+            for (int k = j + 1 + warp; k < K; k += NWARP) {
+                double *ak = M + (int64_t)K * k;
+                double w = 0.0;
+                for (int i = j + 1 + lane; i < K; i += 32) w += aj[i] * ak[i];
+                w = warp_sum(w) + ak[j];
+                w *= t;
+                if (lane == 0) ak[j] -= w;
+                for (int i = j + 1 + lane; i < K; i += 32) ak[i] -= aj[i] * w;
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    return j;
+}
+
 // Truncation workspace for R columns of m rows.
 struct CompressWs {
-    double *X, *Y;      // m x R each (ld m): inputs, destroyed
-    double *M, *J;      // R x R each
-    double *tx, *ty;    // R each
-    double *sig;        // R
-    int *ord;           // R
+    double *X, *Y;      // m x K each (ld m): inputs, destroyed (Householder vectors)
+    double *M, *G, *J;  // K x K, K x K, K x K
+    double *tx, *ty, *tm;   // K each
+    double *sig, *cn;   // K each
+    int *ord, *piv;     // K each
 };
 
-// Truncate X Y^T (m x m, rank <= R) to U V^T with the smallest r such that
-// sigma_{r+1} <= eps * sigma_1, then r <= kmax (if kmax > 0), r <= kcap.
-// U, V: m x kcap (ld ldo).  Returns r; *cap_bound = 1 if kmax cut below the eps-rank,
-// *overflow = 1 if the eps-rank exceeded kcap with kmax == 0 (result truncated to kcap).
-__device__ int compress(const CompressWs &w, int64_t m, int R, double eps, int kmax, int kcap,
-                        double *U, double *V, int64_t ldo, int *cap_bound, int *overflow, double *red)
+// Truncate X Y^T (m x m, rank <= R) to U V^T (A6):
+//   [Q_X, R_X] = qr(X), [Q_Y, R_Y] = qr(Y), M = R_X R_Y^T (R x R);
+//   M Pi = Q_M R_M by pivoted QR stopped at tol_q (rank-revealing pre-truncation, r' rows);
+//   final (svd = true): SVD of the r' x R matrix B = R_M[:r'] Pi^T by one-sided Jacobi on B^T,
+//     keep the smallest r with sigma_{r+1} <= eps sigma_1, then r <= kmax (kmax > 0), r <= rlim;
+//     U = Q_X [Q_M [J_r; 0]; 0],  V = Q_Y [(B^T J)_r; 0];
+//   intermediate (svd = false): r = r', U = Q_X [Q_M [I; 0]; 0], V = Q_Y [B^T; 0].
+// U, V: m x r (ld ldo), must not alias X, Y.  Returns r.  *cap_bound = 1 if kmax cut below the
+// eps-rank, *overflow = 1 if the rank exceeded rlim with kmax == 0.
+__device__ int compress(const CompressWs &w, int64_t m, int R, double eps, double tol_q, bool svd, int kmax,
+                        int rlim, double *U, double *V, int64_t ldo, int *cap_bound, int *overflow, double *red,
+                        double *redv, int64_t *redi)
 {
+    __shared__ int s_r, s_cb, s_of;
     if (R == 0) { if (threadIdx.x == 0) { *cap_bound = 0; *overflow = 0; } __syncthreads(); return 0; }
     qr_house(w.X, m, m, R, w.tx, red);
     qr_house(w.Y, m, m, R, w.ty, red);
+    const int K = R;
     // M = R_X R_Y^T   (R_X[i,k] != 0 for k >= i)
-    for (int e = threadIdx.x; e < R * R; e += NT) {
-        int i = e % R, j = e / R;
+    for (int e = threadIdx.x; e < K * K; e += NT) {
+        int i = e % K, j = e / K;
         double s = 0.0;
-        for (int k = max(i, j); k < R; ++k) s += w.X[i + m * k] * w.Y[j + m * k];
+        for (int k = max(i, j); k < K; ++k) s += w.X[i + m * k] * w.Y[j + m * k];
         w.M[e] = s;
     }
     __syncthreads();
-    jacobi_svd(w.M, w.J, R);
-    for (int i = threadIdx.x; i < R; i += NT) {
-        double s = 0.0;
-        for (int k = 0; k < R; ++k) { double x = w.M[k + R * i]; s += x * x; }
-        w.sig[i] = sqrt(s);
+    const int rq = qrcp_trunc(w.M, K, tol_q, svd ? K : rlim + 1, w.tm, w.piv, w.cn, redv, redi, red);
+    // B^T (K x rq): G[piv[k], i] = R_M[i, k] for k >= i
+    for (int e = threadIdx.x; e < K * rq; e += NT) {
+        int k = e % K, i = e / K;
+        w.G[w.piv[k] + (int64_t)K * i] = (k >= i) ? w.M[i + (int64_t)K * k] : 0.0;
     }
     __syncthreads();
-    // rank of each singular value in descending order (ties -> lower index first)
-    for (int i = threadIdx.x; i < R; i += NT) {
-        int pos = 0;
-        double si = w.sig[i];
-        for (int j = 0; j < R; ++j) {
-            double sj = w.sig[j];
-            if (sj > si || (sj == si && j < i)) ++pos;
+    int r;
+    if (svd) {
+        jacobi_svd(w.G, K, w.J, rq);
+        for (int i = threadIdx.x; i < rq; i += NT) {
+            double s = 0.0;
+            for (int k = 0; k < K; ++k) { double x = w.G[k + (int64_t)K * i]; s += x * x; }
+            w.sig[i] = sqrt(s);
         }
-        w.ord[pos] = i;
+        __syncthreads();
+        for (int i = threadIdx.x; i < rq; i += NT) {
+            int pos = 0;
+            double si = w.sig[i];
+            for (int j = 0; j < rq; ++j) {
+                double sj = w.sig[j];
+                if (sj > si || (sj == si && j < i)) ++pos;
+            }
+            w.ord[pos] = i;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s1 = rq > 0 ? w.sig[w.ord[0]] : 0.0;
+            int rr = 0;
+            if (s1 > 0.0)
+                while (rr < rq && w.sig[w.ord[rr]] > eps * s1) ++rr;
+            int cb = 0, of = 0;
+            if (kmax > 0 && rr > kmax) { rr = kmax; cb = 1; }
+            if (rr > rlim) { rr = rlim; of = (kmax == 0); }
+            s_r = rr; s_cb = cb; s_of = of;
+        }
+        __syncthreads();
+        r = s_r;
+        // U_core = [J_r; 0] (then Q_M applied), V_core = (G J)_r = G[:, ord]
+        for (int64_t e = threadIdx.x; e < (int64_t)m * r; e += NT) {
+            int64_t i = e % m;
+            int c = (int)(e / m);
+            int src = w.ord[c];
+            U[i + ldo * c] = (i < rq) ? w.J[i + (int64_t)rq * src] : 0.0;
+            V[i + ldo * c] = (i < K) ? w.G[i + (int64_t)K * src] : 0.0;
+        }
+    } else {
+        if (threadIdx.x == 0) {
+            int rr = rq, of = 0;
+            if (rr > rlim) { rr = rlim; of = 1; }
+            s_r = rr; s_cb = 0; s_of = of;
+        }
+        __syncthreads();
+        r = s_r;
+        for (int64_t e = threadIdx.x; e < (int64_t)m * r; e += NT) {
+            int64_t i = e % m;
+            int c = (int)(e / m);
+            U[i + ldo * c] = (i == c) ? 1.0 : 0.0;
+            V[i + ldo * c] = (i < K) ? w.G[i + (int64_t)K * c] : 0.0;
+        }
     }
     __syncthreads();
-    __shared__ int s_r, s_cb, s_of;
-    if (threadIdx.x == 0) {
-        double s1 = w.sig[w.ord[0]];
-        int r = 0;
-        if (s1 > 0.0)
-            while (r < R && w.sig[w.ord[r]] > eps * s1) ++r;
-        int cb = 0, of = 0;
-        if (kmax > 0 && r > kmax) { r = kmax; cb = 1; }
-        if (r > kcap) { r = kcap; of = (kmax == 0); }
-        s_r = r; s_cb = cb; s_of = of;
-    }
-    __syncthreads();
-    const int r = s_r;
-    // U = Q_X [ (M J)_r ; 0 ],  V = Q_Y [ J_r ; 0 ]
-    for (int64_t e = threadIdx.x; e < (int64_t)m * r; e += NT) {
-        int64_t i = e % m;
-        int c = (int)(e / m);
-        int src = w.ord[c];
-        U[i + ldo * c] = (i < R) ? w.M[i + R * src] : 0.0;
-        V[i + ldo * c] = (i < R) ? w.J[i + R * src] : 0.0;
-    }
-    __syncthreads();
+    // U <- Q_M U (reflectors of the pivoted QR of M, rows < K)
+    qr_apply_q(w.M, K, K, rq, w.tm, U, ldo, r);
     qr_apply_q(w.X, m, m, R, w.tx, U, ldo, r);
     qr_apply_q(w.Y, m, m, R, w.ty, V, ldo, r);
     if (threadIdx.x == 0) { *cap_bound = s_cb; *overflow = s_of; }

@@ -7,12 +7,12 @@
 //  A2 block tree     — Def. A.2 son rule with the admissibility
 //                      TStdGeomAdmCond(2.0, use_min_diam):
 //                      min(diam tau, diam sigma) <= eta * dist(tau, sigma), dist > 0.
-//  A7 schedule       — lazy, column-oriented (left-looking) H-Cholesky, DESIGN.md Sec. 4.
+//  A3-A9 task DAG    — assembly, lazy column-oriented (left-looking) H-Cholesky and forward
+//                      H-solve as a dependency graph of small tasks.
 #include "plan.h"
 
 #include <algorithm>
 #include <cmath>
-#include <functional>
 #include <limits>
 #include <numeric>
 #include <unordered_map>
@@ -20,47 +20,55 @@
 namespace {
 
 inline int64_t heap_id(int l, int64_t c) { return ((int64_t)1 << l) - 1 + c; }
-inline uint64_t node_key(int l, int64_t i, int64_t j) {
+inline uint64_t node_key(int l, int64_t i, int64_t j)
+{
     return ((uint64_t)l << 58) | ((uint64_t)i << 29) | (uint64_t)j;
 }
 
 struct Builder {
     Plan &P;
+    const PlanOpts &O;
     int L;
     std::unordered_map<uint64_t, int32_t> key2node;
-    std::vector<std::vector<DTerm>> node_terms;
-    std::vector<int32_t> node_term_wave;
-    std::vector<int32_t> tile_wave, rfin_wave, rdone_wave, core_wave, phw_wave;
-    std::vector<int32_t> done_memo;
-    std::vector<std::vector<int32_t>> col;   // per cluster heap id: off-diagonal entries (node ids)
-    int32_t n_fac_u = 0;
+    std::vector<std::vector<int32_t>> node_terms;   // term ids per node
+    std::vector<std::vector<int32_t>> col;          // per cluster heap id: off-diagonal entries
+    std::vector<std::vector<int32_t>> rows;         // per leaf row: T/R nodes intersecting it (cols asc)
+    std::vector<std::vector<int32_t>> deps;         // per task
+    std::vector<int32_t> tile_fill, fin_tile, aca_task, rfin, rdone;
+    std::vector<int32_t> term_p0, term_p1;
+    int32_t root_solve = -1;
 
-    explicit Builder(Plan &p) : P(p), L(p.depth) {}
+    Builder(Plan &p, const PlanOpts &o) : P(p), O(o), L(p.depth) {}
 
-    double diam(int64_t h) const {
+    // ---------------------------------------------------------------- A2 geometry
+    double diam(int64_t h) const
+    {
         const double *b = &P.bb[4 * h];
         double dx = b[2] - b[0], dy = b[3] - b[1];
         return std::sqrt(dx * dx + dy * dy);
     }
-    double dist(int64_t h1, int64_t h2) const {
+    double dist(int64_t h1, int64_t h2) const
+    {
         const double *a = &P.bb[4 * h1], *b = &P.bb[4 * h2];
         double gx = std::max(0.0, std::max(a[0] - b[2], b[0] - a[2]));
         double gy = std::max(0.0, std::max(a[1] - b[3], b[1] - a[3]));
         return std::sqrt(gx * gx + gy * gy);
     }
-    bool admissible(int l, int64_t i, int64_t j) const {
-        if (P.eta <= 0.0) return false;
+    bool admissible(int l, int64_t i, int64_t j) const
+    {
+        if (O.eta <= 0.0) return false;
         int64_t hi = heap_id(l, i), hj = heap_id(l, j);
         double d = dist(hi, hj);
         if (!(d > 0.0)) return false;
-        return std::min(diam(hi), diam(hj)) <= P.eta * d;
+        return std::min(diam(hi), diam(hj)) <= O.eta * d;
     }
 
-    int32_t make(int l, int64_t i, int64_t j, int32_t parent, bool forced) {
+    int32_t make(int l, int64_t i, int64_t j, int32_t parent, bool forced)
+    {
         int32_t id = (int32_t)P.nodes.size();
         DNode nd{};
         nd.level = l; nd.i = (int32_t)i; nd.j = (int32_t)j;
-        nd.parent = parent; nd.idx = -1; nd.leaf_off = 0; nd.leaf_cnt = 0;
+        nd.parent = parent; nd.idx = -1;
         P.nodes.push_back(nd);
         for (int k = 0; k < 4; ++k) P.children.push_back(-1);
         key2node[node_key(l, i, j)] = id;
@@ -69,7 +77,7 @@ struct Builder {
             type = (l == L) ? ND_T : ND_H;
         } else {
             bool adm = !forced && admissible(l, i, j);
-            if (adm && l < L && P.cluster_size(l) > P.dense_below) type = ND_R;
+            if (adm && l < L && P.cluster_size(l) > O.dense_below) type = ND_R;
             else if (l == L) type = ND_T;
             else { type = ND_H; forced = forced || adm; }
         }
@@ -77,9 +85,10 @@ struct Builder {
         if (type == ND_T) {
             P.nodes[id].idx = (int32_t)P.tile_node.size();
             P.tile_node.push_back(id);
+            if (i == j) P.diag_tile[i] = P.nodes[id].idx;
         } else if (type == ND_R) {
             DRBlk r{};
-            r.node = id; r.level = l; r.m = (int32_t)P.cluster_size(l);
+            r.node = id; r.level = l; r.m = (int32_t)P.cluster_size(l); r.solve = -1;
             r.row0 = i * P.cluster_size(l); r.col0 = j * P.cluster_size(l);
             r.uv_off = P.uv_elems;
             P.uv_elems += r.m;
@@ -102,7 +111,8 @@ struct Builder {
         return id;
     }
 
-    int32_t owner(int l, int64_t i, int64_t j) const {
+    int32_t owner(int l, int64_t i, int64_t j) const
+    {
         while (true) {
             auto it = key2node.find(node_key(l, i, j));
             if (it != key2node.end()) return it->second;
@@ -110,40 +120,8 @@ struct Builder {
         }
     }
 
-    int32_t term_wave_chain(int32_t nd) const {
-        int32_t w = 0;
-        for (int32_t x = nd; x >= 0; x = P.nodes[x].parent) w = std::max(w, node_term_wave[x]);
-        return w;
-    }
-
-    int32_t done_wave(int32_t nd) {
-        if (done_memo[nd] >= 0) return done_memo[nd];
-        const DNode &x = P.nodes[nd];
-        int32_t w = 0;
-        if (x.type == ND_T) w = tile_wave[x.idx];
-        else if (x.type == ND_R) w = rdone_wave[x.idx];
-        else
-            for (int k = 0; k < 4; ++k) {
-                int32_t c = P.children[4 * nd + k];
-                if (c >= 0) w = std::max(w, done_wave(c));
-            }
-        done_memo[nd] = w;
-        return w;
-    }
-
-    int32_t emit(int32_t type, int32_t a, int32_t b, int32_t c, int32_t wave) {
-        P.tasks.push_back(DTask{type, a, b, c});
-        P.task_wave.push_back(wave);
-        P.n_waves = std::max(P.n_waves, wave + 1);
-        return wave;
-    }
-
-    void add_term(int32_t target_node, const DTerm &t, int32_t wave) {
-        node_terms[target_node].push_back(t);
-        node_term_wave[target_node] = std::max(node_term_wave[target_node], wave);
-    }
-
-    void collect_leaves(int32_t nd, std::vector<int32_t> &out) const {
+    void collect_leaves(int32_t nd, std::vector<int32_t> &out) const
+    {
         const DNode &x = P.nodes[nd];
         if (x.type != ND_H) { out.push_back(nd); return; }
         for (int k = 0; k < 4; ++k) {
@@ -152,19 +130,213 @@ struct Builder {
         }
     }
 
-    void post(int l, int64_t c) {
-        int64_t sig = heap_id(l, c);
-        int32_t beg_ops = (int32_t)P.ops.size();
+    int64_t col_start(int32_t nd) const { return (int64_t)P.nodes[nd].j * P.cluster_size(P.nodes[nd].level); }
+
+    // ---------------------------------------------------------------- DAG helpers
+    int32_t task(int32_t type, int32_t a, int32_t b, int32_t c, int32_t d, int32_t qcls, std::vector<int32_t> dp)
+    {
+        int32_t id = (int32_t)P.tasks.size();
+        P.tasks.push_back(DTask{type, a, b, c, d, qcls});
+        std::sort(dp.begin(), dp.end());
+        dp.erase(std::unique(dp.begin(), dp.end()), dp.end());
+        if (!dp.empty() && dp[0] < 0) dp.erase(dp.begin(), std::upper_bound(dp.begin(), dp.end(), -1));
+        deps.push_back(std::move(dp));
+        return id;
+    }
+    void add_term_prods(std::vector<int32_t> &dp, int32_t t) const
+    {
+        if (term_p0[t] >= 0) dp.push_back(term_p0[t]);
+        if (term_p1[t] >= 0) dp.push_back(term_p1[t]);
+    }
+    std::vector<int32_t> merged_terms(int32_t nd) const
+    {
+        std::vector<int32_t> v;
+        for (int32_t y = nd; y >= 0; y = P.nodes[y].parent)
+            v.insert(v.end(), node_terms[y].begin(), node_terms[y].end());
+        std::sort(v.begin(), v.end());
+        return v;
+    }
+    // Chunked chain over the merged term list of a leaf node; the last chunk is `fin_type`.
+    int32_t chain(int32_t nd, int32_t first_dep, int32_t app_type, int32_t fin_type, int32_t a, int32_t d,
+                  int32_t extra_dep, int32_t qcls)
+    {
+        std::vector<int32_t> tl = merged_terms(nd);
+        const int32_t base = (int32_t)P.xterm.size();
+        P.xterm.insert(P.xterm.end(), tl.begin(), tl.end());
+        const int k = (int)tl.size();
+        if (k == 0 && fin_type < 0) return first_dep;
+        // tiles: chunks of O.chunk terms (exact updates); low-rank blocks: one task (the
+        // accumulation stays in the task's scratch until the final truncation)
+        int nch = (app_type == TK_RAPP) ? 1 : std::max(1, (k + O.chunk - 1) / O.chunk);
+        int32_t prev = first_dep;
+        for (int q = 0; q < nch; ++q) {
+            int b = (int)((int64_t)k * q / nch), e = (int)((int64_t)k * (q + 1) / nch);
+            const bool last = (q == nch - 1);
+            std::vector<int32_t> dp{prev};
+            for (int z = b; z < e; ++z) add_term_prods(dp, tl[z]);
+            int32_t ty = app_type;
+            if (last && fin_type >= 0) { ty = fin_type; dp.push_back(extra_dep); }
+            prev = task(ty, a, base + b, base + e, d, qcls, dp);
+        }
+        return prev;
+    }
+
+    // ---------------------------------------------------------------- solves
+    struct SolveCtx {
+        int32_t s;
+        int64_t a, b;   // leaf range
+        std::vector<int32_t> seg;   // per leaf (local)
+        std::unordered_map<int64_t, int32_t> join;   // cluster heap id -> task
+        std::unordered_map<int32_t, int32_t> proj;   // R id -> task
+    };
+    int32_t join(SolveCtx &S, int lv, int64_t c)
+    {
+        if (lv == L) return S.seg[c - S.a];
+        int64_t h = heap_id(lv, c);
+        auto it = S.join.find(h);
+        if (it != S.join.end()) return it->second;
+        int32_t j0 = join(S, lv + 1, 2 * c), j1 = join(S, lv + 1, 2 * c + 1);
+        int32_t t = task(TK_NOP, 0, 0, 0, 0, 0, {j0, j1});
+        S.join[h] = t;
+        return t;
+    }
+    int32_t proj_task(SolveCtx &S, int32_t r)
+    {
+        auto it = S.proj.find(r);
+        if (it != S.proj.end()) return it->second;
+        const DRBlk &b = P.rblk[r];
+        const DSolve &sv = P.solves[S.s];
+        DSlot sl{P.slot_a, P.slot_b};
+        if (sv.rhs_cnt > 0) P.slot_a += sv.rhs_cnt; else P.slot_b += 1;
+        int32_t slot = (int32_t)P.slots.size();
+        P.slots.push_back(sl);
+        const int32_t tau = P.nodes[b.node].j;
+        int32_t t = task(TK_PROJ, S.s, r, slot, 0, 0, {rdone[r], rfin[r], join(S, b.level, tau)});
+        S.proj[r] = t;
+        return t;
+    }
+    // Y <- L_ss^{-1} Y on the diagonal block of cluster (l, c); returns the task after which Y is final.
+    int32_t build_solve(int l, int64_t c, const std::vector<int32_t> &rhs)
+    {
+        DSolve sv{};
+        sv.level = l; sv.c = (int32_t)c;
+        sv.rhs_off = (int32_t)P.solve_rhs.size();
+        sv.rhs_cnt = (int32_t)rhs.size();
+        sv.m = P.cluster_size(l);
+        sv.row0 = c * sv.m;
+        P.solve_rhs.insert(P.solve_rhs.end(), rhs.begin(), rhs.end());
+        SolveCtx S;
+        S.s = (int32_t)P.solves.size();
+        P.solves.push_back(sv);
+        S.a = c << (L - l);
+        S.b = (c + 1) << (L - l);
+        S.seg.assign(S.b - S.a, -1);
+        std::vector<int32_t> rhs_deps;
+        for (int32_t r : rhs) rhs_deps.push_back(rfin[r]);
+        for (int64_t i = S.a; i < S.b; ++i) {
+            std::vector<int32_t> dp(rhs_deps);
+            dp.push_back(fin_tile[P.diag_tile[i]]);
+            const int32_t cb = (int32_t)P.ctr.size();
+            for (int32_t nd : rows[i]) {
+                const DNode &x = P.nodes[nd];
+                if (x.type == ND_T) {
+                    if (x.j >= S.a && x.j < i) {
+                        P.ctr.push_back(DCtr{0, x.idx, x.j, 0});
+                        dp.push_back(fin_tile[x.idx]);
+                        dp.push_back(S.seg[x.j - S.a]);
+                    }
+                } else if (col_start(nd) >= S.a * HCOV_LEAF) {
+                    const int32_t r = x.idx;
+                    int32_t pt = proj_task(S, r);
+                    int32_t slot = P.tasks[pt].c;
+                    P.ctr.push_back(DCtr{1, r, slot, 0});
+                    dp.push_back(pt);
+                }
+            }
+            const int32_t ce = (int32_t)P.ctr.size();
+            S.seg[i - S.a] = task(TK_SEG, S.s, (int32_t)i, cb, ce, 0, dp);
+        }
+        return join(S, l, c);
+    }
+
+    // W = H_e * [V of partners]: PHWP per low-rank leaf of H_e, PHWR per leaf row of H_e.
+    int32_t build_phw(int32_t e, const std::vector<int32_t> &rents, int32_t col_off, int32_t solve_done)
+    {
+        const DNode h = P.nodes[e];
+        const int64_t m = P.cluster_size(h.level);
+        DPhw q{};
+        q.hnode = e;
+        q.part_off = col_off;
+        q.part_cnt = (int32_t)rents.size();
+        q.fac_base = (int32_t)P.fac_row0.size();
+        q.m = (int32_t)m;
+        q.w_off = P.w_elems;
+        P.w_elems += m * (int64_t)rents.size();
+        const int32_t qid = (int32_t)P.phw.size();
+        for (int p = 0; p < (int)rents.size(); ++p) {
+            P.fac_row0.push_back((int64_t)h.i * m);
+            P.fac_nrows.push_back((int32_t)m);
+            P.fac_rank_src.push_back(rents[p]);
+            P.fac_off.push_back(q.w_off + (int64_t)p * m);
+            P.fac_pool.push_back(1);
+        }
+        P.phw.push_back(q);
+        std::vector<int32_t> lv;
+        collect_leaves(e, lv);
+        std::unordered_map<int32_t, std::pair<int32_t, int32_t>> rq;   // R id -> (task, slot)
+        for (int32_t nd : lv) {
+            const DNode &x = P.nodes[nd];
+            if (x.type != ND_R) continue;
+            DSlot sl{P.slot_a, P.slot_b};
+            P.slot_a += (int64_t)rents.size();
+            int32_t slot = (int32_t)P.slots.size();
+            P.slots.push_back(sl);
+            int32_t t = task(TK_PHWP, qid, x.idx, slot, 0, 0, {rdone[x.idx], rfin[x.idx], solve_done});
+            rq[x.idx] = {t, slot};
+        }
+        const int64_t rho0 = (int64_t)h.i * m, sig0 = (int64_t)h.j * m;
+        std::vector<int32_t> rowt;
+        for (int64_t i = rho0 / HCOV_LEAF; i < (rho0 + m) / HCOV_LEAF; ++i) {
+            std::vector<int32_t> dp{solve_done};
+            const int32_t cb = (int32_t)P.ctr.size();
+            for (int32_t nd : rows[i]) {
+                const int64_t cs = col_start(nd);
+                if (cs < sig0 || cs >= sig0 + m) continue;
+                const DNode &x = P.nodes[nd];
+                if (x.type == ND_T) {
+                    P.ctr.push_back(DCtr{0, x.idx, x.j, 0});
+                    dp.push_back(fin_tile[x.idx]);
+                } else {
+                    auto pr = rq.at(x.idx);
+                    P.ctr.push_back(DCtr{1, x.idx, pr.second, 0});
+                    dp.push_back(pr.first);
+                }
+            }
+            const int32_t ce = (int32_t)P.ctr.size();
+            rowt.push_back(task(TK_PHWR, qid, (int32_t)i, cb, ce, 0, dp));
+        }
+        return task(TK_NOP, 0, 0, 0, 0, 0, rowt);
+    }
+
+    int32_t new_term(int32_t kind, int32_t a, int32_t b, int32_t core, int32_t p0, int32_t p1, int32_t owner_node)
+    {
+        int32_t id = (int32_t)P.terms.size();
+        P.terms.push_back(DTerm{kind, a, b, core});
+        term_p0.push_back(p0);
+        term_p1.push_back(p1);
+        node_terms[owner_node].push_back(id);
+        return id;
+    }
+
+    // ---------------------------------------------------------------- column processing
+    void post(int l, int64_t c)
+    {
         if (l < L) { post(l + 1, 2 * c); post(l + 1, 2 * c + 1); }
-        const int64_t m = P.cluster_size(l);
-        const int64_t start = c * m;
-        int32_t diag_tile = -1;
+        const int64_t sig = heap_id(l, c);
         if (l == L) {
-            int32_t d = key2node.at(node_key(L, c, c));
-            diag_tile = P.nodes[d].idx;
-            int32_t w = 1 + term_wave_chain(d);
-            tile_wave[diag_tile] = emit(TK_POTRF, d, diag_tile, 0, w);
-            P.ops.push_back(DOp{OP_TRSM, diag_tile, HCOV_LEAF, 0, start, start});
+            const int32_t d = key2node.at(node_key(L, c, c));
+            const int32_t t = P.nodes[d].idx;
+            fin_tile[t] = chain(d, tile_fill[t], TK_TAPP, TK_POTRF, t, -1, -1, 0);
         }
         std::vector<int32_t> &ents = col[sig];
         std::sort(ents.begin(), ents.end(), [&](int32_t a, int32_t b) { return P.nodes[a].i < P.nodes[b].i; });
@@ -172,114 +344,70 @@ struct Builder {
         for (int32_t e : ents) {
             const DNode &x = P.nodes[e];
             if (x.type == ND_T) {
-                int32_t w = 1 + std::max(term_wave_chain(e), tile_wave[diag_tile]);
-                tile_wave[x.idx] = emit(TK_TRSM, e, diag_tile, 0, w);
+                const int32_t dt = P.diag_tile[c];
+                fin_tile[x.idx] = chain(e, tile_fill[x.idx], TK_TAPP, TK_TRSM, x.idx, dt, fin_tile[dt], 0);
             } else if (x.type == ND_R) {
-                int32_t w = 1 + term_wave_chain(e);
-                rfin_wave[x.idx] = emit(TK_RFIN, e, 0, 0, w);
+                const int32_t qc = P.rblk[x.idx].m > O.big_m ? 1 : 0;
+                rfin[x.idx] = chain(e, aca_task[x.idx], TK_RAPP, -1, x.idx, 0, -1, qc);
                 rents.push_back(x.idx);
             }
         }
-        P.col_r_off[sig] = (int32_t)P.col_r.size();
-        for (int32_t r : rents) P.col_r.push_back(r);
-        P.col_r_off[sig + 1] = (int32_t)P.col_r.size();  // (fixed up below; off array is n_clusters+1)
+        const int32_t col_off = (int32_t)P.col_r_off[sig];
+        std::unordered_map<int32_t, int32_t> h2phw, h2done;
         if (!rents.empty()) {
-            int32_t dnode = key2node.at(node_key(l, c, c));
-            int32_t w = done_wave(dnode);
-            for (int32_t r : rents) w = std::max(w, rfin_wave[r]);
-            w = emit(TK_SOLVE, (int32_t)sig, 0, 0, w + 1);
-            for (int32_t r : rents) rdone_wave[r] = w;
-        }
-        for (int32_t e : ents) {
-            const DNode &x = P.nodes[e];
-            int64_t r0 = (int64_t)x.i * m;
-            if (x.type == ND_T) P.ops.push_back(DOp{OP_UPD_T, x.idx, (int32_t)m, 0, r0, start});
-            else if (x.type == ND_R) P.ops.push_back(DOp{OP_UPD_R, x.idx, (int32_t)m, 0, r0, start});
-        }
-        // PHW tasks: one per H entry when the column has R entries.
-        std::unordered_map<int32_t, int32_t> h2phw;
-        if (!rents.empty()) {
+            const int32_t s_id = (int32_t)P.solves.size();
+            for (int32_t r : rents) P.rblk[r].solve = s_id;
+            const int32_t done = build_solve(l, c, rents);
+            for (int32_t r : rents) rdone[r] = done;
             for (int32_t e : ents) {
                 if (P.nodes[e].type != ND_H) continue;
-                DPhw q{};
-                q.hnode = e;
-                q.part_off = P.col_r_off[sig];
-                q.part_cnt = (int32_t)rents.size();
-                q.fac_base = (int32_t)P.fac_row0.size();
-                q.m = (int32_t)m;
-                q.w_off = P.w_elems;
-                P.w_elems += m * (int64_t)rents.size();
-                for (int p = 0; p < (int)rents.size(); ++p) {
-                    P.fac_row0.push_back((int64_t)P.nodes[e].i * m);
-                    P.fac_nrows.push_back((int32_t)m);
-                    P.fac_rank_src.push_back(rents[p]);
-                    P.fac_off.push_back(q.w_off + (int64_t)p * m);
-                    P.fac_pool.push_back(1);
-                }
-                // flattened leaves of the H node
-                std::vector<int32_t> lv;
-                collect_leaves(e, lv);
-                P.nodes[e].leaf_off = (int32_t)P.hleaf.size();
-                P.nodes[e].leaf_cnt = (int32_t)lv.size();
-                P.hleaf.insert(P.hleaf.end(), lv.begin(), lv.end());
-                int32_t w = done_wave(e);
-                for (int32_t r : rents) w = std::max(w, rdone_wave[r]);
-                int32_t qid = (int32_t)P.phw.size();
-                P.phw.push_back(q);
-                phw_wave.push_back(emit(TK_PHW, e, qid, 0, w + 1));
-                h2phw[e] = qid;
+                h2phw[e] = (int32_t)P.phw.size();
+                h2done[e] = build_phw(e, rents, col_off, done);
             }
         }
-        // products among the entries of this column (lower: e1.i >= e2.i)
+        // Schur-complement terms L_{e1} L_{e2}^T (e1.i >= e2.i) onto the owner of (e1.i, e2.i)
         for (size_t a = 0; a < ents.size(); ++a) {
             for (size_t b = 0; b <= a; ++b) {
-                int32_t e1 = ents[a], e2 = ents[b];
+                const int32_t e1 = ents[a], e2 = ents[b];
                 const DNode &x1 = P.nodes[e1], &x2 = P.nodes[e2];
-                int t1 = x1.type, t2 = x2.type;
-                if (t1 == ND_H && t2 == ND_H) continue;
-                int32_t o = owner(l, x1.i, x2.i);
-                DTerm t{};
-                int32_t w;
+                const int t1 = x1.type, t2 = x2.type;
+                if (t1 == ND_H && t2 == ND_H) continue;   // resolved at the children's columns
+                const int32_t o = owner(l, x1.i, x2.i);
                 if (t1 == ND_T && t2 == ND_T) {
-                    t.kind = TM_TT; t.a = x1.idx; t.b = x2.idx; t.core = -1;
-                    w = std::max(tile_wave[x1.idx], tile_wave[x2.idx]);
+                    new_term(TM_TT, x1.idx, x2.idx, -1, fin_tile[x1.idx], fin_tile[x2.idx], o);
                 } else if (t1 == ND_R && t2 == ND_R) {
-                    int32_t core = P.n_cores++;
-                    int32_t wv = 1 + std::max(rdone_wave[x1.idx], rdone_wave[x2.idx]);
-                    core_wave.push_back(emit(TK_PRR, x1.idx, x2.idx, core, wv));
-                    t.kind = TM_LR; t.a = x1.idx; t.b = x2.idx; t.core = core;
-                    w = core_wave[core];
+                    const int32_t core = P.n_cores++;
+                    int32_t pt = task(TK_PRR, x1.idx, x2.idx, core, 0, 0, {rdone[x1.idx], rdone[x2.idx]});
+                    new_term(TM_LR, x1.idx, x2.idx, core, pt, -1, o);
                 } else if (t1 == ND_R && t2 == ND_H) {
-                    int32_t q = h2phw.at(e2);
-                    int p = (int)(std::find(rents.begin(), rents.end(), x1.idx) - rents.begin());
-                    t.kind = TM_LR; t.a = x1.idx; t.b = P.phw[q].fac_base + p; t.core = -1;
-                    w = phw_wave[q];
+                    const int32_t q = h2phw.at(e2);
+                    const int p = (int)(std::find(rents.begin(), rents.end(), x1.idx) - rents.begin());
+                    new_term(TM_LR, x1.idx, P.phw[q].fac_base + p, -1, h2done.at(e2), -1, o);
                 } else if (t1 == ND_H && t2 == ND_R) {
-                    int32_t q = h2phw.at(e1);
-                    int p = (int)(std::find(rents.begin(), rents.end(), x2.idx) - rents.begin());
-                    t.kind = TM_LR; t.a = P.phw[q].fac_base + p; t.b = x2.idx; t.core = -1;
-                    w = phw_wave[q];
-                } else {
-                    continue;  // impossible with same-level entries (T only at leaf level)
+                    const int32_t q = h2phw.at(e1);
+                    const int p = (int)(std::find(rents.begin(), rents.end(), x2.idx) - rents.begin());
+                    new_term(TM_LR, P.phw[q].fac_base + p, x2.idx, -1, h2done.at(e1), -1, o);
                 }
-                add_term(o, t, w);
+                // T x R, R x T cannot occur: entries of one column share the level, T only at level L
             }
         }
-        P.op_beg[sig] = beg_ops;
-        P.op_end[sig] = (int32_t)P.ops.size();
     }
 };
 
 }  // namespace
 
-int plan_build(Plan &P, const double *s, int64_t n, double eta, int dense_below) {
+int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
+{
     if (n <= 0) return 2;
     for (int64_t k = 0; k < 2 * n; ++k)
         if (!std::isfinite(s[k])) return 1;
+    P.opt = opt;
+    P.opt.dense_below = std::max(opt.dense_below, HCOV_LEAF);
+    P.opt.chunk = std::max(1, opt.chunk);
+    P.opt.fill_tiles = std::max(1, opt.fill_tiles);
     int L = 0;
     while (((int64_t)HCOV_LEAF << L) < n) ++L;
     P.n = n; P.depth = L; P.n_leaves = (int64_t)1 << L; P.n_pad = (int64_t)HCOV_LEAF << L;
-    P.eta = eta; P.dense_below = std::max(dense_below, HCOV_LEAF);
     P.n_clusters = ((int64_t)2 << L) - 1;
     P.bb.assign(4 * P.n_clusters, 0.0);
 
@@ -325,104 +453,121 @@ int plan_build(Plan &P, const double *s, int64_t n, double eta, int dense_below)
     }
 
     // ---- A2 -------------------------------------------------------------------------------
-    Builder B(P);
+    Builder B(P, P.opt);
+    P.diag_tile.assign(P.n_leaves, -1);
     B.make(0, 0, 0, -1, false);
     const size_t nn = P.nodes.size();
     B.node_terms.assign(nn, {});
-    B.node_term_wave.assign(nn, 0);
-    B.done_memo.assign(nn, -1);
-    B.tile_wave.assign(P.n_tiles(), 0);
-    B.rfin_wave.assign(P.n_r(), 0);
-    B.rdone_wave.assign(P.n_r(), 0);
     B.col.assign(P.n_clusters, {});
+    B.rows.assign(P.n_leaves, {});
     for (size_t k = 0; k < nn; ++k) {
         const DNode &x = P.nodes[k];
         if (x.i != x.j) B.col[heap_id(x.level, x.j)].push_back((int32_t)k);
+        if (x.type == ND_H) continue;
+        int64_t span = (int64_t)1 << (L - x.level);
+        for (int64_t seg = (int64_t)x.i * span; seg < (int64_t)(x.i + 1) * span; ++seg)
+            B.rows[seg].push_back((int32_t)k);
     }
+    for (auto &rw : B.rows)
+        std::sort(rw.begin(), rw.end(), [&](int32_t a, int32_t b) { return B.col_start(a) < B.col_start(b); });
+    // column R lists (CSR by heap id, rows ascending)
+    P.col_r_off.assign(P.n_clusters + 1, 0);
+    for (int64_t sig = 0; sig < P.n_clusters; ++sig) {
+        std::vector<int32_t> &e = B.col[sig];
+        std::sort(e.begin(), e.end(), [&](int32_t a, int32_t b) { return P.nodes[a].i < P.nodes[b].i; });
+        P.col_r_off[sig] = (int32_t)P.col_r.size();
+        for (int32_t k : e)
+            if (P.nodes[k].type == ND_R) P.col_r.push_back(P.nodes[k].idx);
+    }
+    P.col_r_off[P.n_clusters] = (int32_t)P.col_r.size();
     // factor table part 1: U of R blocks
-    for (const DRBlk &r : P.rblk) {
-        P.fac_row0.push_back(r.row0);
-        P.fac_nrows.push_back(r.m);
-        P.fac_rank_src.push_back((int32_t)(&r - &P.rblk[0]));
-        P.fac_off.push_back(r.uv_off);
+    for (size_t r = 0; r < P.rblk.size(); ++r) {
+        P.fac_row0.push_back(P.rblk[r].row0);
+        P.fac_nrows.push_back(P.rblk[r].m);
+        P.fac_rank_src.push_back((int32_t)r);
+        P.fac_off.push_back(P.rblk[r].uv_off);
         P.fac_pool.push_back(0);
     }
 
-    // ---- A7 schedule (post-order over clusters) -------------------------------------------
-    P.col_r_off.assign(P.n_clusters + 1, 0);
-    P.op_beg.assign(P.n_clusters, 0);
-    P.op_end.assign(P.n_clusters, 0);
-    // col_r_off is written as [off(s), off(s)+cnt) at visit time; keep explicit counts instead
-    std::vector<int32_t> col_cnt(P.n_clusters, 0);
-    {
-        // post() writes col_r_off[sig] and col_r_off[sig+1]; since visits are not in heap-id
-        // order, record counts separately.
-        B.post(0, 0);
+    // ---- A3-A6: assembly tasks (roots) ------------------------------------------------------
+    const int64_t nt = P.n_tiles(), nr = P.n_r();
+    B.tile_fill.assign(nt, -1);
+    B.fin_tile.assign(nt, -1);
+    B.aca_task.assign(nr, -1);
+    B.rfin.assign(nr, -1);
+    B.rdone.assign(nr, -1);
+    for (int64_t t0 = 0; t0 < nt; t0 += P.opt.fill_tiles) {
+        int32_t cnt = (int32_t)std::min<int64_t>(P.opt.fill_tiles, nt - t0);
+        int32_t id = B.task(TK_FILL, (int32_t)t0, cnt, 0, 0, 0, {});
+        for (int64_t t = t0; t < t0 + cnt; ++t) B.tile_fill[t] = id;
     }
-    // recompute col_r_off as a proper CSR in heap-id order
-    {
-        std::vector<std::vector<int32_t>> per(P.n_clusters);
-        for (int64_t sig = 0; sig < P.n_clusters; ++sig) {
-            for (int32_t e : B.col[sig])
-                if (P.nodes[e].type == ND_R) per[sig].push_back(P.nodes[e].idx);
-        }
-        // the PHW partner lists referenced the visit-order offsets; rebuild both consistently
-        std::vector<int32_t> newcol;
-        std::vector<int32_t> newoff(P.n_clusters + 1, 0);
-        for (int64_t sig = 0; sig < P.n_clusters; ++sig) {
-            newoff[sig] = (int32_t)newcol.size();
-            newcol.insert(newcol.end(), per[sig].begin(), per[sig].end());
-        }
-        newoff[P.n_clusters] = (int32_t)newcol.size();
-        for (DPhw &q : P.phw) {
-            const DNode &h = P.nodes[q.hnode];
-            q.part_off = newoff[heap_id(h.level, h.j)];
-        }
-        P.col_r.swap(newcol);
-        P.col_r_off.swap(newoff);
-    }
-    P.phw_part = P.col_r;
+    for (int64_t r = 0; r < nr; ++r)
+        B.aca_task[r] = B.task(TK_ACA, (int32_t)r, 0, 0, 0, P.rblk[r].m > P.opt.big_m ? 1 : 0, {});
 
-    // flatten terms
-    P.terms.clear();
-    for (size_t k = 0; k < nn; ++k) {
-        P.nodes[k].term_off = (int32_t)P.terms.size();
-        P.nodes[k].term_cnt = (int32_t)B.node_terms[k].size();
-        P.terms.insert(P.terms.end(), B.node_terms[k].begin(), B.node_terms[k].end());
-    }
-    // waves: sort tasks by (wave, type)
-    std::vector<int32_t> idx(P.tasks.size());
-    std::iota(idx.begin(), idx.end(), 0);
-    std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
-        if (P.task_wave[a] != P.task_wave[b]) return P.task_wave[a] < P.task_wave[b];
-        return P.tasks[a].type < P.tasks[b].type;
-    });
-    P.wave_tasks = idx;
-    P.wave_off.assign(P.n_waves + 1, 0);
-    for (int32_t t : idx) P.wave_off[P.task_wave[t] + 1]++;
-    for (int32_t w = 0; w < P.n_waves; ++w) P.wave_off[w + 1] += P.wave_off[w];
+    // ---- A7: lazy column H-Cholesky; A9: root forward solve --------------------------------
+    B.post(0, 0);
+    const int32_t first_root_task = (int32_t)P.tasks.size();
+    B.root_solve = (int32_t)P.solves.size();
+    B.build_solve(0, 0, {});
 
-    // row lists: per leaf row segment, T/R nodes intersecting it (lower triangle incl. diag)
-    {
-        std::vector<std::vector<int32_t>> rows(P.n_leaves);
-        for (size_t k = 0; k < nn; ++k) {
-            const DNode &x = P.nodes[k];
-            if (x.type == ND_H) continue;
-            int64_t span = (int64_t)1 << (L - x.level);
-            for (int64_t seg = (int64_t)x.i * span; seg < (int64_t)(x.i + 1) * span; ++seg)
-                rows[seg].push_back((int32_t)k);
-        }
-        P.row_off.assign(P.n_leaves + 1, 0);
-        for (int64_t seg = 0; seg < P.n_leaves; ++seg) {
-            P.row_off[seg] = (int32_t)P.row_nodes.size();
-            // columns ascending
-            std::sort(rows[seg].begin(), rows[seg].end(), [&](int32_t a, int32_t b) {
-                const DNode &xa = P.nodes[a], &xb = P.nodes[b];
-                return ((int64_t)xa.j << (L - xa.level)) < ((int64_t)xb.j << (L - xb.level));
-            });
-            P.row_nodes.insert(P.row_nodes.end(), rows[seg].begin(), rows[seg].end());
-        }
-        P.row_off[P.n_leaves] = (int32_t)P.row_nodes.size();
+    // ---- DAG: phases, successors, per-mode in-degrees and roots, critical path ------------
+    const int32_t ntk = (int32_t)P.tasks.size();
+    P.root_solve = B.root_solve;
+    P.phase.assign(ntk, 1);
+    for (int32_t t = 0; t < ntk; ++t) {
+        const int ty = P.tasks[t].type;
+        if (ty == TK_FILL || ty == TK_ACA) P.phase[t] = 0;
+        else if (t >= first_root_task) P.phase[t] = 2;
     }
+    P.succ_off.assign(ntk + 1, 0);
+    for (int32_t t = 0; t < ntk; ++t)
+        for (int32_t d : B.deps[t]) P.succ_off[d + 1]++;
+    for (int32_t t = 0; t < ntk; ++t) P.succ_off[t + 1] += P.succ_off[t];
+    P.succ.assign(P.succ_off[ntk], 0);
+    {
+        std::vector<int32_t> fillp(P.succ_off.begin(), P.succ_off.end() - 1);
+        for (int32_t t = 0; t < ntk; ++t)
+            for (int32_t d : B.deps[t]) P.succ[fillp[d]++] = t;
+    }
+    std::vector<int32_t> len(ntk, 0);
+    std::vector<int64_t> key(ntk, 0);
+    P.crit_len = 0;
+    for (int32_t t = 0; t < ntk; ++t) {
+        const DTask &k = P.tasks[t];
+        int32_t lmax = 0;
+        for (int32_t d : B.deps[t]) lmax = std::max(lmax, len[d]);
+        len[t] = lmax + (k.type == TK_NOP ? 0 : 1);
+        P.crit_len = std::max(P.crit_len, len[t]);
+        if (k.type == TK_FILL) {
+            int64_t cmin = INT64_MAX;
+            for (int32_t q = k.a; q < k.a + k.b; ++q) cmin = std::min<int64_t>(cmin, P.nodes[P.tile_node[q]].j);
+            key[t] = cmin * HCOV_LEAF;
+        } else if (k.type == TK_ACA) {
+            key[t] = P.rblk[k.a].col0;
+        } else {
+            key[t] = (int64_t)1 << 40;   // non-assembly roots keep generation order
+        }
+    }
+    static const int mask[4] = {7, 1, 2, 4};
+    for (int md = 0; md < 4; ++md) {
+        P.indeg[md].assign(ntk, 0);
+        std::vector<std::pair<int64_t, int32_t>> rk[2];
+        for (int32_t t = 0; t < ntk; ++t) {
+            if (!(mask[md] & (1 << P.phase[t]))) continue;
+            int32_t cnt = 0;
+            for (int32_t d : B.deps[t])
+                if (mask[md] & (1 << P.phase[d])) ++cnt;
+            P.indeg[md][t] = cnt;
+            const DTask &k = P.tasks[t];
+            if (k.type != TK_NOP) P.n_q[md][k.qcls]++;
+            if (cnt == 0) rk[k.qcls].push_back({key[t], t});   // (a NOP always has a dependency)
+        }
+        for (int c = 0; c < 2; ++c) {
+            std::stable_sort(rk[c].begin(), rk[c].end());
+            P.roots[md][c].clear();
+            for (auto &pr : rk[c]) P.roots[md][c].push_back(pr.second);
+        }
+    }
+    for (const DRBlk &r : P.rblk) P.max_rm = std::max<int64_t>(P.max_rm, r.m);
     return 0;
 }

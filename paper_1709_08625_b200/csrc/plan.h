@@ -1,18 +1,26 @@
-// Host-side planner: cluster tree (A1), block tree (A2) and the theta-independent
-// lazy-column H-Cholesky task schedule (A7), see DESIGN.md "H-Cholesky formulation".
+// Host-side planner: cluster tree (A1), block tree (A2) and the theta-independent task DAG of
+// the assembly (A3-A6), the lazy left-looking H-Cholesky (A7) and the forward H-solve (A9).
+// See DESIGN.md "H-Cholesky formulation" and "Engine".
 #pragma once
 #include <cstdint>
 #include <vector>
 
 #include "hcov_internal.h"
 
+struct PlanOpts {
+    double eta = 2.0;
+    int dense_below = 32;   // admissible blocks of cluster size <= dense_below are dense tiles
+    int chunk = 4;          // pending terms applied per TAPP / RAPP task
+    int fill_tiles = 8;     // tiles per FILL task
+    int64_t big_m = 2048;   // ACA / RAPP tasks of blocks larger than this go to the big queue
+};
+
 struct Plan {
+    PlanOpts opt;
     // ---- A1: cluster tree -------------------------------------------------------------
     int64_t n = 0, n_pad = 0;
     int depth = 0;                  // L; leaves = 2^L clusters of 32 (padded) positions
     int64_t n_leaves = 0;
-    double eta = 2.0;
-    int dense_below = 32;
     std::vector<int64_t> perm_i2e;  // n_pad, -1 for phantom positions
     std::vector<double> xs, ys;     // n_pad internal coordinates (NaN for phantom)
     std::vector<double> bb;         // 4 per cluster heap id: lo_x, lo_y, hi_x, hi_y
@@ -23,35 +31,40 @@ struct Plan {
     std::vector<int32_t> tile_node;  // tile id -> node id
     std::vector<DRBlk> rblk;         // R id -> block
     std::vector<int32_t> children;   // 4 per node (-1 where absent); H nodes only
+    std::vector<int32_t> diag_tile;  // per leaf: tile id of its diagonal block
+    int64_t uv_elems = 0;            // U / V pool size per unit kcap
 
-    // ---- A7: schedule ------------------------------------------------------------------
-    std::vector<DTerm> terms;        // flattened by node (DNode::term_off/cnt)
-    std::vector<DTask> tasks;        // in generation (post-order) order
-    std::vector<int32_t> task_wave;  // wave (topological level) of each task
-    int32_t n_waves = 0;
-    std::vector<int32_t> wave_off;   // tasks sorted by (wave, type): wave w = [wave_off[w], wave_off[w+1])
-    std::vector<int32_t> wave_tasks; // task ids sorted by (wave, type, generation)
+    // ---- A7 / A9: terms, factors, products ---------------------------------------------
+    std::vector<DTerm> terms;
+    std::vector<int32_t> xterm_off;  // per tile (t) then per R (n_tiles + r): range in xterm[]
+    std::vector<int32_t> xterm;      // term ids (merged own + ancestor terms, generation order)
     std::vector<int32_t> col_r_off, col_r;   // per cluster heap id: R ids of its column entries
     std::vector<DPhw> phw;
-    std::vector<int32_t> phw_part;   // partner R ids
-    std::vector<int32_t> hleaf;      // flattened leaf node lists of H nodes used by PHW
-    int64_t w_elems = 0;             // W pool size in elements (per unit kcap: multiply by kcap)
+    int64_t w_elems = 0;             // W pool size per unit kcap
     int32_t n_cores = 0;
-    std::vector<int32_t> core_fac;   // unused placeholder (core dims come from factors)
-    // factors: [0, nR) = U of R blocks, [nR, nR + nW) = W slices
-    std::vector<int64_t> fac_row0;
+    std::vector<int64_t> fac_row0;   // factors: [0, nR) = U of R blocks, then W slices
     std::vector<int32_t> fac_nrows;
     std::vector<int32_t> fac_rank_src;  // R id whose rank is the factor's column count
-    std::vector<int64_t> fac_off;       // element offset in its pool (per unit kcap for W: col offset)
+    std::vector<int64_t> fac_off;       // element offset per unit kcap in its pool
     std::vector<int8_t> fac_pool;       // 0 = U pool, 1 = W pool
-    // forward-solve program
-    std::vector<DOp> ops;
-    std::vector<int32_t> op_beg, op_end;  // per cluster heap id
-    // row lists for the parallel forward solve / sampling: per leaf row, T/R nodes intersecting it
-    std::vector<int32_t> row_off, row_nodes;
-    // low-rank blocks in element units
-    int64_t uv_elems = 0;            // per unit kcap
-    int32_t max_m_rfin_small = 0;
+    std::vector<DSolve> solves;      // [0] = root forward solve
+    std::vector<int32_t> solve_rhs;
+    std::vector<DSlot> slots;        // PROJ / PHWP product slots
+    int64_t slot_a = 0, slot_b = 0;  // pool size = slot_a * kcap^2 + slot_b * kcap
+    std::vector<DCtr> ctr;           // SEG / PHWR contribution lists
+
+    // ---- DAG ---------------------------------------------------------------------------
+    // Engine modes: 0 = all phases (hcov_eval), 1 = assembly (A3-A6), 2 = H-Cholesky (A7),
+    // 3 = forward solve (A8-A9).  Phase of a task: 0 assembly, 1 Cholesky, 2 root solve.
+    std::vector<DTask> tasks;
+    std::vector<int8_t> phase;
+    std::vector<int32_t> succ_off, succ;
+    std::vector<int32_t> indeg[4];       // dependencies inside the mode, per task
+    std::vector<int32_t> roots[4][2];    // initial ready tasks per mode and queue class
+    int32_t n_q[4][2] = {};              // non-NOP tasks per mode and queue class
+    int32_t crit_len = 0;                // longest dependency chain (tasks, NOPs excluded)
+    int64_t max_rm = 0;                  // largest low-rank block
+    int32_t root_solve = -1;
 
     int64_t n_tiles() const { return (int64_t)tile_node.size(); }
     int64_t n_r() const { return (int64_t)rblk.size(); }
@@ -59,5 +72,5 @@ struct Plan {
 };
 
 // Build everything from host coordinates s (n x 2 row-major, external order).
-// Returns 0 on success, nonzero on invalid input.
-int plan_build(Plan &P, const double *s_host, int64_t n, double eta, int dense_below);
+// Returns 0 on success, 1 invalid input, 2 empty input.
+int plan_build(Plan &P, const double *s_host, int64_t n, const PlanOpts &opt);

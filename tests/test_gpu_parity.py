@@ -89,7 +89,7 @@ def test_near_full_rank_mode():
     Z = oracle.sample_dense(s, synth.xi(n, 12), *th)
     ref = oracle.loglik_dense(s, Z, *th)
     T = H.Tree(_dev(s))
-    r = H.eval_loglik(T, th, _dev(Z), eps=1e-13, kcap=128)
+    r = H.eval_loglik(T, th, _dev(Z), eps=1e-13, kcap=96)
     assert r["status"] == 0
     assert _rel(r["loglik"], ref[0]) <= 1e-9, (r, ref)
 

@@ -152,8 +152,16 @@ def test_invalid_inputs():
     assert e.value.code == 1
 
 
-def test_schedule_depth_is_linear_in_leaves():
-    # critical path of the lazy column schedule: ~2 waves per diagonal leaf
+def test_task_dag_is_consistent():
+    # every task's arguments are in range; the DAG's longest chain grows ~linearly in the leaves
     for n in (2048, 16384):
-        info = H.Tree(synth.uniform_points(n, 3)).info()
-        assert info["n_waves"] <= 2.5 * info["n_leaves"] + 40
+        T = H.Tree(synth.uniform_points(n, 3))
+        info = T.info()
+        t = T.tasks()
+        assert t.shape[0] == info["n_tasks"]
+        assert set(np.unique(t[:, 0])) <= set(range(12))
+        assert set(np.unique(t[:, 1])) == {0, 1, 2}
+        # phases are ordered: assembly tasks first, the root forward solve last
+        ph = t[:, 1]
+        assert np.all(np.diff(ph[ph > 0]) >= 0)
+        assert info["n_waves"] <= 12 * info["n_leaves"] + 64
