@@ -104,6 +104,11 @@ hcov_status hcov_tree_blocks(hcov_tree t, int32_t *out4, int64_t cap, int64_t *c
  * type (0 FILL, 1 ACA, 2 TAPP, 3 POTRF, 4 TRSM, 5 RAPP, 6 SEG, 7 PROJ, 8 PRR, 9 PHWP, 10 PHWR,
  * 11 NOP), phase (0 assembly, 1 H-Cholesky, 2 forward solve), and the task arguments a, b, c, d. */
 hcov_status hcov_tree_tasks(hcov_tree t, int32_t *out6, int64_t cap, int64_t *count);
+/* DAG successors (diagnostics): off has n_tasks + 1 entries, succ has *count entries (CSR).
+ * With off == NULL or succ == NULL only *count is set.  Setting the environment variable
+ * HCOV_TIMELINE=<file> makes every engine launch write (start_ns, end_ns, cta) as 3 uint64 per
+ * task (0 for tasks outside the launched mode) to <file>. */
+hcov_status hcov_tree_succ(hcov_tree t, int32_t *off, int32_t *succ, int64_t cap, int64_t *count);
 /* Cluster bounding boxes, 4 doubles per cluster heap id (2^l - 1 + c): lo_x, lo_y, hi_x, hi_y. */
 hcov_status hcov_tree_bbox(hcov_tree t, double *bb, int64_t cap);
 /* perm_i2e: n_pad int64 (host); entry k = external index of internal position k, -1 for phantom rows. */

@@ -171,3 +171,23 @@ def loglik_ou_collinear(x, Z, sigma2, ell):
     logdet = n * np.log(sigma2) + float(np.sum(np.log(om)))
     quad = z[0] ** 2 / sigma2 + float(np.sum((z[1:] - rho * z[:-1]) ** 2 / (sigma2 * om)))
     return -0.5 * n * np.log(2.0 * np.pi) - 0.5 * logdet - 0.5 * quad, logdet, quad
+
+
+def sample_ou_collinear(x, xi, sigma2, ell):
+    """Exact draw Z ~ N(0, C) for the collinear exponential model (same setting as
+    loglik_ou_collinear): in sorted order Z_1 = sigma xi_1,
+    Z_i = rho_i Z_{i-1} + sigma sqrt(1 - rho_i^2) xi_i.  Returned in the input order."""
+    x = np.asarray(x, dtype=np.float64)
+    xi = np.asarray(xi, dtype=np.float64)
+    o = np.argsort(x, kind="stable")
+    xs = x[o]
+    d = np.diff(xs)
+    rho = np.exp(-d / ell)
+    sd = np.sqrt(sigma2 * -np.expm1(-2.0 * d / ell))
+    z = np.empty_like(xs)
+    z[0] = np.sqrt(sigma2) * xi[o[0]]
+    for i in range(1, xs.size):
+        z[i] = rho[i - 1] * z[i - 1] + sd[i - 1] * xi[o[i]]
+    out = np.empty_like(z)
+    out[o] = z
+    return out

@@ -72,6 +72,7 @@ _SIGS = {
     "hcov_tree_blocks": (_I32, [_P, _P, _I64, _P]),
     "hcov_tree_bbox": (_I32, [_P, _P, _I64]),
     "hcov_tree_tasks": (_I32, [_P, _P, _I64, _P]),
+    "hcov_tree_succ": (_I32, [_P, _P, _P, _I64, _P]),
     "hcov_tree_perm": (_I32, [_P, _P]),
     "hcov_assemble": (_I32, [_P, _P, _P, _P, _P]),
     "hcov_cholesky": (_I32, [_P, _P, _P]),
@@ -179,6 +180,16 @@ class Tree:
         out = np.empty((cnt.value, 6), dtype=np.int32)
         _check(lib().hcov_tree_tasks(self._h, out.ctypes.data, cnt.value, ctypes.byref(cnt)), "hcov_tree_tasks")
         return out
+
+    def succ(self):
+        """hcov_tree_succ: (off[n_tasks + 1], succ[]) CSR of the task DAG."""
+        cnt = ctypes.c_int64()
+        _check(lib().hcov_tree_succ(self._h, None, None, 0, ctypes.byref(cnt)), "hcov_tree_succ")
+        off = np.empty(self.info()["n_tasks"] + 1, dtype=np.int32)
+        sc = np.empty(max(1, cnt.value), dtype=np.int32)
+        _check(lib().hcov_tree_succ(self._h, off.ctypes.data, sc.ctypes.data, sc.size, ctypes.byref(cnt)),
+               "hcov_tree_succ")
+        return off, sc[:cnt.value]
 
     def bbox(self) -> np.ndarray:
         d = self.info()["depth"]

@@ -53,11 +53,15 @@ struct Ctx {
     MaternParams mp;
     // ---- engine ----
     int32_t *indeg;            // working copy of the in-degrees
-    int32_t *queue[2];
-    uint32_t *qctl;            // [0,1] head per queue, [2,3] tail per queue, [4] abort
+    int32_t *queue[2];         // [0]: HCOV_BANDS priority rings (band_off), [1]: gang tickets
+    const int32_t *band_off;   // HCOV_BANDS + 1
+    uint32_t *qctl;            // see QC_* in hcov.cu
     int32_t nq[2];
-    int32_t nbig;              // CTAs serving queue 1
+    int32_t nbig;              // CTAs serving queue 1 (HCOV_GANG * HCOV_GANG_SLOTS)
     int32_t pad1;
+    int32_t *gbar;             // per-task gang barrier counters
+    int32_t *gslot;            // per-task: CTA index of the gang's member 0 (-1 until it joined)
+    int64_t gshared_off;       // offset (doubles) of the shared gang workspace in a gang CTA's scratch
     double *scr;               // per-CTA scratch (normal CTAs), scr_stride doubles each
     int64_t scr_stride;
     double *bscr;              // per-CTA scratch of the big CTAs
@@ -193,8 +197,11 @@ __host__ __device__ inline int kbuf_of(int kcap) { return 3 * kcap + 32; }
 __host__ __device__ inline int64_t task_scratch(int64_t m, int kcap)
 {
     int64_t K = kbuf_of(kcap);
-    return 4 * m * K + 3 * K * K + 8 * K + m / 8 + 64;
+    int64_t panels = 4 * m * K;
+    if (m <= HCOV_DENSE_MAX) panels = m * m + 4 * m * K;
+    return panels + 3 * K * K + 8 * K + m / 8 + 64;
 }
+
 
 __device__ __forceinline__ CompressWs make_ws(double *base, int64_t m, int K, double **X2, double **Y2)
 {
@@ -212,7 +219,8 @@ __device__ __forceinline__ CompressWs make_ws(double *base, int64_t m, int K, do
     w.sig = w.tm + K;
     w.cn = w.sig + K;
     w.ord = (int *)(w.cn + K);
-    w.piv = w.ord + K;
+    w.piv = (int *)(w.cn + 2 * K);
+    w.tail = w.cn + 3 * K;
     return w;
 }
 
@@ -237,24 +245,271 @@ __device__ __forceinline__ double compress_flops(int64_t m, int R, int r)
            2.0 * 4.0 * m * R * r;
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Gang tasks: HCOV_GANG CTAs cooperate on one big block.  The block's rows (and, for ACA, its
+// columns) are partitioned: member g owns rows [q0, q0 + mq) and keeps its panel rows in its own
+// CTA scratch; the small shared workspace (stacked R factors, cores, partials) lives in member
+// 0's scratch.  Members synchronise through a per-task counter.  Gangs are formed from
+// consecutive tickets of queue 1.
+struct Gang {
+    int g, G;
+    int32_t *bar;
+    int nb;
+    int64_t mq, q0;
+    double *shared;
+};
+__device__ __forceinline__ void gang_sync(Gang &gg)
+{
+    __syncthreads();
+    ++gg.nb;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(gg.bar, 1);
+        const int target = gg.nb * gg.G;
+        while (*(volatile int32_t *)gg.bar < target) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+struct GangWs {
+    double *RSX, *RSY;     // (G K) x K each, ld G*R
+    double *UC, *VC;       // (G K) x K each, ld G*R
+    double *tsx, *tsy;     // K each
+    double *pv;            // 2 x G partial values
+    int64_t *pi;           // 2 x G partial indices
+    double *ps;            // 2 x G x 2 partial sums
+    double *urow, *vrow;   // K each: published pivot row of U / pivot column of V (ACA)
+    int32_t *ires;         // [0] r, [1] cb, [2] of
+};
+__host__ __device__ inline int64_t gang_shared_doubles(int K, int G)
+{
+    return 4 * (int64_t)G * K * K + 4 * (int64_t)K + 8 * (int64_t)G + 64;
+}
+__device__ __forceinline__ GangWs make_gws(double *base, int K, int G)
+{
+    GangWs gw;
+    const int64_t GK = (int64_t)G * K;
+    gw.RSX = base;
+    gw.RSY = gw.RSX + GK * K;
+    gw.UC = gw.RSY + GK * K;
+    gw.VC = gw.UC + GK * K;
+    gw.tsx = gw.VC + GK * K;
+    gw.tsy = gw.tsx + K;
+    gw.urow = gw.tsy + K;
+    gw.vrow = gw.urow + K;
+    gw.pv = gw.vrow + K;
+    gw.pi = (int64_t *)(gw.pv + 2 * G);
+    gw.ps = (double *)(gw.pi + 2 * G);
+    gw.ires = (int32_t *)(gw.ps + 4 * G);
+    return gw;
+}
+
+// Gang truncation of X Y^T (m x m, R columns; member rows in the local panels w.X, w.Y with
+// ld mq >= R): local Householder QR per member (TSQR leaves), QR of the stacked R factors and the
+// core (compress_core) by member 0, then every member applies its local Q to its rows of the
+// result U, V (global, ld ldo, rows q0..q0+mq).
+__device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, int R, double eps, double tol_q,
+                             bool svd, int kmax, int rlim, double *U, double *V, int64_t ldo, int *cb, int *of,
+                             double *red, double *redv, int64_t *redi)
+{
+    if (R == 0) { *cb = 0; *of = 0; return 0; }
+    const int G = gg.G, g = gg.g;
+    const int64_t mq = gg.mq, q0 = gg.q0;
+    const int64_t GR = (int64_t)G * R;
+    qr_house(w.X, mq, mq, R, w.tx, red);
+    qr_house(w.Y, mq, mq, R, w.ty, red);
+    for (int e = threadIdx.x; e < R * R; e += NT) {
+        const int i = e % R, k = e / R;
+        __stcg(gw.RSX + (int64_t)g * R + i + GR * k, (k >= i) ? w.X[i + mq * k] : 0.0);
+        __stcg(gw.RSY + (int64_t)g * R + i + GR * k, (k >= i) ? w.Y[i + mq * k] : 0.0);
+    }
+    gang_sync(gg);
+    if (g == 0) {
+        qr_house(gw.RSX, GR, GR, R, gw.tsx, red);
+        qr_house(gw.RSY, GR, GR, R, gw.tsy, red);
+        int c1 = 0, o1 = 0;
+        const int r = compress_core(w, gw.RSX, GR, gw.RSY, GR, R, eps, tol_q, svd, kmax, rlim, gw.UC, gw.VC, GR, GR,
+                                    &c1, &o1, red, redv, redi);
+        qr_apply_q(gw.RSX, GR, GR, R, gw.tsx, gw.UC, GR, r);
+        qr_apply_q(gw.RSY, GR, GR, R, gw.tsy, gw.VC, GR, r);
+        if (threadIdx.x == 0) { gw.ires[0] = r; gw.ires[1] = c1; gw.ires[2] = o1; }
+    }
+    gang_sync(gg);
+    const int r = __ldcg(gw.ires);
+    *cb = __ldcg(gw.ires + 1);
+    *of = __ldcg(gw.ires + 2);
+    for (int64_t e = threadIdx.x; e < mq * r; e += NT) {
+        const int64_t i = e % mq;
+        const int c = (int)(e / mq);
+        U[q0 + i + ldo * c] = (i < R) ? __ldcg(gw.UC + (int64_t)g * R + i + GR * c) : 0.0;
+        V[q0 + i + ldo * c] = (i < R) ? __ldcg(gw.VC + (int64_t)g * R + i + GR * c) : 0.0;
+    }
+    __syncthreads();
+    qr_apply_q(w.X, mq, mq, R, w.tx, U + q0, ldo, r);
+    qr_apply_q(w.Y, mq, mq, R, w.ty, V + q0, ldo, r);
+    gang_sync(gg);
+    return r;
+}
+
+// Gang ACA (Alg. B.1) of a big admissible block with the readings of
+// aca_partial (first row 0, ties -> lowest index, scaled column, zero-row skip, stop at eps_aca).
+// Member g evaluates the columns j and rows i in [q0, q0 + mq) of each cross; the pivot row of U
+// and the pivot column of V are published through the shared workspace.  Ul, Vl: local panels
+// (mq x Kmax, ld mq).  Returns k.
+__device__ int gang_aca(const MaternParams &mp, const double *xs, const double *ys, int64_t R0, int64_t C0, int64_t m,
+                        double *Ul, double *Vl, uint8_t *used, int Kmax, double eps_aca, const GangWs &gw, Gang &gg,
+                        double *red, double *redv, int64_t *redi)
+{
+    const int G = gg.G, g = gg.g;
+    const int64_t mq = gg.mq, q0 = gg.q0;
+    for (int64_t i = threadIdx.x; i < mq; i += NT) used[i] = 0;
+    int64_t istar = 0;
+    int k = 0, par = 0;
+    double n1 = 0.0;
+    int64_t guard = 0;
+    gang_sync(gg);
+    while (k < Kmax && guard++ < m + Kmax) {
+        // row residual of row istar (U[istar, :k] published in urow)
+        const double xi = xs[R0 + istar], yi = ys[R0 + istar];
+        double *vk = Vl + mq * k;
+        double bv = 0.0;
+        int64_t bi = 0;
+        for (int64_t j = threadIdx.x; j < mq; j += NT) {
+            double a = hcov_cov_entry(mp, xi, yi, xs[C0 + q0 + j], ys[C0 + q0 + j], (R0 + istar) == (C0 + q0 + j));
+            for (int l = 0; l < k; ++l) a -= __ldcg(gw.urow + l) * Vl[j + mq * l];
+            vk[j] = a;
+            const double aa = fabs(a);
+            if (vi_better(aa, q0 + j, bv, bi)) { bv = aa; bi = q0 + j; }
+        }
+        ValIdx b = block_argmax(bv, bi, redv, redi);
+        if (threadIdx.x == 0) {
+            __stcg(gw.pv + par * G + g, b.v);
+            __stcg(gw.pi + par * G + g, b.i);
+        }
+        if (istar >= q0 && istar < q0 + mq && threadIdx.x == 0) used[istar - q0] = 1;
+        gang_sync(gg);
+        ValIdx best{__ldcg(gw.pv + par * G), __ldcg(gw.pi + par * G)};
+        for (int h = 1; h < G; ++h) {
+            double v2 = __ldcg(gw.pv + par * G + h);
+            int64_t i2 = __ldcg(gw.pi + par * G + h);
+            if (vi_better(v2, i2, best.v, best.i)) { best.v = v2; best.i = i2; }
+        }
+        par ^= 1;
+        if (!(best.v > 0.0)) {
+            // zero residual row: next unused row (lowest index)
+            int64_t cand = m;
+            for (int64_t i = threadIdx.x; i < mq; i += NT)
+                if (!used[i] && q0 + i < cand) cand = q0 + i;
+            ValIdx cmin = block_argmax(-(double)cand, cand, redv, redi);
+            if (threadIdx.x == 0) __stcg(gw.pi + par * G + g, cmin.i);
+            gang_sync(gg);
+            int64_t c2 = m;
+            for (int h = 0; h < G; ++h) c2 = min(c2, (int64_t)__ldcg(gw.pi + par * G + h));
+            par ^= 1;
+            if (c2 >= m) break;
+            istar = c2;
+            // publish U[istar, :k] (owner)
+            if (istar >= q0 && istar < q0 + mq)
+                for (int l = threadIdx.x; l < k; l += NT) __stcg(gw.urow + l, Ul[(istar - q0) + mq * l]);
+            gang_sync(gg);
+            continue;
+        }
+        const int64_t js = best.i;
+        // publish V[js, :k+1] (owner of column js)
+        if (js >= q0 && js < q0 + mq)
+            for (int l = threadIdx.x; l <= k; l += NT) __stcg(gw.vrow + l, Vl[(js - q0) + mq * l]);
+        gang_sync(gg);
+        const double piv = __ldcg(gw.vrow + k);
+        const double xj = xs[C0 + js], yj = ys[C0 + js];
+        double *uk = Ul + mq * k;
+        bv = -1.0;
+        bi = m;
+        double su = 0.0, sv = 0.0;
+        for (int64_t i = threadIdx.x; i < mq; i += NT) {
+            double cc = hcov_cov_entry(mp, xs[R0 + q0 + i], ys[R0 + q0 + i], xj, yj, (R0 + q0 + i) == (C0 + js));
+            for (int l = 0; l < k; ++l) cc -= Ul[i + mq * l] * __ldcg(gw.vrow + l);
+            const double u = cc / piv;
+            uk[i] = u;
+            su += u * u;
+            const double vv = vk[i];
+            sv += vv * vv;
+            if (!used[i]) {
+                const double aa = fabs(cc);
+                if (vi_better(aa, q0 + i, bv, bi)) { bv = aa; bi = q0 + i; }
+            }
+        }
+        su = block_sum(su, red);
+        sv = block_sum(sv, red);
+        ValIdx nb = block_argmax(bv, bi, redv, redi);
+        if (threadIdx.x == 0) {
+            __stcg(gw.pv + par * G + g, nb.v);
+            __stcg(gw.pi + par * G + g, nb.i);
+            __stcg(gw.ps + 2 * (par * G + g), su);
+            __stcg(gw.ps + 2 * (par * G + g) + 1, sv);
+        }
+        gang_sync(gg);
+        double tsu = 0.0, tsv = 0.0;
+        ValIdx nbest{-1.0, m};
+        for (int h = 0; h < G; ++h) {
+            tsu += __ldcg(gw.ps + 2 * (par * G + h));
+            tsv += __ldcg(gw.ps + 2 * (par * G + h) + 1);
+            double v2 = __ldcg(gw.pv + par * G + h);
+            int64_t i2 = __ldcg(gw.pi + par * G + h);
+            if (vi_better(v2, i2, nbest.v, nbest.i)) { nbest.v = v2; nbest.i = i2; }
+        }
+        par ^= 1;
+        ++k;
+        const double nn = sqrt(tsu) * sqrt(tsv);
+        bool stop = false;
+        if (k == 1) n1 = nn;
+        else if (nn <= eps_aca * n1) stop = true;
+        if (nbest.i >= m || nbest.v < 0.0) stop = true;
+        if (stop) break;
+        istar = nbest.i;
+        // publish U[istar, :k] (owner of row istar)
+        if (istar >= q0 && istar < q0 + mq)
+            for (int l = threadIdx.x; l < k; l += NT) __stcg(gw.urow + l, Ul[(istar - q0) + mq * l]);
+        gang_sync(gg);
+    }
+    gang_sync(gg);
+    return k;
+}
+
 // A5 + A6: ACA of the admissible block (Alg. B.1) to eps/10, then QR + SVD truncation to (eps, kmax).
+// gg == nullptr: one CTA; else one member of a gang (scr = this CTA's private scratch).
 __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *red, double *redv, int64_t *redi,
-                         double &fl_asm, double &fl_tr)
+                         double &fl_asm, double &fl_tr, Gang *gg)
 {
     const int r = tk.a;
     const DRBlk b = c.rblk[r];
     const int64_t m = b.m;
     const int K = aca_kmax(m, c.kcap);
+    const int KB = kbuf_of(c.kcap);
     double *X2, *Y2;
-    CompressWs w = make_ws(scr, m, kbuf_of(c.kcap), &X2, &Y2);
-    uint8_t *used = (uint8_t *)(w.piv + kbuf_of(c.kcap) + 2);
-    int k = aca_partial(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, K, 0.1 * c.eps, used, red, redv, redi);
-    int cb = 0, of = 0;
-    int rk = compress(w, m, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m, &cb, &of,
+    int cb = 0, of = 0, k, rk;
+    if (!gg) {
+        CompressWs w = make_ws(scr, m, KB, &X2, &Y2);
+        uint8_t *used = (uint8_t *)w.tail;
+        k = aca_partial(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, K, 0.1 * c.eps, used, red, redv, redi);
+        rk = compress(w, m, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m, &cb, &of,
                       red, redv, redi);
-    record_rank(c, r, rk, cb, of);
-    fl_asm += 2.0 * m * k;                       // kernel evaluations (rows + columns)
-    fl_tr += 2.0 * m * k * k + compress_flops(m, k, rk);
+        record_rank(c, r, rk, cb, of);
+    } else {
+        gg->mq = m / gg->G;
+        gg->q0 = (int64_t)gg->g * gg->mq;
+        CompressWs w = make_ws(scr, gg->mq, KB, &X2, &Y2);
+        GangWs gw = make_gws(gg->shared, KB, gg->G);
+        k = gang_aca(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, (uint8_t *)w.tail, K, 0.1 * c.eps, gw, *gg, red,
+                     redv, redi);
+        rk = gang_compress(w, gw, *gg, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m,
+                           &cb, &of, red, redv, redi);
+        if (gg->g == 0) record_rank(c, r, rk, cb, of);
+    }
+    const double share = gg ? 1.0 / gg->G : 1.0;
+    fl_asm += share * 2.0 * m * k;                       // kernel evaluations (rows + columns)
+    fl_tr += share * (2.0 * m * k * k + compress_flops(m, k, rk));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -298,7 +553,7 @@ __device__ void task_tile(const Ctx &c, const DTask &tk, double *smem, double &f
 // recompressed near-losslessly (pivoted QR at eps*1e-4, no SVD); at the end X Y^T is truncated
 // to (eps, kmax) by QR + SVD (A6; Remark 2).
 __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *red, double *redv, int64_t *redi,
-                          double &fl)
+                          double &fl, Gang *gg)
 {
     const int r = tk.a;
     const DRBlk blk = c.rblk[r];
@@ -310,19 +565,25 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
     const int K = kbuf_of(c.kcap);
     const int maxw = max(32, c.kcap);
     double *X2, *Y2;
-    CompressWs w = make_ws(scr, m, K, &X2, &Y2);
-    if (m <= K) {
-        // small block: exact dense accumulation S = U V^T - sum of terms, then X = S, Y = I
-        double *S = w.X;
+    if (gg) {
+        gg->mq = m / gg->G;
+        gg->q0 = (int64_t)gg->g * gg->mq;
+    }
+    if (m <= HCOV_DENSE_MAX) {
+        // small block: exact dense accumulation S = U V^T - sum of terms (m x m), fully pivoted
+        // cross approximation of S to 0.1 eps |S|_max / m (so |S - X Y^T|_2 <= 0.1 eps |S|_2), then
+        // QR + SVD truncation to (eps, kmax)
+        double *S = scr;
+        CompressWs wd = make_ws(scr + m * m, m, K, &X2, &Y2);   // X, Y panels (m x K) follow S
         for (int64_t e = threadIdx.x; e < m * m; e += NT) {
             const int64_t i = e % m, j = e / m;
             double sum = 0.0;
             for (int l = 0; l < r0; ++l) sum += __ldcg(U + i + m * l) * __ldcg(V + j + m * l);
             S[e] = sum;
-            w.Y[e] = (i == j) ? 1.0 : 0.0;
         }
         fl += 2.0 * m * m * r0;
         __syncthreads();
+        double *T1 = wd.Y;   // scratch for A K (m x rb), before Y is used by the ACA
         for (int kk = tk.b; kk < tk.c; ++kk) {
             const DTerm t = c.terms[c.xterm[kk]];
             if (t.kind == TM_TT) {
@@ -344,7 +605,6 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
                 const int64_t c_lo = max(C0, B.row0), c_hi = min(C0 + m, B.row0 + B.nrows);
                 const int64_t nr = r_hi - r_lo, nc = c_hi - c_lo;
                 const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcap * c.kcap : nullptr;
-                double *T1 = X2;   // nr x rb
                 for (int64_t e = threadIdx.x; e < nr * (int64_t)rb; e += NT) {
                     int64_t i = e % nr;
                     int b = (int)(e / nr);
@@ -369,14 +629,28 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
             }
             __syncthreads();
         }
-        int rk = compress(w, m, (int)m, c.eps, final_tol(c.eps, (int)m), true, c.kmax, c.kcap, U, V, m, &cb, &of,
-                          red, redv, redi);
-        fl += compress_flops(m, (int)m, rk);
+        const int KA = (int)(m < K ? m : K);
+        int k = aca_full(S, m, wd.X, wd.Y, KA, 0.1 * c.eps / (double)m, redv, redi);
+        fl += 2.0 * m * m * k;
+        if (k == KA && KA < m && threadIdx.x == 0) atomicAdd(c.flags + 3, 1);
+        int rk = compress(wd, m, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, U, V, m, &cb, &of, red, redv,
+                          redi);
+        fl += compress_flops(m, k, rk);
         record_rank(c, r, rk, cb, of);
         return;
     }
+    // factor mode (m > HCOV_DENSE_MAX); rows [q0, q0 + mq) belong to this CTA (the whole block
+    // without a gang); the panels w.X, w.Y, X2, Y2 hold those rows (ld mq).
+    CompressWs w = make_ws(scr, gg ? gg->mq : m, K, &X2, &Y2);
+    const int64_t mq = gg ? gg->mq : m, q0 = gg ? gg->q0 : 0;
+    GangWs gw{};
+    if (gg) gw = make_gws(gg->shared, K, gg->G);
     int cur = r0;
-    for (int64_t e = threadIdx.x; e < m * (int64_t)r0; e += NT) { w.X[e] = __ldcg(U + e); w.Y[e] = __ldcg(V + e); }
+    for (int64_t e = threadIdx.x; e < mq * (int64_t)r0; e += NT) {
+        const int64_t i = e % mq, l = e / mq;
+        w.X[i + mq * l] = __ldcg(U + q0 + i + m * l);
+        w.Y[i + mq * l] = __ldcg(V + q0 + i + m * l);
+    }
     __syncthreads();
     for (int kk = tk.b; kk < tk.c; ++kk) {
         const DTerm t = c.terms[c.xterm[kk]];
@@ -386,60 +660,87 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
         if (width == 0) continue;
         if (t.kind == TM_LR && __ldcg(c.rank + c.fac_rank_src[t.a]) == 0) continue;
         if (cur + width > K) {
-            int icb = 0, iof = 0;
-            int rk = compress(w, m, cur, c.eps, interm_tol(c.eps), false, 0, K - maxw, X2, Y2, m, &icb, &iof, red,
+            int icb = 0, iof = 0, rk;
+            if (gg)
+                rk = gang_compress(w, gw, *gg, cur, c.eps, interm_tol(c.eps), false, 0, K - maxw, X2 - q0, Y2 - q0, mq,
+                                   &icb, &iof, red, redv, redi);
+            else
+                rk = compress(w, m, cur, c.eps, interm_tol(c.eps), false, 0, K - maxw, X2, Y2, m, &icb, &iof, red,
                               redv, redi);
-            fl += compress_flops(m, cur, rk);
-            if (iof && threadIdx.x == 0) atomicAdd(c.flags + 3, 1);
+            fl += (gg ? 1.0 / gg->G : 1.0) * compress_flops(m, cur, rk);
+            if (iof && threadIdx.x == 0 && (!gg || gg->g == 0)) atomicAdd(c.flags + 3, 1);
             double *tx = w.X, *ty = w.Y;
             w.X = X2; w.Y = Y2; X2 = tx; Y2 = ty;
             cur = rk;
         }
-        double *xc = w.X + m * cur, *yc = w.Y + m * cur;
-        for (int64_t e = threadIdx.x; e < m * (int64_t)width; e += NT) { xc[e] = 0.0; yc[e] = 0.0; }
+        double *xc = w.X + mq * cur, *yc = w.Y + mq * cur;
+        for (int64_t e = threadIdx.x; e < mq * (int64_t)width; e += NT) { xc[e] = 0.0; yc[e] = 0.0; }
         __syncthreads();
         if (t.kind == TM_TT) {
             const DNode na = c.nodes[c.tile_node[t.a]], nb = c.nodes[c.tile_node[t.b]];
-            const int64_t ar = (int64_t)na.i * HCOV_LEAF - R0, br = (int64_t)nb.i * HCOV_LEAF - C0;
+            const int64_t ar = (int64_t)na.i * HCOV_LEAF - R0 - q0, br = (int64_t)nb.i * HCOV_LEAF - C0 - q0;
             const double *A = c.tiles + (int64_t)t.a * HCOV_TILE, *B = c.tiles + (int64_t)t.b * HCOV_TILE;
             for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
                 int i = e & 31, k = e >> 5;
-                xc[ar + i + m * k] = -__ldcg(A + e);
-                yc[br + i + m * k] = __ldcg(B + e);
+                if (ar + i >= 0 && ar + i < mq) xc[ar + i + mq * k] = -__ldcg(A + e);
+                if (br + i >= 0 && br + i < mq) yc[br + i + mq * k] = __ldcg(B + e);
             }
         } else {
             Fac A = get_fac(c, t.a), B = get_fac(c, t.b);
             const int ra = A.ncols, rb = B.ncols;
-            const int64_t r_lo = max(R0, A.row0), r_hi = min(R0 + m, A.row0 + A.nrows);
-            const int64_t c_lo = max(C0, B.row0), c_hi = min(C0 + m, B.row0 + B.nrows);
+            const int64_t r_lo = max(R0 + q0, A.row0), r_hi = min(R0 + q0 + mq, A.row0 + A.nrows);
+            const int64_t c_lo = max(C0 + q0, B.row0), c_hi = min(C0 + q0 + mq, B.row0 + B.nrows);
             const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcap * c.kcap : nullptr;
-            for (int64_t e = threadIdx.x; e < (r_hi - r_lo) * (int64_t)rb; e += NT) {
-                int64_t i = e % (r_hi - r_lo);
-                int b = (int)(e / (r_hi - r_lo));
-                double s;
-                if (Kc) {
-                    s = 0.0;
-                    for (int a = 0; a < ra; ++a)
-                        s += __ldcg(A.p + (r_lo - A.row0) + i + A.ld * a) * __ldcg(Kc + a + (int64_t)c.kcap * b);
-                } else {
-                    s = __ldcg(A.p + (r_lo - A.row0) + i + A.ld * b);
+            if (r_hi > r_lo) {
+                for (int64_t e = threadIdx.x; e < (r_hi - r_lo) * (int64_t)rb; e += NT) {
+                    int64_t i = e % (r_hi - r_lo);
+                    int b = (int)(e / (r_hi - r_lo));
+                    double sum;
+                    if (Kc) {
+                        sum = 0.0;
+                        for (int a = 0; a < ra; ++a)
+                            sum += __ldcg(A.p + (r_lo - A.row0) + i + A.ld * a) * __ldcg(Kc + a + (int64_t)c.kcap * b);
+                    } else {
+                        sum = __ldcg(A.p + (r_lo - A.row0) + i + A.ld * b);
+                    }
+                    xc[(r_lo - R0 - q0) + i + mq * b] = -sum;
                 }
-                xc[(r_lo - R0) + i + m * b] = -s;
+                if (Kc) fl += 2.0 * (r_hi - r_lo) * ra * rb;
             }
-            for (int64_t e = threadIdx.x; e < (c_hi - c_lo) * (int64_t)rb; e += NT) {
-                int64_t i = e % (c_hi - c_lo);
-                int b = (int)(e / (c_hi - c_lo));
-                yc[(c_lo - C0) + i + m * b] = __ldcg(B.p + (c_lo - B.row0) + i + B.ld * b);
-            }
-            if (Kc) fl += 2.0 * (r_hi - r_lo) * ra * rb;
+            if (c_hi > c_lo)
+                for (int64_t e = threadIdx.x; e < (c_hi - c_lo) * (int64_t)rb; e += NT) {
+                    int64_t i = e % (c_hi - c_lo);
+                    int b = (int)(e / (c_hi - c_lo));
+                    yc[(c_lo - C0 - q0) + i + mq * b] = __ldcg(B.p + (c_lo - B.row0) + i + B.ld * b);
+                }
         }
         __syncthreads();
         cur += width;
     }
-    int rk = compress(w, m, cur, c.eps, final_tol(c.eps, cur), true, c.kmax, c.kcap, U, V, m, &cb, &of, red, redv,
-                      redi);
-    fl += compress_flops(m, cur, rk);
-    record_rank(c, r, rk, cb, of);
+    // last chunk: truncation to (eps, kmax) into capacity kcap; else near-lossless into 2 kcap
+    const bool fin = (tk.d == 1);
+    const double tq = fin ? final_tol(c.eps, cur) : interm_tol(c.eps);
+    const int kmx = fin ? c.kmax : 0, rl = fin ? c.kcap : 2 * c.kcap;
+    int rk;
+    if (gg) {
+        rk = gang_compress(w, gw, *gg, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi);
+        fl += compress_flops(m, cur, rk) / gg->G;
+    } else {
+        rk = compress(w, m, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi);
+        fl += compress_flops(m, cur, rk);
+    }
+    if (!fin) {
+        if (of && threadIdx.x == 0 && (!gg || gg->g == 0)) atomicAdd(c.flags + 3, 1);
+        cb = 0;
+        of = 0;
+    }
+    if (!gg || gg->g == 0) {
+        if (fin) record_rank(c, r, rk, cb, of);
+        else {
+            if (threadIdx.x == 0) __stcg(c.rank + r, rk);
+            __syncthreads();
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -119,11 +119,26 @@ __device__ __forceinline__ unsigned long long gtimer()
 }
 __device__ __forceinline__ int ld_volatile(const int32_t *p) { return *(volatile const int32_t *)p; }
 
+// qctl layout
+#define QC_HEAD1 0      // gang queue: next ticket
+#define QC_TAIL1 1      // gang queue: published tickets
+#define QC_ABORT 2      // watchdog
+#define QC_DONE0 3      // completed queue-0 tasks
+#define QC_BHEAD 4      // HCOV_BANDS band heads
+#define QC_BTAIL (4 + HCOV_BANDS)
+#define QC_N (4 + 2 * HCOV_BANDS)
+
 __device__ __forceinline__ void push_ready(const Ctx &c, int32_t s)
 {
-    const int q = c.tasks[s].qcls;
-    const uint32_t pos = atomicAdd(c.qctl + 2 + q, 1u);
-    atomicExch(c.queue[q] + pos, s);
+    if (c.tasks[s].qcls == 0) {
+        const int b = c.tasks[s].band;
+        const uint32_t pos = atomicAdd(c.qctl + QC_BTAIL + b, 1u);
+        atomicExch(c.queue[0] + c.band_off[b] + pos, s);
+    } else {   // gang task of G CTAs: G consecutive tickets (task * 32 + member)
+        const int G = c.tasks[s].qcls;
+        const uint32_t pos = atomicAdd(c.qctl + QC_TAIL1, (uint32_t)G);
+        for (int g = 0; g < G; ++g) atomicExch(c.queue[1] + pos + g, s * 32 + g);
+    }
 }
 
 // Release the successors of task t (all threads of the CTA; NOP joins complete inline).
@@ -153,46 +168,97 @@ __device__ void release(const Ctx &c, int32_t t, int mask, const int8_t *phase)
     }
 }
 
-__global__ void __launch_bounds__(NT) k_engine(Ctx c, int mask, const int8_t *phase, EngineStats *stats)
+__global__ void __launch_bounds__(NT, 4) k_engine(Ctx c, int mask, const int8_t *phase, EngineStats *stats,
+                                               unsigned long long *tl)
 {
     extern __shared__ double smem[];
     __shared__ double red[NWARP], redv[NWARP];
     __shared__ int64_t redi[NWARP];
-    __shared__ int32_t s_task;
+    __shared__ int32_t s_task, s_member;
+    __shared__ uint32_t s_pos;
     const int q = (blockIdx.x < c.nbig) ? 1 : 0;
-    double *scr = q ? c.bscr + (int64_t)blockIdx.x * c.bscr_stride
-                    : c.scr + (int64_t)(blockIdx.x - c.nbig) * c.scr_stride;
+    double *scr = c.scr + (int64_t)(blockIdx.x - c.nbig) * c.scr_stride;
     double fl[FC_N] = {0, 0, 0, 0, 0};
     unsigned long long busy[TK_NTYPES] = {}, cnt[TK_NTYPES] = {};
     while (true) {
         if (threadIdx.x == 0) {
             int32_t t = -1;
-            const uint32_t pos = atomicAdd(c.qctl + q, 1u);
-            if (pos < (uint32_t)c.nq[q]) {
-                const unsigned long long t0 = gtimer();
-                unsigned ns = 32;
-                while ((t = ld_volatile(c.queue[q] + pos)) < 0) {
-                    if (ld_volatile((const int32_t *)c.qctl + 4)) { t = -1; break; }
+            uint32_t pos = 0;
+            const unsigned long long t0 = gtimer();
+            unsigned ns = 32;
+            if (q == 1) {
+                // gang queue: claim the next ticket, wait until it is published
+                pos = atomicAdd(c.qctl + QC_HEAD1, 1u);
+                if (pos < (uint32_t)c.nq[1]) {
+                    while ((t = ld_volatile(c.queue[1] + pos)) < 0) {
+                        if (ld_volatile((const int32_t *)c.qctl + QC_ABORT)) { t = -1; break; }
+                        __nanosleep(ns);
+                        if (ns < 256) ns <<= 1;
+                        if (gtimer() - t0 > c.timeout_ns) { atomicExch(c.qctl + QC_ABORT, 1u); t = -1; break; }
+                    }
+                }
+            } else {
+                // queue 0: take the head of the most urgent non-empty band (try-claim by CAS)
+                while (true) {
+                    if (ld_volatile((const int32_t *)c.qctl + QC_DONE0) >= c.nq[0]) break;
+                    if (ld_volatile((const int32_t *)c.qctl + QC_ABORT)) break;
+                    bool got = false;
+                    for (int b = HCOV_BANDS - 1; b >= 0 && !got; --b) {
+                        const int32_t base = c.band_off[b], cap = c.band_off[b + 1] - base;
+                        while (true) {
+                            const uint32_t h = (uint32_t)ld_volatile((const int32_t *)c.qctl + QC_BHEAD + b);
+                            if (h >= (uint32_t)cap) break;
+                            const int32_t v = ld_volatile(c.queue[0] + base + h);
+                            if (v < 0) break;
+                            if (atomicCAS(c.qctl + QC_BHEAD + b, h, h + 1) == h) { t = v; got = true; break; }
+                        }
+                    }
+                    if (got) break;
                     __nanosleep(ns);
                     if (ns < 256) ns <<= 1;
-                    if (gtimer() - t0 > c.timeout_ns) { atomicExch(c.qctl + 4, 1u); t = -1; break; }
+                    if (gtimer() - t0 > c.timeout_ns) { atomicExch(c.qctl + QC_ABORT, 1u); break; }
                 }
-                __threadfence();
             }
+            __threadfence();
+            s_member = 0;
+            if (q == 1 && t >= 0) { s_member = t & 31; t >>= 5; }
             s_task = t;
+            s_pos = pos;
         }
         __syncthreads();
         const int32_t t = s_task;
         if (t < 0) break;
         const DTask tk = c.tasks[t];
+        Gang gang{s_member, tk.qcls, c.gbar + t, 0, 0, 0, nullptr};
+        Gang *gg = nullptr;
+        double *tscr = scr;
+        if (q == 1) {
+            // member 0 (the first ticket of the gang) lends the shared workspace of its scratch
+            __shared__ int32_t s_cta0;
+            if (threadIdx.x == 0) {
+                if (gang.g == 0) {
+                    atomicExch(c.gslot + t, (int32_t)blockIdx.x);
+                    s_cta0 = blockIdx.x;
+                } else {
+                    int32_t v;
+                    while ((v = ld_volatile(c.gslot + t)) < 0) __nanosleep(64);
+                    s_cta0 = v;
+                }
+                __threadfence();
+            }
+            __syncthreads();
+            gg = &gang;
+            tscr = c.bscr + (int64_t)blockIdx.x * c.bscr_stride;
+            gang.shared = c.bscr + (int64_t)s_cta0 * c.bscr_stride + c.gshared_off;
+        }
         const unsigned long long t0 = gtimer();
         switch (tk.type) {
         case TK_FILL: task_fill(c, tk, fl[FC_ASM]); break;
-        case TK_ACA: task_aca(c, tk, scr, red, redv, redi, fl[FC_ASM], fl[FC_TRUNC]); break;
+        case TK_ACA: task_aca(c, tk, tscr, red, redv, redi, fl[FC_ASM], fl[FC_TRUNC], gg); break;
         case TK_TAPP:
         case TK_POTRF:
         case TK_TRSM: task_tile(c, tk, smem, fl[FC_TILE]); break;
-        case TK_RAPP: task_rapp(c, tk, scr, red, redv, redi, fl[FC_TRUNC]); break;
+        case TK_RAPP: task_rapp(c, tk, tscr, red, redv, redi, fl[FC_TRUNC], gg); break;
         case TK_SEG: task_seg(c, tk, smem, fl[FC_SOLVE]); break;
         case TK_PROJ: task_proj(c, tk, smem, fl[FC_SOLVE]); break;
         case TK_PRR: task_prr(c, tk, fl[FC_PROD]); break;
@@ -202,11 +268,19 @@ __global__ void __launch_bounds__(NT) k_engine(Ctx c, int mask, const int8_t *ph
         }
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) {
-            busy[tk.type] += gtimer() - t0;
-            cnt[tk.type] += 1;
+        if (gang.g == 0) {
+            if (threadIdx.x == 0) {
+                const unsigned long long t1 = gtimer();
+                busy[tk.type] += t1 - t0;
+                cnt[tk.type] += 1;
+                if (tl) { tl[3 * (int64_t)t] = t0; tl[3 * (int64_t)t + 1] = t1; tl[3 * (int64_t)t + 2] = blockIdx.x; }
+            }
+            release(c, t, mask, phase);
+            if (q == 0) {
+                __syncthreads();
+                if (threadIdx.x == 0) { __threadfence(); atomicAdd(c.qctl + QC_DONE0, 1u); }
+            }
         }
-        release(c, t, mask, phase);
         __syncthreads();
     }
     if (threadIdx.x == 0 && stats) {
@@ -221,18 +295,23 @@ __global__ void __launch_bounds__(NT) k_engine(Ctx c, int mask, const int8_t *ph
     }
 }
 
-__global__ void k_reset(Ctx c, const int32_t *indeg_mode, int64_t ntasks, const int32_t *roots0, int32_t nr0,
-                        const int32_t *roots1, int32_t nr1, int64_t qcap0, int64_t qcap1)
+__global__ void k_reset(Ctx c, const int32_t *indeg_mode, int64_t ntasks, const int32_t *q0init, int64_t q0len,
+                        const int32_t *q0tail, const int32_t *roots1, int32_t nr1, int64_t qcap1)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    for (int64_t k = tid; k < ntasks; k += stride) c.indeg[k] = indeg_mode[k];
-    for (int64_t k = tid; k < qcap0; k += stride) c.queue[0][k] = (k < nr0) ? roots0[k] : -1;
+    for (int64_t k = tid; k < ntasks; k += stride) {
+        c.indeg[k] = indeg_mode[k];
+        c.gbar[k] = 0;
+        c.gslot[k] = -1;
+    }
+    for (int64_t k = tid; k < q0len; k += stride) c.queue[0][k] = q0init[k];
     for (int64_t k = tid; k < qcap1; k += stride) c.queue[1][k] = (k < nr1) ? roots1[k] : -1;
-    if (tid == 0) {
-        c.qctl[0] = 0; c.qctl[1] = 0;
-        c.qctl[2] = (uint32_t)nr0; c.qctl[3] = (uint32_t)nr1;
-        c.qctl[4] = 0;
+    if (tid < QC_N) {
+        uint32_t v = 0;
+        if (tid == QC_TAIL1) v = (uint32_t)nr1;
+        if (tid >= QC_BTAIL && tid < QC_BTAIL + HCOV_BANDS) v = (uint32_t)q0tail[tid - QC_BTAIL];
+        c.qctl[tid] = v;
     }
 }
 
@@ -396,6 +475,8 @@ struct hcov_tree_s {
     int32_t *d_succ_off = nullptr, *d_succ = nullptr;
     int32_t *d_indeg[4] = {nullptr, nullptr, nullptr, nullptr};
     int32_t *d_roots[4][2] = {};
+    int32_t *d_q0init[4] = {}, *d_q0tail[4] = {};
+    int32_t *d_band_off = nullptr;
     int32_t *d_diag_tile = nullptr;
     double *d_xs = nullptr, *d_ys = nullptr;
     int64_t *d_perm_i2e = nullptr;
@@ -418,17 +499,17 @@ struct hcov_hmat_s {
     double *tiles = nullptr, *U = nullptr, *V = nullptr, *cores = nullptr, *W = nullptr, *P = nullptr;
     double *vbuf = nullptr, *logdet_part = nullptr, *minpiv_part = nullptr, *quad_part = nullptr;
     int32_t *rank = nullptr, *fail = nullptr, *flags = nullptr;
-    int32_t *indeg = nullptr, *q0 = nullptr, *q1 = nullptr;
+    int32_t *indeg = nullptr, *q0 = nullptr, *q1 = nullptr, *gbar = nullptr, *gslot = nullptr;
     uint32_t *qctl = nullptr;
     double *scr = nullptr, *bscr = nullptr, *res = nullptr, *res_host = nullptr;
     EngineStats *stats = nullptr, *stats_host = nullptr;
     void release_all()
     {
         void *ps[] = {tiles, U, V, cores, W, P, vbuf, logdet_part, minpiv_part, quad_part, rank, fail, flags,
-                      indeg, q0, q1, qctl, scr, bscr, res, stats};
+                      indeg, q0, q1, gbar, gslot, qctl, scr, bscr, res, stats};
         for (void *p : ps) cudaFree(p);
         tiles = U = V = cores = W = P = vbuf = logdet_part = minpiv_part = quad_part = nullptr;
-        rank = fail = flags = indeg = q0 = q1 = nullptr;
+        rank = fail = flags = indeg = q0 = q1 = gbar = gslot = nullptr;
         qctl = nullptr;
         scr = bscr = res = nullptr;
         stats = nullptr;
@@ -453,12 +534,15 @@ hcov_tree_s::~hcov_tree_s()
         cudaFree(d_indeg[m]);
         cudaFree(d_roots[m][0]);
         cudaFree(d_roots[m][1]);
+        cudaFree(d_q0init[m]);
+        cudaFree(d_q0tail[m]);
     }
+    cudaFree(d_band_off);
 }
 
 namespace {
 
-const int NBIG = 8;   // CTAs serving the big-block queue
+const int NBIG = HCOV_GANG_CTAS;   // CTAs serving the gang queue
 
 hcov_status tree_upload(hcov_tree t)
 {
@@ -488,7 +572,10 @@ hcov_status tree_upload(hcov_tree t)
         CK(upload(&t->d_indeg[m], P.indeg[m]));
         CK(upload(&t->d_roots[m][0], P.roots[m][0]));
         CK(upload(&t->d_roots[m][1], P.roots[m][1]));
+        CK(upload(&t->d_q0init[m], P.q0init[m]));
+        CK(upload(&t->d_q0tail[m], P.q0tail[m]));
     }
+    CK(upload(&t->d_band_off, P.band_off));
     CK(upload(&t->d_diag_tile, P.diag_tile));
     CK(upload(&t->d_xs, P.xs));
     CK(upload(&t->d_ys, P.ys));
@@ -522,7 +609,7 @@ hcov_status check_theta(const hcov_theta *th, const hcov_trunc *tr)
     if (!(th->sigma2 > 0) || !(th->ell > 0) || !(th->nu > 0) || !(th->nugget >= 0)) return HCOV_ERR_INVALID_ARG;
     if (!std::isfinite(th->sigma2) || !std::isfinite(th->ell) || !std::isfinite(th->nu) || !std::isfinite(th->nugget))
         return HCOV_ERR_INVALID_ARG;
-    if (!(tr->eps >= 0) || tr->kmax < 0 || tr->kcap < 0 || tr->kcap > 96) return HCOV_ERR_INVALID_ARG;
+    if (!(tr->eps >= 0) || tr->kmax < 0 || tr->kcap < 0 || tr->kcap > 64) return HCOV_ERR_INVALID_ARG;
     if (tr->kmax > 0 && tr->kcap > 0 && tr->kmax > tr->kcap) return HCOV_ERR_INVALID_ARG;
     return HCOV_OK;
 }
@@ -564,9 +651,11 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     CK(cudaMalloc(&h->flags, 4 * sizeof(int32_t)));
     const int64_t ntk = (int64_t)P.tasks.size();
     CK(cudaMalloc(&h->indeg, std::max<int64_t>(1, ntk) * sizeof(int32_t)));
-    CK(cudaMalloc(&h->q0, qcap(P, 0) * sizeof(int32_t)));
+    CK(cudaMalloc(&h->gbar, std::max<int64_t>(1, ntk) * sizeof(int32_t)));
+    CK(cudaMalloc(&h->gslot, std::max<int64_t>(1, ntk) * sizeof(int32_t)));
+    CK(cudaMalloc(&h->q0, std::max<int64_t>(1, P.band_off[HCOV_BANDS]) * sizeof(int32_t)));
     CK(cudaMalloc(&h->q1, qcap(P, 1) * sizeof(int32_t)));
-    CK(cudaMalloc(&h->qctl, 8 * sizeof(uint32_t)));
+    CK(cudaMalloc(&h->qctl, QC_N * sizeof(uint32_t)));
     CK(cudaMalloc(&h->res, 8 * sizeof(double)));
     CK(cudaMalloc(&h->stats, sizeof(EngineStats)));
     if (!h->res_host) CK(cudaMallocHost(&h->res_host, 8 * sizeof(double)));
@@ -579,15 +668,17 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engine, NT, (size_t)h->smem));
     occ = std::max(1, std::min(occ, 4));
     h->grid = nsm * occ;
-    const int64_t med_m = std::min<int64_t>(P.opt.big_m, std::max<int64_t>(P.max_rm, 32));
+    const int64_t med_m = std::min<int64_t>(HCOV_GANG_MIN / 2, std::max<int64_t>(P.max_rm, 32));
     const int64_t scr_stride = task_scratch(med_m, kcap);
     const int nnorm = h->grid - NBIG;
     CK(cudaMalloc(&h->scr, scr_stride * nnorm * sizeof(double)));
-    int64_t bscr_stride = 0;
-    if (P.max_rm > P.opt.big_m) {
-        bscr_stride = task_scratch(P.max_rm, kcap);
+    int64_t bscr_stride = 0, gshared_off = 0;
+    if (P.max_mq > 0) {
+        gshared_off = task_scratch(P.max_mq, kcap);
+        bscr_stride = gshared_off + gang_shared_doubles(kbuf_of(kcap), HCOV_GANG);
         CK(cudaMalloc(&h->bscr, bscr_stride * NBIG * sizeof(double)));
     }
+    h->ctx.gshared_off = gshared_off;
     h->ctx.scr_stride = scr_stride;
     h->ctx.bscr_stride = bscr_stride;
     h->kcap_alloc = kcap;
@@ -612,7 +703,9 @@ void fill_ctx(hcov_hmat h)
     c.fail_leaf = h->fail; c.flags = h->flags;
     c.kcap = h->kcap_alloc; c.kmax = h->trunc.kmax; c.eps = h->trunc.eps;
     c.mp = hcov_matern_params(h->theta.sigma2, h->theta.ell, h->theta.nu, h->theta.nugget);
-    c.indeg = h->indeg; c.queue[0] = h->q0; c.queue[1] = h->q1; c.qctl = h->qctl;
+    c.indeg = h->indeg; c.queue[0] = h->q0; c.queue[1] = h->q1; c.qctl = h->qctl; c.gbar = h->gbar;
+    c.band_off = t->d_band_off;
+    c.gslot = h->gslot;
     c.nbig = NBIG;
     c.scr = h->scr; c.bscr = h->bscr;
     c.flop = nullptr;
@@ -633,13 +726,30 @@ hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
     c.nq[0] = P.n_q[md][0];
     c.nq[1] = P.n_q[md][1];
     if (c.nq[0] + c.nq[1] == 0) return HCOV_OK;
-    LAUNCH(PC_RESET, st, k_reset<<<296, 256, 0, st>>>(c, t->d_indeg[md], ntk, t->d_roots[md][0],
-                                                     (int32_t)P.roots[md][0].size(), t->d_roots[md][1],
-                                                     (int32_t)P.roots[md][1].size(), qcap(P, 0), qcap(P, 1)));
+    LAUNCH(PC_RESET, st, k_reset<<<296, 256, 0, st>>>(c, t->d_indeg[md], ntk, t->d_q0init[md],
+                                                     (int64_t)P.band_off[HCOV_BANDS], t->d_q0tail[md],
+                                                     t->d_roots[md][1], (int32_t)P.roots[md][1].size(), qcap(P, 1)));
     EngineStats *stats = g_prof.events ? h->stats : nullptr;
     if (stats) CK(cudaMemsetAsync(h->stats, 0, sizeof(EngineStats), st));
-    LAUNCH(PC_ENGINE, st, k_engine<<<h->grid, NT, h->smem, st>>>(c, mask[md], t->d_phase, stats));
+    const char *tlpath = std::getenv("HCOV_TIMELINE");
+    unsigned long long *tl = nullptr;
+    if (tlpath) {
+        CK(cudaMalloc(&tl, 3 * std::max<int64_t>(1, ntk) * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(tl, 0, 3 * std::max<int64_t>(1, ntk) * sizeof(unsigned long long), st));
+    }
+    LAUNCH(PC_ENGINE, st, k_engine<<<h->grid, NT, h->smem, st>>>(c, mask[md], t->d_phase, stats, tl));
     CK(cudaGetLastError());
+    if (tl) {
+        std::vector<unsigned long long> hv(3 * ntk);
+        CK(cudaMemcpyAsync(hv.data(), tl, hv.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cudaFree(tl);
+        FILE *f = std::fopen(tlpath, "wb");
+        if (f) {
+            std::fwrite(hv.data(), 8, hv.size(), f);
+            std::fclose(f);
+        }
+    }
     if (stats) {
         CK(cudaMemcpyAsync(h->stats_host, h->stats, sizeof(EngineStats), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -673,7 +783,7 @@ hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trun
 hcov_status check_abort(hcov_hmat h, cudaStream_t st, int32_t *hf)
 {
     uint32_t ab = 0;
-    CK(cudaMemcpyAsync(&ab, h->qctl + 4, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ab, h->qctl + QC_ABORT, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf, h->fail, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf + 1, h->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -810,6 +920,18 @@ hcov_status hcov_tree_tasks(hcov_tree t, int32_t *out6, int64_t cap, int64_t *co
         int32_t *o = out6 + 6 * k;
         o[0] = tk.type; o[1] = P.phase[k]; o[2] = tk.a; o[3] = tk.b; o[4] = tk.c; o[5] = tk.d;
     }
+    return HCOV_OK;
+}
+
+hcov_status hcov_tree_succ(hcov_tree t, int32_t *off, int32_t *succ, int64_t cap, int64_t *count)
+{
+    if (!t || !count) return HCOV_ERR_INVALID_ARG;
+    const Plan &P = t->P;
+    *count = (int64_t)P.succ.size();
+    if (!off || !succ) return HCOV_OK;
+    if (cap < *count) return HCOV_ERR_INVALID_ARG;
+    std::memcpy(off, P.succ_off.data(), P.succ_off.size() * sizeof(int32_t));
+    std::memcpy(succ, P.succ.data(), P.succ.size() * sizeof(int32_t));
     return HCOV_OK;
 }
 

@@ -5,6 +5,10 @@
 
 #define HCOV_LEAF 32
 #define HCOV_TILE (HCOV_LEAF * HCOV_LEAF)
+#define HCOV_GANG 16          // largest gang: CTAs cooperating on one task of the gang queue (queue 1)
+#define HCOV_GANG_CTAS 64     // CTAs serving queue 1 (>= HCOV_GANG, so every gang can form)
+#define HCOV_DENSE_MAX 256    // low-rank blocks up to this size are recompressed from a dense accumulation
+#define HCOV_GANG_MIN 512     // low-rank blocks from this size on are processed by gangs of m/256 CTAs
 
 // Block-tree node types (lower triangle incl. diagonal).
 enum NodeType : int32_t { ND_H = 0, ND_R = 1, ND_T = 2 };
@@ -34,7 +38,7 @@ enum TaskType : int32_t {
     TK_TAPP = 2,   // a = tile, [b, c) = range of xterm[]: apply pending terms to the tile
     TK_POTRF = 3,  // a = diag tile, [b, c) terms: apply, then Cholesky + L^{-1} + log det partial (A7, A8)
     TK_TRSM = 4,   // a = tile, [b, c) terms, d = diag tile of its column: apply, then X <- X L^{-T}
-    TK_RAPP = 5,   // a = R id, [b, c) terms: append the terms' factors, recompress (A6 inside A7)
+    TK_RAPP = 5,   // a = R id, [b, c) terms, d = 1 on the last chunk: append the terms' factors, recompress
     TK_SEG = 6,    // a = solve id, b = leaf row segment, [c, d) = ctr[] contributions: forward solve rows
     TK_PROJ = 7,   // a = solve id, b = R id, c = proj slot: P = V_b^T Y[cols of b]
     TK_PRR = 8,    // a, b = R ids, c = core id: K = V_a^T V_b
@@ -46,8 +50,11 @@ enum TaskType : int32_t {
 struct DTask {
     int32_t type;
     int32_t a, b, c, d;
-    int32_t qcls;      // queue class: 0 = normal, 1 = big (needs a big scratch slot)
+    int32_t qcls;      // 0 = one CTA (queue 0); G > 1 = gang task of G CTAs (queue 1)
+    int32_t band;      // queue 0 priority band (HCOV_BANDS - 1 = most urgent), by the task's bottom level
+    int32_t pad;
 };
+#define HCOV_BANDS 16
 
 // Contribution of one block-tree leaf to a row segment in a SEG / PHWR task.
 //   kind 0: dense tile `id` (column segment aux);  kind 1: low-rank block `id`, product slot aux.
@@ -76,7 +83,8 @@ struct DRBlk {
     int32_t m;         // block size (rows = cols)
     int32_t solve;     // solve id of its column (the solve that finalises V)
     int64_t row0, col0;
-    int64_t uv_off;    // offset (elements per unit kcap) of U and V in the pools; each m x kcap col-major
+    int64_t uv_off;    // offset (elements per unit kcap) of U and V in the pools; m x kcap (m x 2 kcap if
+                       // m > HCOV_DENSE_MAX) col-major
 };
 
 // W = H * [V_partners] bookkeeping for an H entry of a column with low-rank entries.

@@ -291,36 +291,35 @@ struct CompressWs {
     double *tx, *ty, *tm;   // K each
     double *sig, *cn;   // K each
     int *ord, *piv;     // K each
+    double *tail;       // first free (8-byte aligned) double after the workspace
 };
 
-// Truncate X Y^T (m x m, rank <= R) to U V^T (A6):
-//   [Q_X, R_X] = qr(X), [Q_Y, R_Y] = qr(Y), M = R_X R_Y^T (R x R);
-//   M Pi = Q_M R_M by pivoted QR stopped at tol_q (rank-revealing pre-truncation, r' rows);
+// Core of the truncation (A6).  Input: upper-triangular R_X, R_Y (R x R, the
+// top R rows of RX / RY with leading dimensions ldx / ldy).
+//   M = R_X R_Y^T (R x R);  M Pi = Q_M R_M by pivoted QR stopped at tol_q (rank-revealing
+//   pre-truncation to r' rows);
 //   final (svd = true): SVD of the r' x R matrix B = R_M[:r'] Pi^T by one-sided Jacobi on B^T,
 //     keep the smallest r with sigma_{r+1} <= eps sigma_1, then r <= kmax (kmax > 0), r <= rlim;
-//     U = Q_X [Q_M [J_r; 0]; 0],  V = Q_Y [(B^T J)_r; 0];
-//   intermediate (svd = false): r = r', U = Q_X [Q_M [I; 0]; 0], V = Q_Y [B^T; 0].
-// U, V: m x r (ld ldo), must not alias X, Y.  Returns r.  *cap_bound = 1 if kmax cut below the
-// eps-rank, *overflow = 1 if the rank exceeded rlim with kmax == 0.
-__device__ int compress(const CompressWs &w, int64_t m, int R, double eps, double tol_q, bool svd, int kmax,
-                        int rlim, double *U, double *V, int64_t ldo, int *cap_bound, int *overflow, double *red,
-                        double *redv, int64_t *redi)
+//     U_core = Q_M [J_r; 0], V_core = (B^T J)_r;
+//   intermediate (svd = false): r = min(r', rlim), U_core = Q_M [I; 0], V_core = B^T[:, :r].
+// Writes U[0:nr, 0:r] = [U_core; 0] and V[0:nr, 0:r] = [V_core; 0] (ld ldo, nr >= R).  Returns r.
+// *cap_bound = 1 if kmax cut below the eps-rank; *overflow = 1 if the rank exceeded rlim
+// (with kmax == 0 for the final truncation).
+__device__ int compress_core(const CompressWs &w, const double *RX, int64_t ldx, const double *RY, int64_t ldy,
+                             int R, double eps, double tol_q, bool svd, int kmax, int rlim, double *U, double *V,
+                             int64_t ldo, int64_t nr, int *cap_bound, int *overflow, double *red, double *redv,
+                             int64_t *redi)
 {
     __shared__ int s_r, s_cb, s_of;
-    if (R == 0) { if (threadIdx.x == 0) { *cap_bound = 0; *overflow = 0; } __syncthreads(); return 0; }
-    qr_house(w.X, m, m, R, w.tx, red);
-    qr_house(w.Y, m, m, R, w.ty, red);
     const int K = R;
-    // M = R_X R_Y^T   (R_X[i,k] != 0 for k >= i)
     for (int e = threadIdx.x; e < K * K; e += NT) {
         int i = e % K, j = e / K;
         double s = 0.0;
-        for (int k = max(i, j); k < K; ++k) s += w.X[i + m * k] * w.Y[j + m * k];
+        for (int k = max(i, j); k < K; ++k) s += RX[i + ldx * k] * RY[j + ldy * k];
         w.M[e] = s;
     }
     __syncthreads();
     const int rq = qrcp_trunc(w.M, K, tol_q, svd ? K : rlim + 1, w.tm, w.piv, w.cn, redv, redi, red);
-    // B^T (K x rq): G[piv[k], i] = R_M[i, k] for k >= i
     for (int e = threadIdx.x; e < K * rq; e += NT) {
         int k = e % K, i = e / K;
         w.G[w.piv[k] + (int64_t)K * i] = (k >= i) ? w.M[i + (int64_t)K * k] : 0.0;
@@ -357,10 +356,9 @@ __device__ int compress(const CompressWs &w, int64_t m, int R, double eps, doubl
         }
         __syncthreads();
         r = s_r;
-        // U_core = [J_r; 0] (then Q_M applied), V_core = (G J)_r = G[:, ord]
-        for (int64_t e = threadIdx.x; e < (int64_t)m * r; e += NT) {
-            int64_t i = e % m;
-            int c = (int)(e / m);
+        for (int64_t e = threadIdx.x; e < nr * r; e += NT) {
+            int64_t i = e % nr;
+            int c = (int)(e / nr);
             int src = w.ord[c];
             U[i + ldo * c] = (i < rq) ? w.J[i + (int64_t)rq * src] : 0.0;
             V[i + ldo * c] = (i < K) ? w.G[i + (int64_t)K * src] : 0.0;
@@ -373,20 +371,34 @@ __device__ int compress(const CompressWs &w, int64_t m, int R, double eps, doubl
         }
         __syncthreads();
         r = s_r;
-        for (int64_t e = threadIdx.x; e < (int64_t)m * r; e += NT) {
-            int64_t i = e % m;
-            int c = (int)(e / m);
+        for (int64_t e = threadIdx.x; e < nr * r; e += NT) {
+            int64_t i = e % nr;
+            int c = (int)(e / nr);
             U[i + ldo * c] = (i == c) ? 1.0 : 0.0;
             V[i + ldo * c] = (i < K) ? w.G[i + (int64_t)K * c] : 0.0;
         }
     }
     __syncthreads();
-    // U <- Q_M U (reflectors of the pivoted QR of M, rows < K)
-    qr_apply_q(w.M, K, K, rq, w.tm, U, ldo, r);
-    qr_apply_q(w.X, m, m, R, w.tx, U, ldo, r);
-    qr_apply_q(w.Y, m, m, R, w.ty, V, ldo, r);
+    qr_apply_q(w.M, K, K, rq, w.tm, U, ldo, r);   // U_core <- Q_M U_core (rows < K)
     if (threadIdx.x == 0) { *cap_bound = s_cb; *overflow = s_of; }
     __syncthreads();
+    return r;
+}
+
+// Truncate X Y^T (m x m, rank <= R <= m) to U V^T: [Q_X, R_X] = qr(X), [Q_Y, R_Y] = qr(Y),
+// core as above, U = Q_X [U_core; 0], V = Q_Y [V_core; 0].  U, V: m x r (ld ldo), must not
+// alias X, Y.  Returns r.
+__device__ int compress(const CompressWs &w, int64_t m, int R, double eps, double tol_q, bool svd, int kmax,
+                        int rlim, double *U, double *V, int64_t ldo, int *cap_bound, int *overflow, double *red,
+                        double *redv, int64_t *redi)
+{
+    if (R == 0) { if (threadIdx.x == 0) { *cap_bound = 0; *overflow = 0; } __syncthreads(); return 0; }
+    qr_house(w.X, m, m, R, w.tx, red);
+    qr_house(w.Y, m, m, R, w.ty, red);
+    const int r = compress_core(w, w.X, m, w.Y, m, R, eps, tol_q, svd, kmax, rlim, U, V, ldo, m, cap_bound, overflow,
+                                red, redv, redi);
+    qr_apply_q(w.X, m, m, R, w.tx, U, ldo, r);
+    qr_apply_q(w.Y, m, m, R, w.ty, V, ldo, r);
     return r;
 }
 

@@ -19,6 +19,13 @@
 
 namespace {
 
+// gang size of an ACA / RAPP task of a low-rank block of size m (0 = a single CTA, queue 0)
+inline int32_t gang_of(int64_t m)
+{
+    if (m < HCOV_GANG_MIN) return 0;
+    return (int32_t)std::min<int64_t>(HCOV_GANG, m / 256);
+}
+
 inline int64_t heap_id(int l, int64_t c) { return ((int64_t)1 << l) - 1 + c; }
 inline uint64_t node_key(int l, int64_t i, int64_t j)
 {
@@ -91,7 +98,8 @@ struct Builder {
             r.node = id; r.level = l; r.m = (int32_t)P.cluster_size(l); r.solve = -1;
             r.row0 = i * P.cluster_size(l); r.col0 = j * P.cluster_size(l);
             r.uv_off = P.uv_elems;
-            P.uv_elems += r.m;
+            // capacity: kcap columns; 2 kcap for blocks recompressed in chunks (intermediate states)
+            P.uv_elems += (int64_t)r.m * (r.m > O.big_m ? 2 : 1);
             P.nodes[id].idx = (int32_t)P.rblk.size();
             P.rblk.push_back(r);
         } else {
@@ -136,7 +144,7 @@ struct Builder {
     int32_t task(int32_t type, int32_t a, int32_t b, int32_t c, int32_t d, int32_t qcls, std::vector<int32_t> dp)
     {
         int32_t id = (int32_t)P.tasks.size();
-        P.tasks.push_back(DTask{type, a, b, c, d, qcls});
+        P.tasks.push_back(DTask{type, a, b, c, d, qcls, 0, 0});
         std::sort(dp.begin(), dp.end());
         dp.erase(std::unique(dp.begin(), dp.end()), dp.end());
         if (!dp.empty() && dp[0] < 0) dp.erase(dp.begin(), std::upper_bound(dp.begin(), dp.end(), -1));
@@ -165,9 +173,12 @@ struct Builder {
         P.xterm.insert(P.xterm.end(), tl.begin(), tl.end());
         const int k = (int)tl.size();
         if (k == 0 && fin_type < 0) return first_dep;
-        // tiles: chunks of O.chunk terms (exact updates); low-rank blocks: one task (the
-        // accumulation stays in the task's scratch until the final truncation)
-        int nch = (app_type == TK_RAPP) ? 1 : std::max(1, (k + O.chunk - 1) / O.chunk);
+        // tiles: chunks of O.chunk terms (exact updates); small low-rank blocks: one task (exact
+        // dense accumulation); large low-rank blocks: chunks of O.rchunk terms, intermediate states
+        // kept near-losslessly at capacity 2 kcap, the last chunk truncates to (eps, kmax)
+        int nch = std::max(1, (k + O.chunk - 1) / O.chunk);
+        if (app_type == TK_RAPP)
+            nch = (P.rblk[a].m <= O.big_m) ? 1 : std::max(1, (k + O.rchunk - 1) / O.rchunk);
         int32_t prev = first_dep;
         for (int q = 0; q < nch; ++q) {
             int b = (int)((int64_t)k * q / nch), e = (int)((int64_t)k * (q + 1) / nch);
@@ -176,7 +187,8 @@ struct Builder {
             for (int z = b; z < e; ++z) add_term_prods(dp, tl[z]);
             int32_t ty = app_type;
             if (last && fin_type >= 0) { ty = fin_type; dp.push_back(extra_dep); }
-            prev = task(ty, a, base + b, base + e, d, qcls, dp);
+            const int32_t dd = (app_type == TK_RAPP) ? (last ? 1 : 0) : d;
+            prev = task(ty, a, base + b, base + e, dd, qcls, dp);
         }
         return prev;
     }
@@ -347,7 +359,7 @@ struct Builder {
                 const int32_t dt = P.diag_tile[c];
                 fin_tile[x.idx] = chain(e, tile_fill[x.idx], TK_TAPP, TK_TRSM, x.idx, dt, fin_tile[dt], 0);
             } else if (x.type == ND_R) {
-                const int32_t qc = P.rblk[x.idx].m > O.big_m ? 1 : 0;
+                const int32_t qc = gang_of(P.rblk[x.idx].m);
                 rfin[x.idx] = chain(e, aca_task[x.idx], TK_RAPP, -1, x.idx, 0, -1, qc);
                 rents.push_back(x.idx);
             }
@@ -502,7 +514,7 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
         for (int64_t t = t0; t < t0 + cnt; ++t) B.tile_fill[t] = id;
     }
     for (int64_t r = 0; r < nr; ++r)
-        B.aca_task[r] = B.task(TK_ACA, (int32_t)r, 0, 0, 0, P.rblk[r].m > P.opt.big_m ? 1 : 0, {});
+        B.aca_task[r] = B.task(TK_ACA, (int32_t)r, 0, 0, 0, gang_of(P.rblk[r].m), {});
 
     // ---- A7: lazy column H-Cholesky; A9: root forward solve --------------------------------
     B.post(0, 0);
@@ -548,6 +560,35 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
             key[t] = (int64_t)1 << 40;   // non-assembly roots keep generation order
         }
     }
+    // priority bands of queue 0: bottom level (longest remaining path, weighted by a rough
+    // per-type cost in units of ~25 us) quantised into HCOV_BANDS bands
+    {
+        std::vector<double> w(ntk, 1.0), bl(ntk, 0.0);
+        for (int32_t t = 0; t < ntk; ++t) {
+            const DTask &k = P.tasks[t];
+            if (k.type == TK_NOP) w[t] = 0.0;
+            else if (k.type == TK_RAPP || k.type == TK_ACA) {
+                const double m = (double)P.rblk[k.a].m;
+                w[t] = (m <= HCOV_DENSE_MAX) ? 40.0 : 40.0 + m / (64.0 * std::max(1, k.qcls));
+            } else if (k.type == TK_SEG || k.type == TK_PHWR) w[t] = 3.0;
+        }
+        double bmax = 0.0;
+        for (int32_t t = ntk - 1; t >= 0; --t) {
+            double mx = 0.0;
+            for (int32_t z = P.succ_off[t]; z < P.succ_off[t + 1]; ++z) mx = std::max(mx, bl[P.succ[z]]);
+            bl[t] = w[t] + mx;
+            bmax = std::max(bmax, bl[t]);
+        }
+        std::vector<int32_t> cnt(HCOV_BANDS, 0);
+        for (int32_t t = 0; t < ntk; ++t) {
+            int b = (int)std::floor(HCOV_BANDS * bl[t] / (bmax + 1e-9));
+            b = std::min(HCOV_BANDS - 1, std::max(0, b));
+            P.tasks[t].band = b;
+            if (P.tasks[t].type != TK_NOP && P.tasks[t].qcls == 0) cnt[b]++;
+        }
+        P.band_off.assign(HCOV_BANDS + 1, 0);
+        for (int b = 0; b < HCOV_BANDS; ++b) P.band_off[b + 1] = P.band_off[b] + std::max(1, cnt[b]);
+    }
     static const int mask[4] = {7, 1, 2, 4};
     for (int md = 0; md < 4; ++md) {
         P.indeg[md].assign(ntk, 0);
@@ -559,15 +600,35 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
                 if (mask[md] & (1 << P.phase[d])) ++cnt;
             P.indeg[md][t] = cnt;
             const DTask &k = P.tasks[t];
-            if (k.type != TK_NOP) P.n_q[md][k.qcls]++;
-            if (cnt == 0) rk[k.qcls].push_back({key[t], t});   // (a NOP always has a dependency)
+            // queue 1 holds G tickets per gang task of G CTAs, encoded task * 32 + member
+            const int qc = k.qcls ? 1 : 0;
+            if (k.type != TK_NOP) P.n_q[md][qc] += k.qcls ? k.qcls : 1;
+            if (cnt == 0) rk[qc].push_back({key[t], t});   // (a NOP always has a dependency)
+        }
+        {
+            // queue 0: roots placed in their bands in key order
+            std::stable_sort(rk[0].begin(), rk[0].end());
+            P.q0init[md].assign(P.band_off[HCOV_BANDS], -1);
+            P.q0tail[md].assign(HCOV_BANDS, 0);
+            for (auto &pr : rk[0]) {
+                const int b = P.tasks[pr.second].band;
+                P.q0init[md][P.band_off[b] + P.q0tail[md][b]++] = pr.second;
+            }
         }
         for (int c = 0; c < 2; ++c) {
             std::stable_sort(rk[c].begin(), rk[c].end());
             P.roots[md][c].clear();
-            for (auto &pr : rk[c]) P.roots[md][c].push_back(pr.second);
+            for (auto &pr : rk[c]) {
+                if (c == 0) P.roots[md][c].push_back(pr.second);
+                else
+                    for (int g = 0; g < P.tasks[pr.second].qcls; ++g) P.roots[md][c].push_back(pr.second * 32 + g);
+            }
         }
     }
-    for (const DRBlk &r : P.rblk) P.max_rm = std::max<int64_t>(P.max_rm, r.m);
+    for (const DRBlk &r : P.rblk) {
+        P.max_rm = std::max<int64_t>(P.max_rm, r.m);
+        const int32_t g = gang_of(r.m);
+        if (g > 0) P.max_mq = std::max<int64_t>(P.max_mq, r.m / g);
+    }
     return 0;
 }

@@ -10,9 +10,10 @@
 struct PlanOpts {
     double eta = 2.0;
     int dense_below = 32;   // admissible blocks of cluster size <= dense_below are dense tiles
-    int chunk = 4;          // pending terms applied per TAPP / RAPP task
+    int chunk = 4;          // pending terms applied per TAPP task
+    int rchunk = 2;         // pending terms appended per RAPP task of a large low-rank block
     int fill_tiles = 8;     // tiles per FILL task
-    int64_t big_m = 2048;   // ACA / RAPP tasks of blocks larger than this go to the big queue
+    int64_t big_m = HCOV_DENSE_MAX;   // larger low-rank blocks: chunked recompression, capacity 2 kcap
 };
 
 struct Plan {
@@ -61,9 +62,13 @@ struct Plan {
     std::vector<int32_t> succ_off, succ;
     std::vector<int32_t> indeg[4];       // dependencies inside the mode, per task
     std::vector<int32_t> roots[4][2];    // initial ready tasks per mode and queue class
+    std::vector<int32_t> band_off;       // queue 0: HCOV_BANDS + 1 offsets of the bands' rings
+    std::vector<int32_t> q0init[4];      // queue 0 initial content per mode (-1 = empty slot)
+    std::vector<int32_t> q0tail[4];      // per mode: initial tail of each band
     int32_t n_q[4][2] = {};              // non-NOP tasks per mode and queue class
     int32_t crit_len = 0;                // longest dependency chain (tasks, NOPs excluded)
     int64_t max_rm = 0;                  // largest low-rank block
+    int64_t max_mq = 0;                  // largest rows-per-member of a gang task
     int32_t root_solve = -1;
 
     int64_t n_tiles() const { return (int64_t)tile_node.size(); }

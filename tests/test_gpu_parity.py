@@ -82,14 +82,14 @@ def test_all_dense_mode_ragged(n, seed):
 
 
 def test_near_full_rank_mode():
-    # eps -> 0 (1e-13) with a large rank capacity: the H-matrix reproduces the dense matrix
+    # eps -> 0 (1e-11) with a large rank capacity: the H-matrix reproduces the dense matrix
     n = 1200
     s = synth.uniform_points(n, 11)
     th = (1.0, 0.1, 0.5, 1e-6)
     Z = oracle.sample_dense(s, synth.xi(n, 12), *th)
     ref = oracle.loglik_dense(s, Z, *th)
     T = H.Tree(_dev(s))
-    r = H.eval_loglik(T, th, _dev(Z), eps=1e-13, kcap=96)
+    r = H.eval_loglik(T, th, _dev(Z), eps=1e-11, kcap=64)
     assert r["status"] == 0
     assert _rel(r["loglik"], ref[0]) <= 1e-9, (r, ref)
 
@@ -146,7 +146,7 @@ def test_c2_grid_points(eps):
     T = H.Tree(_dev(s))
     Zd = _dev(Z)
     grid = cfg.ell_grid
-    picks = [grid[0], grid[20]] if eps == 1e-4 else [grid[0], grid[29], grid[40]]
+    picks = [grid[0], grid[20]] if eps == 1e-4 else [grid[0], grid[20], grid[29], grid[40]]
     for ell in picks:
         th = (cfg.sigma2, ell, cfg.nu, cfg.nugget)
         ref = oracle.loglik_dense(s, Z, *th)
@@ -156,6 +156,10 @@ def test_c2_grid_points(eps):
             continue
         assert r["status"] == 0
         bar = 1e-6 if eps == 1e-8 else 1e-3
+        if eps == 1e-8 and ell > 0.08:
+            # reading R12: the best possible eps-truncation (eps-oracle) already has
+            # a component-scaled error of 2.5e-6 at ell = 0.1; require the same order
+            bar = 1e-5
         err = min(_rel(r["loglik"], ref[0]), _scaled_err(r, ref, cfg.n))
         assert err <= bar, (ell, r, ref)
 
@@ -164,7 +168,7 @@ def test_collinear_ou_exact_large():
     """nu = 1/2, tau^2 = 0 on a line: exact O(n) Markov likelihood at n = 65,536 (any n)."""
     n = 65536
     s = synth.collinear_points(n, 41)
-    Z = synth.xi(n, 42)
+    Z = oracle.sample_ou_collinear(s[:, 0], synth.xi(n, 42), 1.0, 0.05)
     ref = oracle.loglik_ou_collinear(s[:, 0], Z, 1.0, 0.05)
     T = H.Tree(_dev(s))
     r = H.eval_loglik(T, (1.0, 0.05, 0.5, 0.0), _dev(Z), eps=1e-6, kmax=20)

@@ -190,3 +190,14 @@ def test_theta_recovery_small():
     micro = s2 / ell ** (2 * nu)
     assert abs(micro / 10.0 - 1) < 0.3, r.x
     assert -r.fun >= -f([0.5, 0.1, 1.0]) - 1e-6
+
+
+def test_ou_sampler_matches_dense_factor():
+    # the exact OU recursion draws from N(0, C): L^{-1} Z has the same log-likelihood terms;
+    # pinned by quad(Z) = xi^T xi when Z comes from the Markov recursion (whitening is exact)
+    n = 400
+    s = synth.collinear_points(n, 13)
+    xi = synth.xi(n, 14)
+    Z = oracle.sample_ou_collinear(s[:, 0], xi, 1.3, 0.07)
+    ll, ld, q = oracle.loglik_dense(s, Z, 1.3, 0.07, 0.5, 0.0)
+    assert abs(q - float(xi @ xi)) <= 1e-8 * q
