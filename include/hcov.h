@@ -164,11 +164,22 @@ typedef struct {
     double task_busy_ms[HCOV_PROF_CLASSES];
     double task_count[HCOV_PROF_CLASSES];
     double flop[8];
+    double phase_ms[16];               /* CTA-time of truncation phases: 0 panel QRs, 1 core product,
+                                          2 pivoted QR, 3 SVD, 4 Q applications, 5 full-pivot ACA,
+                                          6 dense updates, 8 partial ACA */
 } hcov_prof;
 hcov_status hcov_prof_control(int32_t enable_events, int32_t reset);
 hcov_status hcov_prof_read(hcov_prof *out);
 const char *hcov_prof_class_name(int32_t cls);
 const char *hcov_prof_task_name(int32_t type);
+
+/* Unit test of the truncation step A6 on one CTA: X, Y (m x R, col-major device
+ * arrays) -> U, V (m x rlim device arrays) with X Y^T ~ U V^T, sigma_{r+1} <= eps sigma_1, r <= kmax
+ * (kmax > 0), r <= rlim.  path 0: Householder QRs; 1: shifted CholeskyQR3 (taken when m >= 2R).
+ * out3_host: rank, cap-bound flag, overflow flag.  Synchronises the device. */
+hcov_status hcov_test_truncate(const double *X_dev, const double *Y_dev, int64_t m, int32_t R, double eps,
+                               int32_t kmax, int32_t rlim, int32_t path, double *U_dev, double *V_dev,
+                               int32_t *out3_host);
 
 void hcov_tree_free(hcov_tree t);
 void hcov_hmat_free(hcov_hmat h);

@@ -60,7 +60,7 @@ class Prof(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("n_task_types", ctypes.c_int32),
                 ("count", ctypes.c_int64 * 16), ("ms", ctypes.c_double * 16),
                 ("task_busy_ms", ctypes.c_double * 16), ("task_count", ctypes.c_double * 16),
-                ("flop", ctypes.c_double * 8)]
+                ("flop", ctypes.c_double * 8), ("phase_ms", ctypes.c_double * 16)]
 
 
 # name -> (restype, argtypes) ; every symbol declared in include/hcov.h
@@ -86,6 +86,7 @@ _SIGS = {
     "hcov_prof_read": (_I32, [_P]),
     "hcov_prof_class_name": (ctypes.c_char_p, [_I32]),
     "hcov_prof_task_name": (ctypes.c_char_p, [_I32]),
+    "hcov_test_truncate": (_I32, [_P, _P, _I64, _I32, _D, _I32, _I32, _I32, _P, _P, _P]),
     "hcov_tree_free": (None, [_P]),
     "hcov_hmat_free": (None, [_P]),
     "hcov_status_string": (ctypes.c_char_p, [_I32]),
@@ -294,7 +295,12 @@ def prof_read() -> dict:
             "ms": {nm: p.ms[k] for k, nm in enumerate(names)},
             "task_busy_ms": {nm: p.task_busy_ms[k] for k, nm in enumerate(tnames)},
             "task_count": {nm: int(p.task_count[k]) for k, nm in enumerate(tnames)},
-            "flop": {nm: p.flop[k] for k, nm in enumerate(FLOP_CLASSES)}}
+            "flop": {nm: p.flop[k] for k, nm in enumerate(FLOP_CLASSES)},
+            "phase_ms": {nm: p.phase_ms[k] for k, nm in enumerate(PHASES) if nm}}
+
+
+PHASES = ["panel_qr", "core_product", "pivoted_qr", "svd", "q_apply", "aca_full", "dense_updates", "",
+          "aca_partial", "", "", "", "", "", "", ""]
 
 
 FLOP_CLASSES = ["assembly_evals", "tile", "truncation", "solve", "products"]
@@ -306,3 +312,18 @@ def roofline(prof: dict, peaks: dict) -> dict:
     ms = prof["ms"]
     top = max(ms, key=lambda k: ms[k]) if ms else None
     return {"kernel": top, "ms": ms.get(top), "launches": prof["count"].get(top)}
+
+
+def test_truncate(X, Y, eps: float, kmax: int = 0, rlim: int = 64, path: int = 1):
+    """hcov_test_truncate: truncation A6 of X Y^T on one CTA; returns (U, V, rank, cap_bound, overflow)."""
+    import torch
+    m, R = X.shape
+    Xc = X.T.contiguous()   # column-major
+    Yc = Y.T.contiguous()
+    U = torch.zeros((rlim, m), dtype=torch.float64, device="cuda")
+    V = torch.zeros((rlim, m), dtype=torch.float64, device="cuda")
+    out = np.zeros(3, dtype=np.int32)
+    _check(lib().hcov_test_truncate(_dev_f64(Xc), _dev_f64(Yc), m, R, eps, kmax, rlim, path, _dev_f64(U), _dev_f64(V),
+                                    out.ctypes.data), "hcov_test_truncate")
+    r = int(out[0])
+    return U[:r].T, V[:r].T, r, int(out[1]), int(out[2])

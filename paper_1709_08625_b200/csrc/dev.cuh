@@ -60,3 +60,19 @@ __device__ __forceinline__ ValIdx block_argmax(double v, int64_t i, double *redv
 // Loads that bypass L1 (data written by other CTAs in earlier launches/waves is always in
 // L2; within a launch no task reads data another task of the same launch writes).
 __device__ __forceinline__ double ldg_cg(const double *p) { return __ldcg(p); }
+
+// Phase timers (diagnostics, hcov_prof with events enabled): thread 0 of a CTA accumulates
+// globaltimer spans of the truncation phases into g_phase_ns.
+__device__ unsigned long long g_phase_ns[16];
+__device__ int g_phase_on;
+__device__ __forceinline__ unsigned long long ph_now()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PH_BEGIN(v) const unsigned long long v = (g_phase_on && threadIdx.x == 0) ? ph_now() : 0ull
+#define PH_END(k, v)                                                  \
+    do {                                                              \
+        if (g_phase_on && threadIdx.x == 0) atomicAdd(&g_phase_ns[k], ph_now() - (v)); \
+    } while (0)

@@ -67,6 +67,7 @@ struct Ctx {
     double *bscr;              // per-CTA scratch of the big CTAs
     int64_t bscr_stride;
     double *flop;              // FC_N accumulators
+    int64_t smem_dbl;          // dynamic shared memory of the engine (doubles)
     unsigned long long timeout_ns;
 };
 
@@ -197,9 +198,9 @@ __host__ __device__ inline int kbuf_of(int kcap) { return 3 * kcap + 32; }
 __host__ __device__ inline int64_t task_scratch(int64_t m, int kcap)
 {
     int64_t K = kbuf_of(kcap);
-    int64_t panels = 4 * m * K;
-    if (m <= HCOV_DENSE_MAX) panels = m * m + 4 * m * K;
-    return panels + 3 * K * K + 8 * K + m / 8 + 64;
+    int64_t panels = 6 * m * K;
+    if (m <= HCOV_DENSE_MAX) panels = m * m + 6 * m * K;
+    return panels + 8 * K * K + 10 * K + m / 8 + 64;
 }
 
 
@@ -210,17 +211,26 @@ __device__ __forceinline__ CompressWs make_ws(double *base, int64_t m, int K, do
     w.Y = w.X + m * K;
     *X2 = w.Y + m * K;
     *Y2 = *X2 + m * K;
-    w.M = *Y2 + m * K;
+    w.T1 = *Y2 + m * K;
+    w.T2 = w.T1 + m * K;
+    w.M = w.T2 + m * K;
     w.G = w.M + (int64_t)K * K;
     w.J = w.G + (int64_t)K * K;
-    w.tx = w.J + (int64_t)K * K;
+    w.RX = w.J + (int64_t)K * K;
+    w.RY = w.RX + (int64_t)K * K;
+    w.UC = w.RY + (int64_t)K * K;
+    w.VC = w.UC + (int64_t)K * K;
+    w.Ri = w.VC + (int64_t)K * K;
+    w.tx = w.Ri + (int64_t)K * K;
     w.ty = w.tx + K;
     w.tm = w.ty + K;
     w.sig = w.tm + K;
     w.cn = w.sig + K;
-    w.ord = (int *)(w.cn + K);
-    w.piv = (int *)(w.cn + 2 * K);
-    w.tail = w.cn + 3 * K;
+    w.dX = w.cn + K;
+    w.dY = w.dX + K;
+    w.ord = (int *)(w.dY + K);
+    w.piv = (int *)(w.dY + 2 * K);
+    w.tail = w.dY + 3 * K;
     return w;
 }
 
@@ -479,8 +489,8 @@ __device__ int gang_aca(const MaternParams &mp, const double *xs, const double *
 
 // A5 + A6: ACA of the admissible block (Alg. B.1) to eps/10, then QR + SVD truncation to (eps, kmax).
 // gg == nullptr: one CTA; else one member of a gang (scr = this CTA's private scratch).
-__device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *red, double *redv, int64_t *redi,
-                         double &fl_asm, double &fl_tr, Gang *gg)
+__device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *smem, double *red, double *redv,
+                         int64_t *redi, double &fl_asm, double &fl_tr, Gang *gg)
 {
     const int r = tk.a;
     const DRBlk b = c.rblk[r];
@@ -492,9 +502,11 @@ __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *red
     if (!gg) {
         CompressWs w = make_ws(scr, m, KB, &X2, &Y2);
         uint8_t *used = (uint8_t *)w.tail;
+        PH_BEGIN(tp);
         k = aca_partial(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, K, 0.1 * c.eps, used, red, redv, redi);
+        PH_END(8, tp);
         rk = compress(w, m, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m, &cb, &of,
-                      red, redv, redi);
+                      red, redv, redi, smem, c.smem_dbl);
         record_rank(c, r, rk, cb, of);
     } else {
         gg->mq = m / gg->G;
@@ -552,8 +564,8 @@ __device__ void task_tile(const Ctx &c, const DTask &tk, double *smem, double &f
 // X = [U, -A_1 K_1, ...], Y = [V, B_1, ...] (in scratch).  When the panel is full it is
 // recompressed near-losslessly (pivoted QR at eps*1e-4, no SVD); at the end X Y^T is truncated
 // to (eps, kmax) by QR + SVD (A6; Remark 2).
-__device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *red, double *redv, int64_t *redi,
-                          double &fl, Gang *gg)
+__device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *smem, double *red, double *redv,
+                          int64_t *redi, double &fl, Gang *gg)
 {
     const int r = tk.a;
     const DRBlk blk = c.rblk[r];
@@ -575,12 +587,9 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
         // QR + SVD truncation to (eps, kmax)
         double *S = scr;
         CompressWs wd = make_ws(scr + m * m, m, K, &X2, &Y2);   // X, Y panels (m x K) follow S
-        for (int64_t e = threadIdx.x; e < m * m; e += NT) {
-            const int64_t i = e % m, j = e / m;
-            double sum = 0.0;
-            for (int l = 0; l < r0; ++l) sum += __ldcg(U + i + m * l) * __ldcg(V + j + m * l);
-            S[e] = sum;
-        }
+        PH_BEGIN(tg);
+        for (int64_t e = threadIdx.x; e < m * m; e += NT) S[e] = 0.0;
+        if (r0 > 0) cta_gemm_nt(S, m, m, m, r0, U, m, V, 1, m, 1.0, smem);   // S = U V^T
         fl += 2.0 * m * m * r0;
         __syncthreads();
         double *T1 = wd.Y;   // scratch for A K (m x rb), before Y is used by the ACA
@@ -590,12 +599,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
                 const DNode na = c.nodes[c.tile_node[t.a]], nb = c.nodes[c.tile_node[t.b]];
                 const int64_t ar = (int64_t)na.i * HCOV_LEAF - R0, br = (int64_t)nb.i * HCOV_LEAF - C0;
                 const double *A = c.tiles + (int64_t)t.a * HCOV_TILE, *B = c.tiles + (int64_t)t.b * HCOV_TILE;
-                for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
-                    int i = e & 31, j = e >> 5;
-                    double sum = 0.0;
-                    for (int l = 0; l < 32; ++l) sum += __ldcg(A + i + 32 * l) * __ldcg(B + j + 32 * l);
-                    S[(ar + i) + m * (br + j)] -= sum;
-                }
+                cta_gemm_nt(S + ar + m * br, m, 32, 32, 32, A, 32, B, 1, 32, -1.0, smem);
                 fl += 2.0 * 32 * 32 * 32;
             } else {
                 Fac A = get_fac(c, t.a), B = get_fac(c, t.b);
@@ -604,37 +608,30 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
                 const int64_t r_lo = max(R0, A.row0), r_hi = min(R0 + m, A.row0 + A.nrows);
                 const int64_t c_lo = max(C0, B.row0), c_hi = min(C0 + m, B.row0 + B.nrows);
                 const int64_t nr = r_hi - r_lo, nc = c_hi - c_lo;
-                const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcap * c.kcap : nullptr;
-                for (int64_t e = threadIdx.x; e < nr * (int64_t)rb; e += NT) {
-                    int64_t i = e % nr;
-                    int b = (int)(e / nr);
-                    double sum;
-                    if (Kc) {
-                        sum = 0.0;
-                        for (int a = 0; a < ra; ++a)
-                            sum += __ldcg(A.p + (r_lo - A.row0) + i + A.ld * a) * __ldcg(Kc + a + (int64_t)c.kcap * b);
-                    } else {
-                        sum = __ldcg(A.p + (r_lo - A.row0) + i + A.ld * b);
-                    }
-                    T1[e] = sum;
+                const double *Ap = A.p + (r_lo - A.row0);
+                const double *Bq = B.p + (c_lo - B.row0);
+                if (t.core >= 0) {
+                    // T1 = A K (nr x rb): T1(i, b) = sum_a A(i, a) K(a, b), K(a, b) = Kc[a + kcap b]
+                    const double *Kc = c.cores + (int64_t)t.core * c.kcap * c.kcap;
+                    for (int64_t e = threadIdx.x; e < nr * (int64_t)rb; e += NT) T1[e] = 0.0;
+                    cta_gemm_nt(T1, nr, nr, rb, ra, Ap, A.ld, Kc, c.kcap, 1, 1.0, smem);
+                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, T1, nr, Bq, 1, B.ld, -1.0, smem);
+                    fl += 2.0 * nr * ra * rb;
+                } else {
+                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, Ap, A.ld, Bq, 1, B.ld, -1.0, smem);
                 }
-                __syncthreads();
-                for (int64_t e = threadIdx.x; e < nr * nc; e += NT) {
-                    const int64_t i = e % nr, j = e / nr;
-                    double sum = 0.0;
-                    for (int b = 0; b < rb; ++b) sum += T1[i + nr * b] * __ldcg(B.p + (c_lo - B.row0) + j + B.ld * b);
-                    S[(r_lo - R0 + i) + m * (c_lo - C0 + j)] -= sum;
-                }
-                fl += 2.0 * nr * nc * rb + (Kc ? 2.0 * nr * ra * rb : 0.0);
+                fl += 2.0 * nr * nc * rb;
             }
-            __syncthreads();
         }
+        PH_END(6, tg);
         const int KA = (int)(m < K ? m : K);
-        int k = aca_full(S, m, wd.X, wd.Y, KA, 0.1 * c.eps / (double)m, redv, redi);
+        PH_BEGIN(ta);
+        int k = aca_full(S, m, wd.X, wd.Y, KA, 0.1 * c.eps / (double)m, 0.1 * c.eps, red, redv, redi);
+        PH_END(5, ta);
         fl += 2.0 * m * m * k;
         if (k == KA && KA < m && threadIdx.x == 0) atomicAdd(c.flags + 3, 1);
         int rk = compress(wd, m, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, U, V, m, &cb, &of, red, redv,
-                          redi);
+                          redi, smem, c.smem_dbl);
         fl += compress_flops(m, k, rk);
         record_rank(c, r, rk, cb, of);
         return;
@@ -666,7 +663,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
                                    &icb, &iof, red, redv, redi);
             else
                 rk = compress(w, m, cur, c.eps, interm_tol(c.eps), false, 0, K - maxw, X2, Y2, m, &icb, &iof, red,
-                              redv, redi);
+                              redv, redi, smem, c.smem_dbl);
             fl += (gg ? 1.0 / gg->G : 1.0) * compress_flops(m, cur, rk);
             if (iof && threadIdx.x == 0 && (!gg || gg->g == 0)) atomicAdd(c.flags + 3, 1);
             double *tx = w.X, *ty = w.Y;
@@ -692,20 +689,17 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
             const int64_t c_lo = max(C0 + q0, B.row0), c_hi = min(C0 + q0 + mq, B.row0 + B.nrows);
             const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcap * c.kcap : nullptr;
             if (r_hi > r_lo) {
-                for (int64_t e = threadIdx.x; e < (r_hi - r_lo) * (int64_t)rb; e += NT) {
-                    int64_t i = e % (r_hi - r_lo);
-                    int b = (int)(e / (r_hi - r_lo));
-                    double sum;
-                    if (Kc) {
-                        sum = 0.0;
-                        for (int a = 0; a < ra; ++a)
-                            sum += __ldcg(A.p + (r_lo - A.row0) + i + A.ld * a) * __ldcg(Kc + a + (int64_t)c.kcap * b);
-                    } else {
-                        sum = __ldcg(A.p + (r_lo - A.row0) + i + A.ld * b);
+                if (Kc) {   // xc = -A K  (columns b < rb), staged GEMM
+                    cta_gemm_nt(xc + (r_lo - R0 - q0), mq, r_hi - r_lo, rb, ra, A.p + (r_lo - A.row0), A.ld, Kc, c.kcap,
+                                1, -1.0, smem);
+                    fl += 2.0 * (r_hi - r_lo) * ra * rb;
+                } else {
+                    for (int64_t e = threadIdx.x; e < (r_hi - r_lo) * (int64_t)rb; e += NT) {
+                        int64_t i = e % (r_hi - r_lo);
+                        int b = (int)(e / (r_hi - r_lo));
+                        xc[(r_lo - R0 - q0) + i + mq * b] = -__ldcg(A.p + (r_lo - A.row0) + i + A.ld * b);
                     }
-                    xc[(r_lo - R0 - q0) + i + mq * b] = -sum;
                 }
-                if (Kc) fl += 2.0 * (r_hi - r_lo) * ra * rb;
             }
             if (c_hi > c_lo)
                 for (int64_t e = threadIdx.x; e < (c_hi - c_lo) * (int64_t)rb; e += NT) {
@@ -726,7 +720,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *re
         rk = gang_compress(w, gw, *gg, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi);
         fl += compress_flops(m, cur, rk) / gg->G;
     } else {
-        rk = compress(w, m, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi);
+        rk = compress(w, m, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi, smem, c.smem_dbl);
         fl += compress_flops(m, cur, rk);
     }
     if (!fin) {

@@ -60,6 +60,7 @@ struct Prof {
     double busy_ns[TK_NTYPES] = {};
     double tasks[TK_NTYPES] = {};
     double flop[FC_N] = {};
+    double phase_ns[16] = {};
 };
 Prof g_prof;
 
@@ -175,7 +176,6 @@ __global__ void __launch_bounds__(NT, 4) k_engine(Ctx c, int mask, const int8_t 
     __shared__ double red[NWARP], redv[NWARP];
     __shared__ int64_t redi[NWARP];
     __shared__ int32_t s_task, s_member;
-    __shared__ uint32_t s_pos;
     const int q = (blockIdx.x < c.nbig) ? 1 : 0;
     double *scr = c.scr + (int64_t)(blockIdx.x - c.nbig) * c.scr_stride;
     double fl[FC_N] = {0, 0, 0, 0, 0};
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(NT, 4) k_engine(Ctx c, int mask, const int8_t 
             s_member = 0;
             if (q == 1 && t >= 0) { s_member = t & 31; t >>= 5; }
             s_task = t;
-            s_pos = pos;
+            (void)pos;
         }
         __syncthreads();
         const int32_t t = s_task;
@@ -254,11 +254,11 @@ __global__ void __launch_bounds__(NT, 4) k_engine(Ctx c, int mask, const int8_t 
         const unsigned long long t0 = gtimer();
         switch (tk.type) {
         case TK_FILL: task_fill(c, tk, fl[FC_ASM]); break;
-        case TK_ACA: task_aca(c, tk, tscr, red, redv, redi, fl[FC_ASM], fl[FC_TRUNC], gg); break;
+        case TK_ACA: task_aca(c, tk, tscr, smem, red, redv, redi, fl[FC_ASM], fl[FC_TRUNC], gg); break;
         case TK_TAPP:
         case TK_POTRF:
         case TK_TRSM: task_tile(c, tk, smem, fl[FC_TILE]); break;
-        case TK_RAPP: task_rapp(c, tk, tscr, red, redv, redi, fl[FC_TRUNC], gg); break;
+        case TK_RAPP: task_rapp(c, tk, tscr, smem, red, redv, redi, fl[FC_TRUNC], gg); break;
         case TK_SEG: task_seg(c, tk, smem, fl[FC_SOLVE]); break;
         case TK_PROJ: task_proj(c, tk, smem, fl[FC_SOLVE]); break;
         case TK_PRR: task_prr(c, tk, fl[FC_PROD]); break;
@@ -447,6 +447,22 @@ __global__ void k_columns_perm(Ctx c, const double *in, int mcols, double *out)
     }
 }
 
+// Unit-test kernel for the truncation (A6): one CTA truncates X Y^T (m x m, R columns).
+__global__ void __launch_bounds__(NT) k_test_truncate(double *scr, int64_t m, int R, int K, double eps, int kmax,
+                                                      int rlim, int path, double *U, double *V, int *rank,
+                                                      int64_t smem_dbl)
+{
+    extern __shared__ double smem[];
+    __shared__ double red[NWARP], redv[NWARP];
+    __shared__ int64_t redi[NWARP];
+    double *X2, *Y2;
+    CompressWs w = make_ws(scr, m, K, &X2, &Y2);
+    int cb = 0, of = 0;
+    const int r = compress(w, m, R, eps, final_tol(eps, R), true, kmax, rlim, U, V, m, &cb, &of, red, redv, redi,
+                           path == 1 ? smem : nullptr, smem_dbl);
+    if (threadIdx.x == 0) { rank[0] = r; rank[1] = cb; rank[2] = of; }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
@@ -502,6 +518,7 @@ struct hcov_hmat_s {
     int32_t *indeg = nullptr, *q0 = nullptr, *q1 = nullptr, *gbar = nullptr, *gslot = nullptr;
     uint32_t *qctl = nullptr;
     double *scr = nullptr, *bscr = nullptr, *res = nullptr, *res_host = nullptr;
+    double *ktab = nullptr, *ktab_host = nullptr;
     EngineStats *stats = nullptr, *stats_host = nullptr;
     void release_all()
     {
@@ -518,6 +535,8 @@ struct hcov_hmat_s {
     ~hcov_hmat_s()
     {
         release_all();
+        cudaFree(ktab);
+        if (ktab_host) cudaFreeHost(ktab_host);
         if (res_host) cudaFreeHost(res_host);
         if (stats_host) cudaFreeHost(stats_host);
     }
@@ -703,12 +722,14 @@ void fill_ctx(hcov_hmat h)
     c.fail_leaf = h->fail; c.flags = h->flags;
     c.kcap = h->kcap_alloc; c.kmax = h->trunc.kmax; c.eps = h->trunc.eps;
     c.mp = hcov_matern_params(h->theta.sigma2, h->theta.ell, h->theta.nu, h->theta.nugget);
+    if (c.mp.kind == 3) c.mp.tab = h->ktab;
     c.indeg = h->indeg; c.queue[0] = h->q0; c.queue[1] = h->q1; c.qctl = h->qctl; c.gbar = h->gbar;
     c.band_off = t->d_band_off;
     c.gslot = h->gslot;
     c.nbig = NBIG;
     c.scr = h->scr; c.bscr = h->bscr;
     c.flop = nullptr;
+    c.smem_dbl = h->smem / (int64_t)sizeof(double);
     const char *wd = std::getenv("HCOV_WATCHDOG_S");
     double wds = wd ? std::atof(wd) : 300.0;
     if (!(wds > 0)) wds = 300.0;
@@ -731,6 +752,12 @@ hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
                                                      t->d_roots[md][1], (int32_t)P.roots[md][1].size(), qcap(P, 1)));
     EngineStats *stats = g_prof.events ? h->stats : nullptr;
     if (stats) CK(cudaMemsetAsync(h->stats, 0, sizeof(EngineStats), st));
+    {
+        static const unsigned long long zeros[16] = {};
+        const int on = stats ? 1 : 0;
+        CK(cudaMemcpyToSymbolAsync(g_phase_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+        if (on) CK(cudaMemcpyToSymbolAsync(g_phase_ns, zeros, sizeof(zeros), 0, cudaMemcpyHostToDevice, st));
+    }
     const char *tlpath = std::getenv("HCOV_TIMELINE");
     unsigned long long *tl = nullptr;
     if (tlpath) {
@@ -758,6 +785,9 @@ hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
             g_prof.tasks[k] += (double)h->stats_host->tasks[k];
         }
         for (int k = 0; k < FC_N; ++k) g_prof.flop[k] += h->stats_host->flop[k];
+        unsigned long long ph[16];
+        CK(cudaMemcpyFromSymbol(ph, g_phase_ns, sizeof(ph)));
+        for (int k = 0; k < 16; ++k) g_prof.phase_ns[k] += (double)ph[k];
     }
     return HCOV_OK;
 }
@@ -771,6 +801,18 @@ hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trun
     h->theta = *theta;
     h->trunc = *trunc;
     if ((s = hmat_alloc(h, kcap))) return s;
+    if (!h->ktab) {
+        CK(cudaMalloc(&h->ktab, KTAB_NI * KTAB_NC * sizeof(double)));
+        CK(cudaMallocHost(&h->ktab_host, KTAB_NI * KTAB_NC * sizeof(double)));
+    }
+    {
+        const MaternParams mp = hcov_matern_params(theta->sigma2, theta->ell, theta->nu, theta->nugget);
+        if (mp.kind == 3) {
+            CK(cudaStreamSynchronize(st));   // the pinned staging buffer may still feed a previous copy
+            hcov_matern_table(theta->nu, h->ktab_host);
+            CK(cudaMemcpyAsync(h->ktab, h->ktab_host, KTAB_NI * KTAB_NC * sizeof(double), cudaMemcpyHostToDevice, st));
+        }
+    }
     fill_ctx(h);
     Plan &P = t->P;
     CK(cudaMemsetAsync(h->rank, 0, std::max<int64_t>(1, P.n_r()) * sizeof(int32_t), st));
@@ -1105,6 +1147,7 @@ hcov_status hcov_prof_control(int32_t enable_events, int32_t reset)
         for (int k = 0; k < PC_N; ++k) { g_prof.count[k] = 0; g_prof.ms[k] = 0.0; }
         for (int k = 0; k < TK_NTYPES; ++k) { g_prof.busy_ns[k] = 0; g_prof.tasks[k] = 0; }
         for (int k = 0; k < FC_N; ++k) g_prof.flop[k] = 0;
+        for (int k = 0; k < 16; ++k) g_prof.phase_ns[k] = 0;
     }
     g_prof.events = enable_events != 0;
     return HCOV_OK;
@@ -1127,6 +1170,7 @@ hcov_status hcov_prof_read(hcov_prof *out)
         out->task_count[k] = g_prof.tasks[k];
     }
     for (int k = 0; k < FC_N; ++k) out->flop[k] = g_prof.flop[k];
+    for (int k = 0; k < 16; ++k) out->phase_ms[k] = g_prof.phase_ns[k] * 1e-6;
     return HCOV_OK;
 }
 
@@ -1138,6 +1182,29 @@ const char *hcov_prof_class_name(int32_t cls)
 const char *hcov_prof_task_name(int32_t type)
 {
     return (type >= 0 && type < TK_NTYPES) ? TASK_NAMES[type] : "";
+}
+
+hcov_status hcov_test_truncate(const double *X_dev, const double *Y_dev, int64_t m, int32_t R, double eps,
+                               int32_t kmax, int32_t rlim, int32_t path, double *U_dev, double *V_dev,
+                               int32_t *out3_host)
+{
+    if (!X_dev || !Y_dev || !U_dev || !V_dev || !out3_host || m < 1 || R < 0 || R > 224 || rlim < 1) return HCOV_ERR_INVALID_ARG;
+    const int K = R > 0 ? R : 1;
+    const int64_t need = 6 * m * K + 8 * (int64_t)K * K + 10 * K + m / 8 + 64;
+    double *scr = nullptr;
+    int *rk = nullptr;
+    CK(cudaMalloc(&scr, need * sizeof(double)));
+    CK(cudaMalloc(&rk, 3 * sizeof(int)));
+    CK(cudaMemcpy(scr, X_dev, m * (int64_t)R * sizeof(double), cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(scr + m * K, Y_dev, m * (int64_t)R * sizeof(double), cudaMemcpyDeviceToDevice));
+    const int64_t smem = 16384 * sizeof(double);
+    CK(cudaFuncSetAttribute(k_test_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_test_truncate<<<1, NT, smem, 0>>>(scr, m, R, K, eps, kmax, rlim, path, U_dev, V_dev, rk, 16384);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(out3_host, rk, 3 * sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(scr);
+    cudaFree(rk);
+    return e == cudaSuccess ? HCOV_OK : map_err(e);
 }
 
 void hcov_tree_free(hcov_tree t) { delete t; }

@@ -6,9 +6,9 @@
 #define HCOV_LEAF 32
 #define HCOV_TILE (HCOV_LEAF * HCOV_LEAF)
 #define HCOV_GANG 16          // largest gang: CTAs cooperating on one task of the gang queue (queue 1)
-#define HCOV_GANG_CTAS 64     // CTAs serving queue 1 (>= HCOV_GANG, so every gang can form)
+#define HCOV_GANG_CTAS 128    // CTAs serving queue 1 (>= HCOV_GANG, so every gang can form)
 #define HCOV_DENSE_MAX 256    // low-rank blocks up to this size are recompressed from a dense accumulation
-#define HCOV_GANG_MIN 512     // low-rank blocks from this size on are processed by gangs of m/256 CTAs
+#define HCOV_GANG_MIN 2048    // low-rank blocks from this size on are processed by gangs of m/1024 CTAs
 
 // Block-tree node types (lower triangle incl. diagonal).
 enum NodeType : int32_t { ND_H = 0, ND_R = 1, ND_T = 2 };

@@ -94,15 +94,102 @@ __device__ __forceinline__ void tile_gemm_nt_sub(double *S, const double *A, con
 }
 
 // ------------------------------------------------------------------------------------------
+// CTA GEMM update  C(i, j) += alpha * sum_l A(i, l) B(j, l),  i < nr, j < nc, l < kd, with
+// A(i, l) = Ap[i + l * lda] (L2 loads, coalesced in i), B(j, l) = Bp[j * bsj + l * bsl] staged
+// through shared memory in chunks of GEMM_JC columns j, C(i, j) = Cp[i + j * ldc] (CTA-private).
+// Each thread owns rows i and keeps GEMM_JC accumulators: A is read once per column chunk and B
+// once in total, instead of once per output entry.  smem: >= GEMM_JC * kd doubles.
+// ------------------------------------------------------------------------------------------
+#define GEMM_JC 16
+__device__ void cta_gemm_nt(double *Cp, int64_t ldc, int64_t nr, int64_t nc, int kd, const double *Ap, int64_t lda,
+                            const double *Bp, int64_t bsj, int64_t bsl, double alpha, double *smem)
+{
+    for (int64_t j0 = 0; j0 < nc; j0 += GEMM_JC) {
+        const int jc = (int)(nc - j0 < GEMM_JC ? nc - j0 : GEMM_JC);
+        __syncthreads();
+        for (int e = threadIdx.x; e < GEMM_JC * kd; e += NT) {
+            const int jj = e % GEMM_JC, l = e / GEMM_JC;
+            smem[e] = (jj < jc) ? __ldcg(Bp + (j0 + jj) * bsj + (int64_t)l * bsl) : 0.0;
+        }
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < nr; i += NT) {
+            double acc[GEMM_JC];
+#pragma unroll
+            for (int jj = 0; jj < GEMM_JC; ++jj) acc[jj] = 0.0;
+            for (int l = 0; l < kd; ++l) {
+                const double a = __ldcg(Ap + i + (int64_t)l * lda);
+                const double *bl = smem + GEMM_JC * l;
+#pragma unroll
+                for (int jj = 0; jj < GEMM_JC; ++jj) acc[jj] = fma(a, bl[jj], acc[jj]);
+            }
+            for (int jj = 0; jj < jc; ++jj) Cp[i + (j0 + jj) * ldc] += alpha * acc[jj];
+        }
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------
 // Householder QR of a tall-skinny panel in global memory: A (m x R, lda), R <= m.
 // Reflector j: v_j = [1; A[j+1:m, j]], H_j = I - tau_j v_j v_j^T; R in the upper triangle.
 // ------------------------------------------------------------------------------------------
+// Apply H = I - t v v^T (v = [1; aj[j+1:m]]) to columns k0..k1-1 of B (ld ldb, rows j..m-1):
+// one warp per group of 4 columns, the 4 dot products reduced together (interleaved shuffles).
+__device__ __forceinline__ void householder_update(const double *aj, int64_t j, int64_t m, double t, double *B,
+                                                   int64_t ldb, int k0, int k1)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k = k0 + 4 * warp; k < k1; k += 4 * NWARP) {
+        const int nk = min(4, k1 - k);
+        double *b0 = B + ldb * k;
+        double *b1 = (nk > 1) ? b0 + ldb : b0;
+        double *b2 = (nk > 2) ? b0 + 2 * ldb : b0;
+        double *b3 = (nk > 3) ? b0 + 3 * ldb : b0;
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+#pragma unroll 4
+        for (int64_t i = j + 1 + lane; i < m; i += 32) {
+            const double v = aj[i];
+            w0 = fma(v, b0[i], w0);
+            w1 = fma(v, b1[i], w1);
+            w2 = fma(v, b2[i], w2);
+            w3 = fma(v, b3[i], w3);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            w0 += __shfl_xor_sync(0xffffffffu, w0, o);
+            w1 += __shfl_xor_sync(0xffffffffu, w1, o);
+            w2 += __shfl_xor_sync(0xffffffffu, w2, o);
+            w3 += __shfl_xor_sync(0xffffffffu, w3, o);
+        }
+        w0 = t * (w0 + b0[j]);
+        w1 = t * (w1 + b1[j]);
+        w2 = t * (w2 + b2[j]);
+        w3 = t * (w3 + b3[j]);
+        __syncwarp();
+        if (lane == 0) {
+            b0[j] -= w0;
+            if (nk > 1) b1[j] -= w1;
+            if (nk > 2) b2[j] -= w2;
+            if (nk > 3) b3[j] -= w3;
+        }
+#pragma unroll 4
+        for (int64_t i = j + 1 + lane; i < m; i += 32) {
+            const double v = aj[i];
+            b0[i] -= v * w0;
+            if (nk > 1) b1[i] -= v * w1;
+            if (nk > 2) b2[i] -= v * w2;
+            if (nk > 3) b3[i] -= v * w3;
+        }
+        __syncwarp();
+    }
+}
+
 __device__ void qr_house(double *A, int64_t lda, int64_t m, int R, double *tau, double *red)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int j = 0; j < R; ++j) {
         double *aj = A + lda * j;
         double s = 0.0;
+#pragma unroll 4
         for (int64_t i = j + 1 + threadIdx.x; i < m; i += NT) { double v = aj[i]; s += v * v; }
         s = block_sum(s, red);
         const double alpha = aj[j];
@@ -118,17 +205,7 @@ __device__ void qr_house(double *A, int64_t lda, int64_t m, int R, double *tau, 
         }
         if (threadIdx.x == 0) { aj[j] = beta; tau[j] = t; }
         __syncthreads();
-        if (t != 0.0) {
-            for (int k = j + 1 + warp; k < R; k += NWARP) {
-                double *ak = A + lda * k;
-                double w = 0.0;
-                for (int64_t i = j + 1 + lane; i < m; i += 32) w += aj[i] * ak[i];
-                w = warp_sum(w) + ak[j];
-                w *= t;
-                if (lane == 0) ak[j] -= w;
-                for (int64_t i = j + 1 + lane; i < m; i += 32) ak[i] -= aj[i] * w;
-            }
-        }
+        if (t != 0.0) householder_update(aj, j, m, t, A, lda, j + 1, R);
         __syncthreads();
     }
 }
@@ -141,16 +218,7 @@ __device__ void qr_apply_q(const double *A, int64_t lda, int64_t m, int R, const
     for (int j = R - 1; j >= 0; --j) {
         const double t = tau[j];
         if (t == 0.0) continue;
-        const double *aj = A + lda * j;
-        for (int c = warp; c < r; c += NWARP) {
-            double *bc = B + ldb * c;
-            double w = 0.0;
-            for (int64_t i = j + 1 + lane; i < m; i += 32) w += aj[i] * bc[i];
-            w = warp_sum(w) + bc[j];
-            w *= t;
-            if (lane == 0) bc[j] -= w;
-            for (int64_t i = j + 1 + lane; i < m; i += 32) bc[i] -= aj[i] * w;
-        }
+        householder_update(A + lda * j, j, m, t, B, ldb, 0, r);
         __syncthreads();
     }
 }
@@ -284,13 +352,185 @@ __device__ int qrcp_trunc(double *M, int K, double tol, int rmax, double *tau, i
     return j;
 }
 
+// ------------------------------------------------------------------------------------------
+// Cholesky-QR path of the panel QRs (BLAS-3 shaped: streaming Gram products and GEMMs instead of
+// one sweep over the panel per Householder reflector).  Shifted CholeskyQR3 (Fukaya et al.):
+// column scaling, G = X^T X + s I, R = chol(G), X <- X R^{-1}, then two unshifted passes; the
+// product of the triangular factors is R.  A Cholesky breakdown returns false (the caller falls
+// back to Householder).
+// ------------------------------------------------------------------------------------------
+
+// G(a, b) = sum_i X(i, a) X(i, b) for a <= b (upper triangle, ld K).  4x4 register blocks per
+// thread, row strips staged in shared memory (smem_dbl doubles available).
+__device__ void gram_upper(const double *X, int64_t m, int64_t ld, int K, double *G, double *smem, int64_t smem_dbl)
+{
+    const int nb = (K + 3) / 4, W = 4 * nb;
+    const int nblk = nb * (nb + 1) / 2;
+    int RS = 32;
+    while (RS > 1 && (int64_t)RS * W > smem_dbl) RS >>= 1;
+    for (int p0 = 0; p0 < nblk; p0 += NT) {
+        const int p = p0 + threadIdx.x;
+        const bool act = p < nblk;
+        int A = 0, off = 0;
+        if (act)
+            while (off + (nb - A) <= p) { off += nb - A; ++A; }
+        const int B = A + (p - off);
+        double acc[16];
+#pragma unroll
+        for (int z = 0; z < 16; ++z) acc[z] = 0.0;
+        for (int64_t r0 = 0; r0 < m; r0 += RS) {
+            const int rows = (int)(m - r0 < RS ? m - r0 : RS);
+            __syncthreads();
+            for (int e = threadIdx.x; e < RS * W; e += NT) {
+                const int r = e % RS, cc = e / RS;
+                smem[e] = (r < rows && cc < K) ? X[r0 + r + ld * cc] : 0.0;
+            }
+            __syncthreads();
+            if (act) {
+                const double *sa = smem + RS * 4 * A, *sb = smem + RS * 4 * B;
+                for (int r = 0; r < rows; ++r) {
+                    const double a0 = sa[r], a1 = sa[r + RS], a2 = sa[r + 2 * RS], a3 = sa[r + 3 * RS];
+                    const double b0 = sb[r], b1 = sb[r + RS], b2 = sb[r + 2 * RS], b3 = sb[r + 3 * RS];
+                    acc[0] = fma(a0, b0, acc[0]); acc[1] = fma(a0, b1, acc[1]);
+                    acc[2] = fma(a0, b2, acc[2]); acc[3] = fma(a0, b3, acc[3]);
+                    acc[4] = fma(a1, b0, acc[4]); acc[5] = fma(a1, b1, acc[5]);
+                    acc[6] = fma(a1, b2, acc[6]); acc[7] = fma(a1, b3, acc[7]);
+                    acc[8] = fma(a2, b0, acc[8]); acc[9] = fma(a2, b1, acc[9]);
+                    acc[10] = fma(a2, b2, acc[10]); acc[11] = fma(a2, b3, acc[11]);
+                    acc[12] = fma(a3, b0, acc[12]); acc[13] = fma(a3, b1, acc[13]);
+                    acc[14] = fma(a3, b2, acc[14]); acc[15] = fma(a3, b3, acc[15]);
+                }
+            }
+        }
+        if (act)
+            for (int u = 0; u < 4; ++u)
+                for (int v = 0; v < 4; ++v) {
+                    const int a = 4 * A + u, bb = 4 * B + v;
+                    if (a <= bb && bb < K) G[a + (int64_t)K * bb] = acc[4 * u + v];
+                }
+    }
+    __syncthreads();
+}
+
+// Upper Cholesky G = R^T R in place (upper triangle, ld K) by one warp (warp-synchronous).
+// Returns false on a non-positive or non-finite pivot.
+__device__ bool chol_upper_warp(double *G, int K)
+{
+    const int lane = threadIdx.x & 31;
+    for (int k = 0; k < K; ++k) {
+        const double d = G[k + (int64_t)K * k];
+        if (!(d > 0.0) || !isfinite(d)) return false;
+        const double rk = sqrt(d);
+        __syncwarp();
+        for (int j = k + lane; j < K; j += 32) G[k + (int64_t)K * j] = (j == k) ? rk : G[k + (int64_t)K * j] / rk;
+        __syncwarp();
+        for (int j = k + 1 + lane; j < K; j += 32) {
+            const double gkj = G[k + (int64_t)K * j];
+            for (int i = k + 1; i <= j; ++i) G[i + (int64_t)K * j] -= G[k + (int64_t)K * i] * gkj;
+        }
+        __syncwarp();
+    }
+    return true;
+}
+
+// Ri = R^{-1} (upper triangular, ld K), one column per thread (back substitution).
+__device__ void tri_inv_upper(const double *R, int K, double *Ri)
+{
+    for (int j = threadIdx.x; j < K; j += NT) {
+        for (int i = j + 1; i < K; ++i) Ri[i + (int64_t)K * j] = 0.0;
+        Ri[j + (int64_t)K * j] = 1.0 / R[j + (int64_t)K * j];
+        for (int i = j - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int l = i + 1; l <= j; ++l) s += R[i + (int64_t)K * l] * Ri[l + (int64_t)K * j];
+            Ri[i + (int64_t)K * j] = -s / R[i + (int64_t)K * i];
+        }
+    }
+    __syncthreads();
+}
+
+// C = A B (A: m x K ld lda, B: K x K upper triangular ld K, C: m x K ld ldc, C != A)
+__device__ void gemm_upper(double *C, int64_t ldc, const double *A, int64_t lda, int64_t m, int K, const double *B,
+                           double *smem)
+{
+    for (int64_t e = threadIdx.x; e < m * (int64_t)K; e += NT) {
+        const int64_t i = e % m, j = e / m;
+        C[i + ldc * j] = 0.0;
+    }
+    __syncthreads();
+    // C(i, j) += sum_l A(i, l) B(l, j) = sum_l A(i, l) Bt(j, l),  Bt(j, l) = B[l + K j]
+    cta_gemm_nt(C, ldc, m, K, K, A, lda, B, K, 1, 1.0, smem);
+}
+
+// Shifted CholeskyQR3 of X (m x K, ld m) into Q (overwrites Xq, which must not alias X: the
+// passes alternate X -> Xq -> X -> Xq) and R (upper, ld K; includes the column scaling).
+// Returns false on breakdown.  smem: the engine's dynamic shared memory (smem_dbl doubles).
+__device__ bool cholqr3(double *X, double *Xq, int64_t m, int K, double *R, double *Racc, double *G, double *Ri,
+                        double *dcol, double *smem, int64_t smem_dbl, double *red, double **Qout)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ int s_ok;
+    // column scaling to unit norms
+    for (int c = warp; c < K; c += NWARP) {
+        double s = 0.0;
+        for (int64_t i = lane; i < m; i += 32) s += X[i + m * c] * X[i + m * c];
+        s = warp_sum(s);
+        if (lane == 0) dcol[c] = (s > 0.0) ? sqrt(s) : 1.0;
+    }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < m * (int64_t)K; e += NT) X[e] /= dcol[e / m];
+    for (int e = threadIdx.x; e < K * K; e += NT) Racc[e] = ((e % K) == (e / K)) ? 1.0 : 0.0;
+    __syncthreads();
+    double *src = X, *dst = Xq;
+    for (int pass = 0; pass < 3; ++pass) {
+        // pass 0 is shifted; a later pass that breaks down (numerically rank-deficient panel) is
+        // retried once with the shift 11 (m K + K (K + 1)) u tr(G)  (tr(G) >= ||X||_2^2)
+        for (int attempt = (pass == 0 ? 1 : 0); attempt < 2; ++attempt) {
+            gram_upper(src, m, m, K, G, smem, smem_dbl);
+            if (attempt == 1 && threadIdx.x == 0) {
+                double tr = 0.0;
+                for (int a = 0; a < K; ++a) tr += G[a + (int64_t)K * a];
+                const double sh = 11.0 * ((double)m * K + (double)K * (K + 1)) * 1.1102230246251565e-16 * tr;
+                for (int a = 0; a < K; ++a) G[a + (int64_t)K * a] += sh;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const bool ok = chol_upper_warp(G, K);
+                if (lane == 0) s_ok = ok;
+            }
+            __syncthreads();
+            if (s_ok) break;
+        }
+        if (!s_ok) return false;
+        // Racc <- R_pass Racc (both upper)
+        for (int e = threadIdx.x; e < K * K; e += NT) {
+            const int i = e % K, j = e / K;
+            double sum = 0.0;
+            for (int l = i; l <= j; ++l) sum += G[i + (int64_t)K * l] * Racc[l + (int64_t)K * j];
+            R[e] = (i <= j) ? sum : 0.0;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < K * K; e += NT) Racc[e] = R[e];
+        tri_inv_upper(G, K, Ri);
+        gemm_upper(dst, m, src, m, m, K, Ri, smem);
+        double *t = src; src = dst; dst = t;
+    }
+    // R = Racc diag(d)
+    for (int e = threadIdx.x; e < K * K; e += NT) R[e] = Racc[e] * dcol[e / K];
+    __syncthreads();
+    *Qout = src;
+    return true;
+}
+
 // Truncation workspace for R columns of m rows.
 struct CompressWs {
-    double *X, *Y;      // m x K each (ld m): inputs, destroyed (Householder vectors)
+    double *X, *Y;      // m x K each (ld m): inputs, destroyed (Householder vectors / Q factors)
     double *M, *G, *J;  // K x K, K x K, K x K
     double *tx, *ty, *tm;   // K each
     double *sig, *cn;   // K each
     int *ord, *piv;     // K each
+    double *RX, *RY, *UC, *VC, *Ri;   // K x K each (Cholesky-QR path)
+    double *T1, *T2;    // m x K each: Cholesky-QR ping-pong panels (Q_X ends in T1, Q_Y in T2)
+    double *dX, *dY;    // K each (column scales)
     double *tail;       // first free (8-byte aligned) double after the workspace
 };
 
@@ -312,6 +552,7 @@ __device__ int compress_core(const CompressWs &w, const double *RX, int64_t ldx,
 {
     __shared__ int s_r, s_cb, s_of;
     const int K = R;
+    PH_BEGIN(t1);
     for (int e = threadIdx.x; e < K * K; e += NT) {
         int i = e % K, j = e / K;
         double s = 0.0;
@@ -319,7 +560,11 @@ __device__ int compress_core(const CompressWs &w, const double *RX, int64_t ldx,
         w.M[e] = s;
     }
     __syncthreads();
+    PH_END(1, t1);
+    PH_BEGIN(t2);
     const int rq = qrcp_trunc(w.M, K, tol_q, svd ? K : rlim + 1, w.tm, w.piv, w.cn, redv, redi, red);
+    PH_END(2, t2);
+    PH_BEGIN(t3);
     for (int e = threadIdx.x; e < K * rq; e += NT) {
         int k = e % K, i = e / K;
         w.G[w.piv[k] + (int64_t)K * i] = (k >= i) ? w.M[i + (int64_t)K * k] : 0.0;
@@ -379,6 +624,7 @@ __device__ int compress_core(const CompressWs &w, const double *RX, int64_t ldx,
         }
     }
     __syncthreads();
+    PH_END(3, t3);
     qr_apply_q(w.M, K, K, rq, w.tm, U, ldo, r);   // U_core <- Q_M U_core (rows < K)
     if (threadIdx.x == 0) { *cap_bound = s_cb; *overflow = s_of; }
     __syncthreads();
@@ -390,35 +636,75 @@ __device__ int compress_core(const CompressWs &w, const double *RX, int64_t ldx,
 // alias X, Y.  Returns r.
 __device__ int compress(const CompressWs &w, int64_t m, int R, double eps, double tol_q, bool svd, int kmax,
                         int rlim, double *U, double *V, int64_t ldo, int *cap_bound, int *overflow, double *red,
-                        double *redv, int64_t *redi)
+                        double *redv, int64_t *redi, double *smem = nullptr, int64_t smem_dbl = 0)
 {
     if (R == 0) { if (threadIdx.x == 0) { *cap_bound = 0; *overflow = 0; } __syncthreads(); return 0; }
+    if (smem && m >= 2 * R) {
+        // BLAS-3 path: shifted CholeskyQR3 of X and Y, core, U = Q_X U_core, V = Q_Y V_core
+        PH_BEGIN(tc);
+        double *QX = nullptr, *QY = nullptr;
+        bool ok = cholqr3(w.X, w.T1, m, R, w.RX, w.M, w.G, w.Ri, w.dX, smem, smem_dbl, red, &QX);
+        if (ok) ok = cholqr3(w.Y, w.T2, m, R, w.RY, w.M, w.G, w.Ri, w.dY, smem, smem_dbl, red, &QY);
+        PH_END(0, tc);
+        if (!ok) {
+            // breakdown (non-finite data): report as a rank-capacity failure
+            if (threadIdx.x == 0) { *cap_bound = 0; *overflow = 1; }
+            __syncthreads();
+            return 0;
+        }
+        const int r = compress_core(w, w.RX, R, w.RY, R, R, eps, tol_q, svd, kmax, rlim, w.UC, w.VC, R, R, cap_bound,
+                                    overflow, red, redv, redi);
+        PH_BEGIN(t4c);
+        for (int64_t e = threadIdx.x; e < m * (int64_t)r; e += NT) {
+            const int64_t i = e % m, j = e / m;
+            U[i + ldo * j] = 0.0;
+            V[i + ldo * j] = 0.0;
+        }
+        __syncthreads();
+        if (r > 0) {
+            cta_gemm_nt(U, ldo, m, r, R, QX, m, w.UC, R, 1, 1.0, smem);
+            cta_gemm_nt(V, ldo, m, r, R, QY, m, w.VC, R, 1, 1.0, smem);
+        }
+        PH_END(4, t4c);
+        return r;
+    }
+    PH_BEGIN(t0);
     qr_house(w.X, m, m, R, w.tx, red);
     qr_house(w.Y, m, m, R, w.ty, red);
+    PH_END(0, t0);
     const int r = compress_core(w, w.X, m, w.Y, m, R, eps, tol_q, svd, kmax, rlim, U, V, ldo, m, cap_bound, overflow,
                                 red, redv, redi);
+    PH_BEGIN(t4);
     qr_apply_q(w.X, m, m, R, w.tx, U, ldo, r);
     qr_apply_q(w.Y, m, m, R, w.ty, V, ldo, r);
+    PH_END(4, t4);
     return r;
 }
 
 // ------------------------------------------------------------------------------------------
 // Fully pivoted cross approximation of a dense m x m block S (global, ld m), destroyed.
-// Appends up to Kmax columns to X, Y (ld m): S ~= X Y^T.  Stops when max |residual| <= tol.
+// Appends up to Kmax columns to X, Y (ld m): S ~= X Y^T.  Stops when max |residual| <=
+// rel_tol max |S| or ||residual||_F <= rel_fro ||S||_F (the residual is known exactly).
 // ------------------------------------------------------------------------------------------
-__device__ int aca_full(double *S, int64_t m, double *X, double *Y, int Kmax, double rel_tol,
-                        double *redv, int64_t *redi)
+__device__ int aca_full(double *S, int64_t m, double *X, double *Y, int Kmax, double rel_tol, double rel_fro,
+                        double *red, double *redv, int64_t *redi)
 {
-    const int64_t mm = m * m;
-    double bv = 0.0; int64_t bi = 0;
-    for (int64_t e = threadIdx.x; e < mm; e += NT) {
-        double a = fabs(S[e]);
-        if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
-    }
+    // rows i = threadIdx.x + NT q are owned by one thread for all columns (no index divisions)
+    double bv = 0.0, ss = 0.0;
+    int64_t bi = 0;
+    for (int64_t j = 0; j < m; ++j)
+        for (int64_t i = threadIdx.x; i < m; i += NT) {
+            const int64_t e = i + m * j;
+            const double v = S[e], a = fabs(v);
+            ss += v * v;
+            if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
+        }
     ValIdx b = block_argmax(bv, bi, redv, redi);
-    const double tol = rel_tol * b.v;
+    const double fro0 = sqrt(block_sum(ss, red));
+    const double tol = rel_tol * b.v, tolf = rel_fro * fro0;
+    double fro = fro0;
     int k = 0;
-    while (k < Kmax && b.v > tol && b.v > 0.0) {
+    while (k < Kmax && b.v > tol && fro > tolf && b.v > 0.0) {
         const int64_t is = b.i % m, js = b.i / m;
         const double p = S[is + m * js];
         for (int64_t i = threadIdx.x; i < m; i += NT) {
@@ -426,16 +712,21 @@ __device__ int aca_full(double *S, int64_t m, double *X, double *Y, int Kmax, do
             Y[i + m * k] = S[is + m * i] / p;
         }
         __syncthreads();
-        bv = 0.0; bi = 0;
+        bv = 0.0; bi = 0; ss = 0.0;
         const double *xk = X + m * k, *yk = Y + m * k;
-        for (int64_t e = threadIdx.x; e < mm; e += NT) {
-            int64_t i = e % m, j = e / m;
-            double v = S[e] - xk[i] * yk[j];
-            S[e] = v;
-            double a = fabs(v);
-            if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
+        for (int64_t j = 0; j < m; ++j) {
+            const double yj = yk[j];
+            for (int64_t i = threadIdx.x; i < m; i += NT) {
+                const int64_t e = i + m * j;
+                const double v = S[e] - xk[i] * yj;
+                S[e] = v;
+                ss += v * v;
+                const double a = fabs(v);
+                if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
+            }
         }
         b = block_argmax(bv, bi, redv, redi);
+        fro = sqrt(block_sum(ss, red));
         ++k;
     }
     __syncthreads();

@@ -124,11 +124,23 @@ HD double hcov_besselk_scaled(double nu, double x)
 
 HD double hcov_besselk(double nu, double x) { return exp(-x) * hcov_besselk_scaled(nu, x); }
 
+// General nu: g(t) = x^nu K_nu(x) e^x with t = log x is analytic in t (singularities at
+// Im t = +-pi), so a piecewise Chebyshev interpolant in t converges geometrically.  The table is
+// built once per theta on the host from the series / continued fraction above (same accuracy,
+// ~1e-16 interpolation error at degree 11 on intervals of width 0.32) and replaces ~100 divisions
+// per entry by one Clenshaw recurrence.  Outside [KTAB_X0, KTAB_X1] the direct evaluation is used.
+#define KTAB_NI 64
+#define KTAB_NC 12
+#define KTAB_X0 9.5367431640625e-07   /* 2^-20 */
+#define KTAB_X1 745.0
+
 // Matern parameters preprocessed once per theta.
 struct MaternParams {
     double sigma2, inv_ell, nu, nugget;
     double pre;      // sigma2 * 2^(1-nu) / Gamma(nu)
     int kind;        // 0: nu=1/2, 1: nu=3/2, 2: nu=5/2, 3: general
+    const double *tab;   // device: KTAB_NI x KTAB_NC Chebyshev coefficients of g (kind 3), or null
+    double t0, inv_w;    // log(KTAB_X0), intervals per unit t
 };
 
 inline MaternParams hcov_matern_params(double sigma2, double ell, double nu, double nugget)
@@ -137,7 +149,50 @@ inline MaternParams hcov_matern_params(double sigma2, double ell, double nu, dou
     p.sigma2 = sigma2; p.inv_ell = 1.0 / ell; p.nu = nu; p.nugget = nugget;
     p.kind = (nu == 0.5) ? 0 : (nu == 1.5) ? 1 : (nu == 2.5) ? 2 : 3;
     p.pre = sigma2 * exp((1.0 - nu) * log(2.0) - lgamma(nu));
+    p.tab = nullptr;
+    p.t0 = log(KTAB_X0);
+    p.inv_w = KTAB_NI / (log(KTAB_X1) - log(KTAB_X0));
     return p;
+}
+
+// Host: Chebyshev coefficients (KTAB_NI x KTAB_NC, row per interval) of g on each interval.
+inline void hcov_matern_table(double nu, double *coef)
+{
+    const double PI = 3.141592653589793;
+    const double t0 = log(KTAB_X0), w = (log(KTAB_X1) - t0) / KTAB_NI;
+    const int N = KTAB_NC;
+    for (int i = 0; i < KTAB_NI; ++i) {
+        double f[KTAB_NC];
+        for (int j = 0; j < N; ++j) {
+            const double sj = cos(PI * (j + 0.5) / N);
+            const double t = t0 + w * (i + 0.5 * (sj + 1.0));
+            const double x = exp(t);
+            f[j] = exp(nu * t) * hcov_besselk_scaled(nu, x);
+        }
+        for (int k = 0; k < N; ++k) {
+            double sum = 0.0;
+            for (int j = 0; j < N; ++j) sum += f[j] * cos(PI * k * (j + 0.5) / N);
+            coef[i * N + k] = (k == 0 ? 1.0 : 2.0) * sum / N;
+        }
+    }
+}
+
+HD double hcov_matern_tab(const MaternParams &p, double x, double lx)
+{
+    const double u = (lx - p.t0) * p.inv_w;
+    int i = (int)u;
+    if (i > KTAB_NI - 1) i = KTAB_NI - 1;
+    const double s = 2.0 * (u - i) - 1.0, s2 = 2.0 * s;
+    const double *c = p.tab + i * KTAB_NC;
+    double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+    for (int k = KTAB_NC - 1; k >= 1; --k) {
+        const double b0 = fma(s2, b1, c[k] - b2);
+        b2 = b1;
+        b1 = b0;
+    }
+    const double g = fma(s, b1, c[0] - b2);
+    return p.pre * g * exp(-x);
 }
 
 // C(h), h >= 0 (Eq. (3)); no nugget.
@@ -152,6 +207,7 @@ HD double hcov_matern(const MaternParams &p, double h)
     default: {
         if (x > 740.0) return 0.0;
         double lx = log(x);
+        if (p.tab && x >= KTAB_X0) return hcov_matern_tab(p, x, lx);
         return p.pre * exp(p.nu * lx - x) * hcov_besselk_scaled(p.nu, x);
     }
     }

@@ -23,7 +23,7 @@ namespace {
 inline int32_t gang_of(int64_t m)
 {
     if (m < HCOV_GANG_MIN) return 0;
-    return (int32_t)std::min<int64_t>(HCOV_GANG, m / 256);
+    return (int32_t)std::min<int64_t>(HCOV_GANG, m / 1024);
 }
 
 inline int64_t heap_id(int l, int64_t c) { return ((int64_t)1 << l) - 1 + c; }

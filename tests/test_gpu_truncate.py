@@ -1,0 +1,40 @@
+"""GPU unit tests of the truncation step (A6) against numpy's SVD:
+||X Y^T - U V^T||_2 <= 10 eps ||X Y^T||_2 (SURVEY Sec. 8(c) pin; SPEC acceptance), both QR paths."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import paper_1709_08625_b200 as H  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _panel(m, R, seed, kind):
+    rng = np.random.default_rng(seed)
+    if kind == "decay":          # singular values 10^(-k/4)
+        A = np.linalg.qr(rng.standard_normal((m, R)))[0]
+        B = np.linalg.qr(rng.standard_normal((m, R)))[0]
+        return A * 10.0 ** (-np.arange(R) / 4.0), B
+    if kind == "dependent":      # exactly rank-deficient X (repeated columns)
+        A = rng.standard_normal((m, R // 2))
+        X = np.concatenate([A, A @ rng.standard_normal((R // 2, R - R // 2))], axis=1)
+        return X, rng.standard_normal((m, R))
+    if kind == "scaled":         # columns of wildly different scales
+        X = rng.standard_normal((m, R)) * 10.0 ** rng.uniform(-8, 2, R)
+        return X, rng.standard_normal((m, R))
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("kind", ["decay", "dependent", "scaled"])
+@pytest.mark.parametrize("m,R,eps", [(512, 60, 1e-6), (256, 80, 1e-8), (1024, 92, 1e-5)])
+def test_truncation_error_bound(path, kind, m, R, eps):
+    X, Y = _panel(m, R, 7 + m + R, kind)
+    S = X @ Y.T
+    U, V, r, cb, of = H.test_truncate(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda(), eps, rlim=R, path=path)
+    assert of == 0
+    s = np.linalg.svd(S, compute_uv=False)
+    err = np.linalg.norm(S - U.cpu().numpy() @ V.cpu().numpy().T, 2)
+    assert err <= 10 * eps * s[0], (err / s[0], r)
+    r_ref = int(np.sum(s > eps * s[0]))
+    assert abs(r - r_ref) <= 2, (r, r_ref)

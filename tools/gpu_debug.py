@@ -34,6 +34,7 @@ def run(n, eta, eps, nu=0.5, ell=0.1, kmax=0, seed=1, nug=1e-6, geom='u', staged
           f"oracle {to:.2f}s tasks={info['n_tasks']} crit={info['n_waves']}", flush=True)
     busy = {k: round(v, 2) for k, v in p['task_busy_ms'].items() if v}
     print("   busy ms:", busy, "engine ms:", round(p['ms']['engine'], 2), flush=True)
+    print("   phases ms:", {k: round(v, 1) for k, v in p['phase_ms'].items()}, flush=True)
     return rel
 
 
@@ -49,4 +50,4 @@ if __name__ == '__main__':
     else:
         run(16384, 2.0, 1e-8, nu=1.5, ell=0.05)
         run(16384, 2.0, 1e-4, nu=1.5, ell=0.01)
-        run(65536, 2.0, 1e-5, nu=1.0, ell=0.05, kmax=20)
+        run(65536, 2.0, 1e-6, nu=0.5, ell=0.1, kmax=20)

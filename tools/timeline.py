@@ -25,10 +25,14 @@ def run(tag, n, nu, ell, eps, kmax, kcap=0):
     os.environ["HCOV_TIMELINE"] = path
     torch.cuda.synchronize()
     import time
+    H.prof_control(True, True)
     t0 = time.time()
     r = H.eval_loglik(T, th, Z, eps, kmax, kcap)
     torch.cuda.synchronize()
     wall = time.time() - t0
+    pr = H.prof_read()
+    H.prof_control(False, True)
+    print("phases ms:", {k: round(v, 1) for k, v in pr["phase_ms"].items()}, "flop:", pr["flop"], flush=True)
     del os.environ["HCOV_TIMELINE"]
     tl = np.fromfile(path, dtype=np.uint64).reshape(-1, 3)
     off, sc = T.succ()
