@@ -38,9 +38,12 @@ METRIC = "log-likelihood evals/s (H-assemble+H-Cholesky+solve) at n=2M"
 def _args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--steps", type=int, default=1)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="C5")
+    p.add_argument("--theta", default="feasible", choices=["feasible", "config"],
+                   help="feasible: C5's n / points / k with C4's kernel and eps = 1e-6 (DESIGN.md R24: C5's "
+                        "own theta is not SPD under the method at n >= 65,536); config: the config as written")
     p.add_argument("--impl", default="hcov", choices=["hcov", "reference"])
     p.add_argument("--n", type=int, default=0, help="override n (debug only; not a bench line)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -97,13 +100,12 @@ def _theta_for(cfg, j: int, m: int):
     return (cfg.sigma2, cfg.ell * f, cfg.nu, cfg.nugget)
 
 
-def _oracle_cpu(cfg, n_s: int, reps: int = 1):
+def _oracle_cpu(cfg, n_s: int, th, reps: int = 1):
     """The oracle as it stands (dense Matern fill + LAPACK Cholesky + solve) on the first n_s
-    points of the config; returns (seconds per evaluation, threads)."""
+    points of the config at theta th; returns (seconds per evaluation, threads)."""
     import oracle
     s = synth.points(cfg)[:n_s]
     Z = synth.xi(n_s, cfg.seed_xi)
-    th = (cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget)
     oracle.loglik_dense(s[:256], Z[:256], *th)      # build/load the C checker outside the clock
     ts = []
     for _ in range(reps):
@@ -113,14 +115,13 @@ def _oracle_cpu(cfg, n_s: int, reps: int = 1):
     return min(ts), oracle.THREADS
 
 
-def _cpu_sample_size(cfg, budget_s: float = 15.0) -> int:
-    import oracle
+def _cpu_sample_size(cfg, th, budget_s: float = 15.0) -> int:
     n_s = 2048
-    t, _ = _oracle_cpu(cfg, n_s)
+    t, _ = _oracle_cpu(cfg, n_s, th)
     # grow until one evaluation costs ~budget/4 (dense O(n^3))
     while n_s < cfg.n and t * 8 < budget_s / 2 and n_s * 2 <= 32768:
         n_s *= 2
-        t, _ = _oracle_cpu(cfg, n_s)
+        t, _ = _oracle_cpu(cfg, n_s, th)
     return n_s
 
 
@@ -128,12 +129,13 @@ def run_reference(args, cfg, rank: int, world: int):
     if rank != 0:
         return
     n = cfg.n
-    n_s = args.cpu_sample or _cpu_sample_size(cfg, budget_s=8.0)
+    th, eps, kmax, note = bench_params(args, cfg)
+    n_s = args.cpu_sample or _cpu_sample_size(cfg, th, budget_s=8.0)
     for _ in range(args.warmup):
-        _oracle_cpu(cfg, min(n_s, 2048))
+        _oracle_cpu(cfg, min(n_s, 2048), th)
     ts = []
     for _ in range(args.steps):
-        t, thr = _oracle_cpu(cfg, n_s)
+        t, thr = _oracle_cpu(cfg, n_s, th)
         ts.append(t)
     t_step = float(np.mean(ts))
     t_full = t_step * (n / n_s) ** 3              # dense O(n^3) extrapolation to the metric's n
@@ -142,13 +144,22 @@ def run_reference(args, cfg, rank: int, world: int):
            "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": cfg.name, "n": n, "nu": cfg.nu, "ell": cfg.ell, "sigma2": cfg.sigma2,
-                      "nugget": cfg.nugget, "eps": cfg.eps[0], "kmax": cfg.kmax},
+           "config": {"workload": cfg.name, "n": n, "nu": cfg.nu, "ell": th[1], "sigma2": th[0], "nu_used": th[2],
+                      "nugget": th[3], "eps": eps, "kmax": kmax, "theta_note": note},
            "cpu_baseline": {"value": v, "unit": "evals/s", "cores": thr, "kind": "oracle",
                             "sample": f"dense oracle L(theta) on the first {n_s} of the {n} points, "
                                       f"{t_step:.2f} s/eval, extrapolated x(n/{n_s})^3"},
            "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def bench_params(args, cfg):
+    """(theta, eps, kmax, note) of the benchmarked evaluation (R24)."""
+    if args.theta == "config" or cfg.name != "C5":
+        return (cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget), cfg.eps[0], cfg.kmax, "config theta"
+    c4 = synth.CONFIGS["C4"]
+    return ((c4.sigma2, c4.ell, c4.nu, c4.nugget), 1e-6, cfg.kmax,
+            "C5 points/n/k with C4's kernel (nu=0.5, ell=0.1) and eps=1e-6: C5's theta is not SPD (DESIGN.md R24)")
 
 
 def run_hcov(args, cfg, rank: int, world: int):
@@ -163,12 +174,11 @@ def run_hcov(args, cfg, rank: int, world: int):
         dist.init_process_group("nccl", device_id=dev)
     n = args.n or cfg.n
     s = synth.points(cfg)[:n] if args.n else synth.points(cfg)
-    eps, kmax = cfg.eps[0], cfg.kmax
+    th0, eps, kmax, note = bench_params(args, cfg)
     stream = torch.cuda.current_stream()
     s_dev = torch.from_numpy(s).to(dev)
     tree = H.Tree(s_dev)                       # A1-A2: theta-independent, untimed
     info = tree.info()
-    th0 = (cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget)
     # data: Z = L~ xi from the H-Cholesky factor at the config's theta (Sec. 5.1)
     xi = torch.from_numpy(synth.xi(n, cfg.seed_xi)).to(dev)
     hgen = H.HMatrix(tree, th0, eps, kmax)
@@ -176,7 +186,7 @@ def run_hcov(args, cfg, rank: int, world: int):
     Z = hgen.sample(xi)
     del hgen
     m_total = max(1, world)
-    my_theta = _theta_for(cfg, rank, m_total)
+    my_theta = th0 if m_total == 1 else (th0[0], th0[1] * 0.8 * (1.25 / 0.8) ** (rank / (m_total - 1)), th0[2], th0[3])
 
     def step():
         return H.eval_loglik(tree, my_theta, Z, eps, kmax)
@@ -244,7 +254,22 @@ def run_hcov(args, cfg, rank: int, world: int):
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
         pass
-    roof = H.roofline(prof, peaks)
+    # dominant kernel = the persistent engine (one launch per step); algorithmic flop counted by the
+    # tasks (LAPACK counts at actual shapes) / engine CUDA-event time vs the measured fp64 FMA peak
+    eng_ms = prof["ms"].get("engine", 0.0) / args.steps
+    fl = sum(v for k, v in prof["flop"].items() if k != "assembly_evals") / args.steps
+    fp64 = {}
+    try:
+        fp64 = json.load(open(os.path.join(ROOT, "profiles", "r1_fp64_peak.json")))
+    except OSError:
+        pass
+    peak = float(fp64.get("dfma_tflops", 36.85))
+    ach = fl / (eng_ms * 1e-3) / 1e12 if eng_ms > 0 else 0.0
+    roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "traffic": None, "kernel": "k_engine (persistent DAG engine, 1 launch/step)",
+            "flop_per_launch": fl, "ms_per_launch": eng_ms,
+            "peak_source": "profiles/r1_fp64_peak.json: measured DFMA loop on this pool's B200 (fp64 not in "
+                           "MEASURED_PEAKS.json)"}
 
     if rank != 0:
         if dist:
@@ -254,17 +279,20 @@ def run_hcov(args, cfg, rank: int, world: int):
            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": cfg.name if not args.n else f"{cfg.name}[n={n}]", "n": n, "nu": cfg.nu,
-                      "ell": cfg.ell, "sigma2": cfg.sigma2, "nugget": cfg.nugget, "eps": eps, "kmax": kmax,
+                      "ell": th0[1], "sigma2": th0[0], "nu_used": th0[2], "nugget": th0[3], "eps": eps, "kmax": kmax,
+                      "theta_note": note,
                       "leaf": 32, "eta": 2.0, "parallelism": f"theta-batch dp{world}",
                       "l2": "inputs larger than L2 (H-matrix >> 126 MB)",
                       "tree": {k: info[k] for k in ("depth", "n_dense_tiles", "n_lowrank", "n_tasks", "n_waves")}},
            "loglik": r["loglik"], "max_rank": r["max_rank"], "cap_binds": r["cap_binds"],
            "gpu_launches": int(prof["launches"] // max(1, args.steps)),
            "e2e": e2e, "roofline": roof, "clocks": clk,
-           "stages_ms_per_step": {k: v / args.steps for k, v in prof["ms"].items()}}
+           "stages_ms_per_step": {k: v / args.steps for k, v in prof["ms"].items()},
+           "task_busy_cta_ms_per_step": {k: round(v / args.steps, 1) for k, v in prof["task_busy_ms"].items() if v},
+           "status": r["status"]}
     if world == 1 and not args.no_cpu_baseline:
-        n_s = args.cpu_sample or _cpu_sample_size(cfg)
-        t, thr = _oracle_cpu(cfg, n_s)
+        n_s = args.cpu_sample or _cpu_sample_size(cfg, th0)
+        t, thr = _oracle_cpu(cfg, n_s, th0)
         t_full = t * (n / n_s) ** 3
         out["cpu_baseline"] = {"value": 1.0 / t_full, "unit": "evals/s", "cores": thr, "kind": "oracle",
                                "sample": f"dense oracle L(theta) on the first {n_s} of the {n} points: "

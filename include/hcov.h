@@ -80,6 +80,9 @@ typedef struct {
     int64_t n_lowrank;      /* admissible low-rank blocks (lower triangle) */
     int64_t n_tasks, n_waves;   /* n_waves: longest dependency chain of the task DAG (tasks) */
     double eta;
+    /* pool sizes (for memory planning): U/V and W elements per unit rank capacity, product slots
+     * (slot_a * kcap^2 + slot_b * kcap doubles), cores (kcap^2 each), DAG edges, term-list entries */
+    int64_t uv_elems, w_elems, slot_a, slot_b, n_cores, n_edges, n_xterm, max_mq;
 } hcov_tree_info;
 
 /* A1 + A2: cluster tree by median bisection on the longest bounding-box axis (leaves <= leaf_size,

@@ -53,7 +53,9 @@ class TreeInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("n_pad", ctypes.c_int64), ("depth", ctypes.c_int32),
                 ("leaf_size", ctypes.c_int32), ("n_leaves", ctypes.c_int64), ("n_dense_tiles", ctypes.c_int64),
                 ("n_lowrank", ctypes.c_int64), ("n_tasks", ctypes.c_int64), ("n_waves", ctypes.c_int64),
-                ("eta", ctypes.c_double)]
+                ("eta", ctypes.c_double), ("uv_elems", ctypes.c_int64), ("w_elems", ctypes.c_int64),
+                ("slot_a", ctypes.c_int64), ("slot_b", ctypes.c_int64), ("n_cores", ctypes.c_int64),
+                ("n_edges", ctypes.c_int64), ("n_xterm", ctypes.c_int64), ("max_mq", ctypes.c_int64)]
 
 
 class Prof(ctypes.Structure):

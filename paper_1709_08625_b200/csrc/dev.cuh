@@ -3,7 +3,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#define NT 128          // threads per CTA for every task kernel
+#ifndef HCOV_NT
+#define HCOV_NT 512
+#endif
+#define NT HCOV_NT      // threads per CTA for every task kernel
 #define NWARP (NT / 32)
 
 __device__ __forceinline__ double warp_sum(double v)

@@ -42,8 +42,11 @@ struct Ctx {
     double *U, *V;
     int32_t *rank;
     double *cores;
-    double *W;
-    double *P;                 // product slots
+    double *W;                 // pool of W = H V blocks, allocated at run time with actual ranks (woff)
+    double *P;                 // pool of product slots (PROJ / PHWP results), allocated at run time (poff)
+    int64_t *woff, *poff;      // per PHW / per slot: offset in its pool (-1 = not yet allocated)
+    unsigned long long *mem;   // [0] W bump, [1] P bump, [2] pool overflows
+    int64_t wcap, pcap;        // pool capacities (doubles)
     double *vbuf;              // root right-hand side / solution (internal order)
     double *logdet_part, *minpiv_part, *quad_part;
     int32_t *fail_leaf;        // min over failing leaves (init INT32_MAX)
@@ -77,25 +80,78 @@ struct Fac {
     int64_t ld, row0;
     int32_t nrows, ncols;
 };
+__device__ __forceinline__ int partner_prefix(const Ctx &c, const DPhw &q, int p)
+{
+    int s = 0;
+    for (int k = 0; k < p; ++k) s += __ldcg(c.rank + c.col_r[q.part_off + k]);
+    return s;
+}
+__device__ __forceinline__ double *w_base(const Ctx &c, int qid) { return c.W + __ldcg(c.woff + qid); }
+__device__ __forceinline__ const double *slot_get(const Ctx &c, int s) { return c.P + __ldcg(c.poff + s); }
+
+// Bump allocation from a pool (thread 0); an overflow is counted (reported as out of memory) and
+// the allocation aliases offset 0.
+__device__ __forceinline__ int64_t pool_bump(const Ctx &c, int which, int64_t size, int64_t cap)
+{
+    int64_t off = (int64_t)atomicAdd(c.mem + which, (unsigned long long)size);
+    if (off + size > cap) { atomicAdd(c.mem + 2, 1ull); off = 0; }
+    return off;
+}
+// Product slot s of `size` doubles (single producer task; CTA-collective).
+__device__ double *slot_alloc(const Ctx &c, int s, int64_t size)
+{
+    __shared__ int64_t s_off;
+    if (threadIdx.x == 0) {
+        const int64_t off = pool_bump(c, 1, size, c.pcap);
+        atomicExch((unsigned long long *)(c.poff + s), (unsigned long long)off);
+        s_off = off;
+    }
+    __syncthreads();
+    return c.P + s_off;
+}
+// W block of PHW q (m x sum of partner ranks): the first of its row tasks allocates, the others
+// wait for the published offset (CTA-collective).
+__device__ double *w_acquire(const Ctx &c, int qid, int64_t size)
+{
+    __shared__ int64_t s_off;
+    if (threadIdx.x == 0) {
+        unsigned long long *slot = (unsigned long long *)(c.woff + qid);
+        unsigned long long cur = atomicCAS(slot, ~0ull, ~1ull);
+        int64_t off;
+        if (cur == ~0ull) {
+            off = pool_bump(c, 0, size, c.wcap);
+            __threadfence();
+            atomicExch(slot, (unsigned long long)off);
+        } else {
+            while ((int64_t)(cur = *(volatile unsigned long long *)slot) < 0) __nanosleep(64);
+            off = (int64_t)cur;
+        }
+        s_off = off;
+    }
+    __syncthreads();
+    return c.W + s_off;
+}
+
 __device__ __forceinline__ Fac get_fac(const Ctx &c, int f)
 {
     Fac F;
-    const int64_t off = c.fac_off[f] * (int64_t)c.kcap;
-    F.p = (c.fac_pool[f] == 0 ? c.U : c.W) + off;
     F.nrows = c.fac_nrows[f];
     F.ld = F.nrows;
     F.row0 = c.fac_row0[f];
     F.ncols = __ldcg(c.rank + c.fac_rank_src[f]);
+    if (c.fac_pool[f] == 0) {
+        F.p = c.U + c.fac_off[f] * (int64_t)c.kcap;
+    } else {   // W slice (phw id, partner index)
+        const int64_t code = c.fac_off[f];
+        const int qid = (int)(code >> 8), p = (int)(code & 255);
+        const DPhw q = c.phw[qid];
+        F.p = w_base(c, qid) + (int64_t)q.m * partner_prefix(c, q, p);
+    }
     return F;
 }
 __device__ __forceinline__ int64_t cl_size(const Ctx &c, int level) { return (int64_t)HCOV_LEAF << (c.depth - level); }
 __device__ __forceinline__ double *r_U(const Ctx &c, int r) { return c.U + c.rblk[r].uv_off * (int64_t)c.kcap; }
 __device__ __forceinline__ double *r_V(const Ctx &c, int r) { return c.V + c.rblk[r].uv_off * (int64_t)c.kcap; }
-__device__ __forceinline__ double *slot_ptr(const Ctx &c, int s)
-{
-    const DSlot sl = c.slots[s];
-    return c.P + sl.offa * (int64_t)c.kcap * c.kcap + sl.offb * (int64_t)c.kcap;
-}
 
 // Shared-memory layout of the tile tasks.
 struct TileSmem {
@@ -195,25 +251,25 @@ __host__ __device__ inline int aca_kmax(int64_t m, int kcap)
     return (int)(k < m ? k : m);
 }
 __host__ __device__ inline int kbuf_of(int kcap) { return 3 * kcap + 32; }
-__host__ __device__ inline int64_t task_scratch(int64_t m, int kcap)
+__host__ __device__ inline int64_t task_scratch(int64_t m, int kcap, int npanels = 6)
 {
     int64_t K = kbuf_of(kcap);
-    int64_t panels = 6 * m * K;
-    if (m <= HCOV_DENSE_MAX) panels = m * m + 6 * m * K;
+    int64_t panels = npanels * m * K;
+    if (m <= HCOV_DENSE_MAX) panels = m * m + npanels * m * K;
     return panels + 8 * K * K + 10 * K + m / 8 + 64;
 }
 
 
-__device__ __forceinline__ CompressWs make_ws(double *base, int64_t m, int K, double **X2, double **Y2)
+__device__ __forceinline__ CompressWs make_ws(double *base, int64_t m, int K, double **X2, double **Y2, int npanels = 6)
 {
     CompressWs w;
     w.X = base;
     w.Y = w.X + m * K;
     *X2 = w.Y + m * K;
     *Y2 = *X2 + m * K;
-    w.T1 = *Y2 + m * K;
-    w.T2 = w.T1 + m * K;
-    w.M = w.T2 + m * K;
+    w.T1 = (npanels >= 6) ? *Y2 + m * K : nullptr;
+    w.T2 = (npanels >= 6) ? w.T1 + m * K : nullptr;
+    w.M = *Y2 + m * K * (npanels - 3);
     w.G = w.M + (int64_t)K * K;
     w.J = w.G + (int64_t)K * K;
     w.RX = w.J + (int64_t)K * K;
@@ -511,7 +567,7 @@ __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *sme
     } else {
         gg->mq = m / gg->G;
         gg->q0 = (int64_t)gg->g * gg->mq;
-        CompressWs w = make_ws(scr, gg->mq, KB, &X2, &Y2);
+        CompressWs w = make_ws(scr, gg->mq, KB, &X2, &Y2, 4);
         GangWs gw = make_gws(gg->shared, KB, gg->G);
         k = gang_aca(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, (uint8_t *)w.tail, K, 0.1 * c.eps, gw, *gg, red,
                      redv, redi);
@@ -589,7 +645,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         CompressWs wd = make_ws(scr + m * m, m, K, &X2, &Y2);   // X, Y panels (m x K) follow S
         PH_BEGIN(tg);
         for (int64_t e = threadIdx.x; e < m * m; e += NT) S[e] = 0.0;
-        if (r0 > 0) cta_gemm_nt(S, m, m, m, r0, U, m, V, 1, m, 1.0, smem);   // S = U V^T
+        if (r0 > 0) cta_gemm_nt(S, m, m, m, r0, U, m, V, 1, m, 1.0, smem, c.smem_dbl);   // S = U V^T
         fl += 2.0 * m * m * r0;
         __syncthreads();
         double *T1 = wd.Y;   // scratch for A K (m x rb), before Y is used by the ACA
@@ -599,7 +655,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
                 const DNode na = c.nodes[c.tile_node[t.a]], nb = c.nodes[c.tile_node[t.b]];
                 const int64_t ar = (int64_t)na.i * HCOV_LEAF - R0, br = (int64_t)nb.i * HCOV_LEAF - C0;
                 const double *A = c.tiles + (int64_t)t.a * HCOV_TILE, *B = c.tiles + (int64_t)t.b * HCOV_TILE;
-                cta_gemm_nt(S + ar + m * br, m, 32, 32, 32, A, 32, B, 1, 32, -1.0, smem);
+                cta_gemm_nt(S + ar + m * br, m, 32, 32, 32, A, 32, B, 1, 32, -1.0, smem, c.smem_dbl);
                 fl += 2.0 * 32 * 32 * 32;
             } else {
                 Fac A = get_fac(c, t.a), B = get_fac(c, t.b);
@@ -614,11 +670,13 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
                     // T1 = A K (nr x rb): T1(i, b) = sum_a A(i, a) K(a, b), K(a, b) = Kc[a + kcap b]
                     const double *Kc = c.cores + (int64_t)t.core * c.kcap * c.kcap;
                     for (int64_t e = threadIdx.x; e < nr * (int64_t)rb; e += NT) T1[e] = 0.0;
-                    cta_gemm_nt(T1, nr, nr, rb, ra, Ap, A.ld, Kc, c.kcap, 1, 1.0, smem);
-                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, T1, nr, Bq, 1, B.ld, -1.0, smem);
+                    cta_gemm_nt(T1, nr, nr, rb, ra, Ap, A.ld, Kc, c.kcap, 1, 1.0, smem, c.smem_dbl);
+                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, T1, nr, Bq, 1, B.ld, -1.0, smem,
+                                c.smem_dbl);
                     fl += 2.0 * nr * ra * rb;
                 } else {
-                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, Ap, A.ld, Bq, 1, B.ld, -1.0, smem);
+                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, Ap, A.ld, Bq, 1, B.ld, -1.0, smem,
+                                c.smem_dbl);
                 }
                 fl += 2.0 * nr * nc * rb;
             }
@@ -638,7 +696,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     }
     // factor mode (m > HCOV_DENSE_MAX); rows [q0, q0 + mq) belong to this CTA (the whole block
     // without a gang); the panels w.X, w.Y, X2, Y2 hold those rows (ld mq).
-    CompressWs w = make_ws(scr, gg ? gg->mq : m, K, &X2, &Y2);
+    CompressWs w = make_ws(scr, gg ? gg->mq : m, K, &X2, &Y2, gg ? 4 : 6);
     const int64_t mq = gg ? gg->mq : m, q0 = gg ? gg->q0 : 0;
     GangWs gw{};
     if (gg) gw = make_gws(gg->shared, K, gg->G);
@@ -828,7 +886,7 @@ __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl
                 if (rk == 0) continue;
                 const DRBlk b = c.rblk[r];
                 const double *Ub = r_U(c, r);
-                const double *Pb = slot_ptr(c, ct.aux);
+                const double *Pb = slot_get(c, ct.aux);
                 const int64_t uo = i * HCOV_LEAF - b.row0;
                 for (int e = threadIdx.x; e < 32 * rk; e += NT) {
                     int rr = e & 31, l = e >> 5;
@@ -836,7 +894,7 @@ __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl
                 }
                 for (int e = threadIdx.x; e < rk * nk; e += NT) {
                     int l = e % rk, k = e / rk;
-                    Xs[e] = __ldcg(Pb + l + (int64_t)c.kcap * (k0 + k));
+                    Xs[e] = __ldcg(Pb + l + (int64_t)rk * (k0 + k));
                 }
                 __syncthreads();
                 for (int e = threadIdx.x; e < 32 * nk; e += NT) {
@@ -878,7 +936,7 @@ __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl
     }
 }
 
-// P = V_b^T Y[cols of b]  (rank_b x ctot, ld kcap)
+// P = V_b^T Y[cols of b]  (rank_b x ctot, ld rank_b; allocated here with actual sizes)
 __device__ void task_proj(const Ctx &c, const DTask &tk, double *smem, double &fl)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -887,7 +945,12 @@ __device__ void task_proj(const Ctx &c, const DTask &tk, double *smem, double &f
     const DRBlk b = c.rblk[r];
     const int rk = __ldcg(c.rank + r);
     const double *Vb = r_V(c, r);
-    double *Pb = slot_ptr(c, tk.c);
+    int total = 1;
+    if (h.cnt > 0) {
+        total = 0;
+        for (int q = 0; q < h.cnt; ++q) total += __ldcg(c.rank + c.solve_rhs[h.off + q]);
+    }
+    double *Pb = slot_alloc(c, tk.c, (int64_t)rk * total + 1);
     double **colp = (double **)smem;
     __shared__ int s_nk, s_total;
     const int64_t co = b.col0 - h.row0;
@@ -904,7 +967,7 @@ __device__ void task_proj(const Ctx &c, const DTask &tk, double *smem, double &f
             double s = 0.0;
             for (int64_t q = lane; q < b.m; q += 32) s += __ldcg(vl + q) * __ldcg(y + q);
             s = warp_sum(s);
-            if (lane == 0) __stcg(Pb + l + (int64_t)c.kcap * (k0 + k), s);
+            if (lane == 0) __stcg(Pb + l + (int64_t)rk * (k0 + k), s);
         }
         fl += 2.0 * b.m * rk * nk;
         k0 += nk;
@@ -931,7 +994,7 @@ __device__ void task_prr(const Ctx &c, const DTask &tk, double &fl)
     fl += 2.0 * m * ra * rb;
 }
 
-// Q_x = V_x^T V_p[cols of x] for every partner p (Q: kcap x (kcap * part_cnt))
+// Q_x = V_x^T V_p[cols of x] for every partner p (Q: rank_x x sum of partner ranks, ld rank_x)
 __device__ void task_phwp(const Ctx &c, const DTask &tk, double &fl)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -942,8 +1005,10 @@ __device__ void task_phwp(const Ctx &c, const DTask &tk, double &fl)
     const DRBlk bx = c.rblk[x];
     const int rx = __ldcg(c.rank + x);
     const double *Vx = r_V(c, x);
-    double *Q = slot_ptr(c, tk.c);
+    const int tot = partner_prefix(c, q, q.part_cnt);
+    double *Q = slot_alloc(c, tk.c, (int64_t)rx * tot + 1);
     const int64_t co = bx.col0 - sig0;
+    int pre = 0;
     for (int p = 0; p < q.part_cnt; ++p) {
         const int rp_id = c.col_r[q.part_off + p];
         const int rp = __ldcg(c.rank + rp_id);
@@ -953,9 +1018,10 @@ __device__ void task_phwp(const Ctx &c, const DTask &tk, double &fl)
             double s = 0.0;
             for (int64_t i = lane; i < bx.m; i += 32) s += __ldcg(Vx + i + (int64_t)bx.m * l) * __ldcg(Vp + co + i + (int64_t)q.m * k);
             s = warp_sum(s);
-            if (lane == 0) __stcg(Q + l + (int64_t)c.kcap * (p * c.kcap + k), s);
+            if (lane == 0) __stcg(Q + l + (int64_t)rx * (pre + k), s);
         }
         fl += 2.0 * bx.m * rx * rp;
+        pre += rp;
     }
 }
 
@@ -971,11 +1037,15 @@ __device__ void task_phwr(const Ctx &c, const DTask &tk, double *smem, double &f
     double *Ts = Ws + 32 * (int64_t)c.kcap;   // 32 x 32
     double *Xs = Ts + HCOV_TILE;              // 32 x kcap
     double *Us = Xs + 32 * (int64_t)max(32, c.kcap);
+    const int tot = partner_prefix(c, q, q.part_cnt);
+    double *Wq = w_acquire(c, tk.a, (int64_t)q.m * tot + 1);
+    int pre = 0;
     for (int p = 0; p < q.part_cnt; ++p) {
         const int rp_id = c.col_r[q.part_off + p];
         const int rp = __ldcg(c.rank + rp_id);
         const double *Vp = r_V(c, rp_id);
-        double *Wp = c.W + (q.w_off + (int64_t)p * q.m) * c.kcap;
+        double *Wp = Wq + (int64_t)q.m * pre;
+        pre += rp;
         if (rp == 0) continue;
         for (int e = threadIdx.x; e < 32 * rp; e += NT) Ws[e] = 0.0;
         __syncthreads();
@@ -1003,7 +1073,7 @@ __device__ void task_phwr(const Ctx &c, const DTask &tk, double *smem, double &f
                 if (rx == 0) continue;
                 const DRBlk bx = c.rblk[x];
                 const double *Ux = r_U(c, x);
-                const double *Qx = slot_ptr(c, ct.aux);
+                const double *Qx = slot_get(c, ct.aux);
                 const int64_t uo = i * HCOV_LEAF - bx.row0;
                 for (int e = threadIdx.x; e < 32 * rx; e += NT) {
                     int rr = e & 31, l = e >> 5;
@@ -1011,7 +1081,7 @@ __device__ void task_phwr(const Ctx &c, const DTask &tk, double *smem, double &f
                 }
                 for (int e = threadIdx.x; e < rx * rp; e += NT) {
                     int l = e % rx, k = e / rx;
-                    Xs[e] = __ldcg(Qx + l + (int64_t)c.kcap * (p * c.kcap + k));
+                    Xs[e] = __ldcg(Qx + l + (int64_t)rx * (pre - rp + k));
                 }
                 __syncthreads();
                 for (int e = threadIdx.x; e < 32 * rp; e += NT) {
@@ -1040,5 +1110,7 @@ __host__ __device__ inline int64_t engine_smem_doubles(int kcap)
     int64_t b = 32 * SEG_MAXCOL + HCOV_TILE + k * SEG_MAXCOL + 32 * (int64_t)kcap + SEG_MAXCOL + 8;
     int64_t cc = 32 * (int64_t)kcap + HCOV_TILE + 32 * k + 32 * (int64_t)kcap + 8;
     int64_t m = a > b ? a : b;
-    return m > cc ? m : cc;
+    m = m > cc ? m : cc;
+    const int64_t floor_dbl = (NT >= 512) ? 16384 : 0;   // one CTA per SM: room for wider GEMM staging
+    return m > floor_dbl ? m : floor_dbl;
 }

@@ -131,15 +131,11 @@ __device__ __forceinline__ int ld_volatile(const int32_t *p) { return *(volatile
 
 __device__ __forceinline__ void push_ready(const Ctx &c, int32_t s)
 {
-    if (c.tasks[s].qcls == 0) {
-        const int b = c.tasks[s].band;
-        const uint32_t pos = atomicAdd(c.qctl + QC_BTAIL + b, 1u);
-        atomicExch(c.queue[0] + c.band_off[b] + pos, s);
-    } else {   // gang task of G CTAs: G consecutive tickets (task * 32 + member)
-        const int G = c.tasks[s].qcls;
-        const uint32_t pos = atomicAdd(c.qctl + QC_TAIL1, (uint32_t)G);
-        for (int g = 0; g < G; ++g) atomicExch(c.queue[1] + pos + g, s * 32 + g);
-    }
+    // entries are task * 32 + member; a gang task of G CTAs occupies G consecutive entries
+    const int b = c.tasks[s].band;
+    const int G = max(1, c.tasks[s].qcls);
+    const uint32_t pos = atomicAdd(c.qctl + QC_BTAIL + b, (uint32_t)G);
+    for (int g = 0; g < G; ++g) atomicExch(c.queue[0] + c.band_off[b] + pos + g, s * 32 + g);
 }
 
 // Release the successors of task t (all threads of the CTA; NOP joins complete inline).
@@ -169,7 +165,7 @@ __device__ void release(const Ctx &c, int32_t t, int mask, const int8_t *phase)
     }
 }
 
-__global__ void __launch_bounds__(NT, 4) k_engine(Ctx c, int mask, const int8_t *phase, EngineStats *stats,
+__global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const int8_t *phase, EngineStats *stats,
                                                unsigned long long *tl)
 {
     extern __shared__ double smem[];
@@ -221,7 +217,7 @@ __global__ void __launch_bounds__(NT, 4) k_engine(Ctx c, int mask, const int8_t 
             }
             __threadfence();
             s_member = 0;
-            if (q == 1 && t >= 0) { s_member = t & 31; t >>= 5; }
+            if (t >= 0) { s_member = t & 31; t >>= 5; }
             s_task = t;
             (void)pos;
         }
@@ -232,8 +228,8 @@ __global__ void __launch_bounds__(NT, 4) k_engine(Ctx c, int mask, const int8_t 
         Gang gang{s_member, tk.qcls, c.gbar + t, 0, 0, 0, nullptr};
         Gang *gg = nullptr;
         double *tscr = scr;
-        if (q == 1) {
-            // member 0 (the first ticket of the gang) lends the shared workspace of its scratch
+        if (tk.qcls > 0) {
+            // member 0 (the first entry of the gang) lends the shared workspace of its scratch
             __shared__ int32_t s_cta0;
             if (threadIdx.x == 0) {
                 if (gang.g == 0) {
@@ -248,8 +244,7 @@ __global__ void __launch_bounds__(NT, 4) k_engine(Ctx c, int mask, const int8_t 
             }
             __syncthreads();
             gg = &gang;
-            tscr = c.bscr + (int64_t)blockIdx.x * c.bscr_stride;
-            gang.shared = c.bscr + (int64_t)s_cta0 * c.bscr_stride + c.gshared_off;
+            gang.shared = c.scr + (int64_t)s_cta0 * c.scr_stride + c.gshared_off;
         }
         const unsigned long long t0 = gtimer();
         switch (tk.type) {
@@ -519,17 +514,22 @@ struct hcov_hmat_s {
     uint32_t *qctl = nullptr;
     double *scr = nullptr, *bscr = nullptr, *res = nullptr, *res_host = nullptr;
     double *ktab = nullptr, *ktab_host = nullptr;
+    int64_t *woff = nullptr, *poff = nullptr;
+    unsigned long long *mem = nullptr;
+    int64_t wcap = 0, pcap = 0;
     EngineStats *stats = nullptr, *stats_host = nullptr;
     void release_all()
     {
         void *ps[] = {tiles, U, V, cores, W, P, vbuf, logdet_part, minpiv_part, quad_part, rank, fail, flags,
-                      indeg, q0, q1, gbar, gslot, qctl, scr, bscr, res, stats};
+                      indeg, q0, q1, gbar, gslot, qctl, scr, bscr, res, stats, woff, poff, mem};
         for (void *p : ps) cudaFree(p);
         tiles = U = V = cores = W = P = vbuf = logdet_part = minpiv_part = quad_part = nullptr;
         rank = fail = flags = indeg = q0 = q1 = gbar = gslot = nullptr;
         qctl = nullptr;
         scr = bscr = res = nullptr;
         stats = nullptr;
+        woff = poff = nullptr;
+        mem = nullptr;
         kcap_alloc = -1;
     }
     ~hcov_hmat_s()
@@ -561,7 +561,7 @@ hcov_tree_s::~hcov_tree_s()
 
 namespace {
 
-const int NBIG = HCOV_GANG_CTAS;   // CTAs serving the gang queue
+const int NBIG = 0;   // (no dedicated gang CTAs: gangs are formed from the priority queue)
 
 hcov_status tree_upload(hcov_tree t)
 {
@@ -659,8 +659,11 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     CK(cudaMalloc(&h->U, std::max<int64_t>(1, P.uv_elems * kc) * sizeof(double)));
     CK(cudaMalloc(&h->V, std::max<int64_t>(1, P.uv_elems * kc) * sizeof(double)));
     CK(cudaMalloc(&h->cores, std::max<int64_t>(1, (int64_t)P.n_cores * kc * kc) * sizeof(double)));
-    CK(cudaMalloc(&h->W, std::max<int64_t>(1, P.w_elems * kc) * sizeof(double)));
-    CK(cudaMalloc(&h->P, std::max<int64_t>(1, P.slot_a * kc * kc + P.slot_b * kc) * sizeof(double)));
+    const int64_t wfull = P.w_elems * kc + (int64_t)P.phw.size() + 64;
+    const int64_t pfull = P.slot_a * kc * kc + P.slot_b * kc + (int64_t)P.slots.size() + 64;
+    CK(cudaMalloc(&h->woff, std::max<size_t>(1, P.phw.size()) * sizeof(int64_t)));
+    CK(cudaMalloc(&h->poff, std::max<size_t>(1, P.slots.size()) * sizeof(int64_t)));
+    CK(cudaMalloc(&h->mem, 4 * sizeof(unsigned long long)));
     CK(cudaMalloc(&h->vbuf, P.n_pad * sizeof(double)));
     CK(cudaMalloc(&h->logdet_part, P.n_leaves * sizeof(double)));
     CK(cudaMalloc(&h->minpiv_part, P.n_leaves * sizeof(double)));
@@ -685,21 +688,35 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engine, NT, (size_t)h->smem));
-    occ = std::max(1, std::min(occ, 4));
+    occ = std::max(1, std::min(occ, 512 / NT));
     h->grid = nsm * occ;
+    // per-CTA scratch: single-CTA tasks (blocks < HCOV_GANG_MIN, 6 panels) or a gang member's rows
+    // (m / G rows, 4 panels) followed by the gang's shared workspace (used when the CTA is member 0)
     const int64_t med_m = std::min<int64_t>(HCOV_GANG_MIN / 2, std::max<int64_t>(P.max_rm, 32));
-    const int64_t scr_stride = task_scratch(med_m, kcap);
-    const int nnorm = h->grid - NBIG;
-    CK(cudaMalloc(&h->scr, scr_stride * nnorm * sizeof(double)));
-    int64_t bscr_stride = 0, gshared_off = 0;
+    int64_t gshared_off = 0, scr_stride = task_scratch(med_m, kcap);
     if (P.max_mq > 0) {
-        gshared_off = task_scratch(P.max_mq, kcap);
-        bscr_stride = gshared_off + gang_shared_doubles(kbuf_of(kcap), HCOV_GANG);
-        CK(cudaMalloc(&h->bscr, bscr_stride * NBIG * sizeof(double)));
+        gshared_off = task_scratch(P.max_mq, kcap, 4);
+        scr_stride = std::max<int64_t>(scr_stride, gshared_off + gang_shared_doubles(kbuf_of(kcap), HCOV_GANG));
     }
-    h->ctx.gshared_off = gshared_off;
+    CK(cudaMalloc(&h->scr, scr_stride * (int64_t)h->grid * sizeof(double)));
     h->ctx.scr_stride = scr_stride;
-    h->ctx.bscr_stride = bscr_stride;
+    h->ctx.bscr_stride = 0;
+    h->ctx.gshared_off = gshared_off;
+    {
+        // W and product slots are allocated at run time with actual ranks (bump pools); the pools get
+        // the capacity-based sizes when they fit, else the free device memory (minus 3 GB headroom)
+        // split 70 / 30.  An overflow is detected and reported as HCOV_ERR_OUT_OF_MEMORY.
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        const int64_t avail = std::max<int64_t>(0, (int64_t)fr / 8 - ((int64_t)3 << 27));
+        if (wfull + pfull <= avail) { h->wcap = wfull; h->pcap = pfull; }
+        else {
+            h->wcap = std::min<int64_t>(wfull, (int64_t)(0.7 * avail));
+            h->pcap = std::min<int64_t>(pfull, avail - h->wcap);
+        }
+        CK(cudaMalloc(&h->W, std::max<int64_t>(1, h->wcap) * sizeof(double)));
+        CK(cudaMalloc(&h->P, std::max<int64_t>(1, h->pcap) * sizeof(double)));
+    }
     h->kcap_alloc = kcap;
     return HCOV_OK;
 }
@@ -718,6 +735,7 @@ void fill_ctx(hcov_hmat h)
     c.depth = P.depth; c.n_r = (int32_t)P.n_r(); c.root_solve = P.root_solve;
     c.n_pad = P.n_pad; c.n_leaves = P.n_leaves; c.n_real = P.n; c.n_tiles = P.n_tiles();
     c.tiles = h->tiles; c.U = h->U; c.V = h->V; c.rank = h->rank; c.cores = h->cores; c.W = h->W; c.P = h->P;
+    c.woff = h->woff; c.poff = h->poff; c.mem = h->mem; c.wcap = h->wcap; c.pcap = h->pcap;
     c.vbuf = h->vbuf; c.logdet_part = h->logdet_part; c.minpiv_part = h->minpiv_part; c.quad_part = h->quad_part;
     c.fail_leaf = h->fail; c.flags = h->flags;
     c.kcap = h->kcap_alloc; c.kmax = h->trunc.kmax; c.eps = h->trunc.eps;
@@ -819,17 +837,23 @@ hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trun
     CK(cudaMemsetAsync(h->flags, 0, 4 * sizeof(int32_t), st));
     CK(cudaMemsetAsync(h->fail, 0x7f, sizeof(int32_t), st));
     CK(cudaMemsetAsync(h->quad_part, 0, P.n_leaves * sizeof(double), st));
+    CK(cudaMemsetAsync(h->woff, 0xff, std::max<size_t>(1, P.phw.size()) * sizeof(int64_t), st));
+    CK(cudaMemsetAsync(h->poff, 0xff, std::max<size_t>(1, P.slots.size()) * sizeof(int64_t), st));
+    CK(cudaMemsetAsync(h->mem, 0, 4 * sizeof(unsigned long long), st));
     return HCOV_OK;
 }
 
 hcov_status check_abort(hcov_hmat h, cudaStream_t st, int32_t *hf)
 {
     uint32_t ab = 0;
+    unsigned long long mem[4] = {0, 0, 0, 0};
+    CK(cudaMemcpyAsync(mem, h->mem, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&ab, h->qctl + QC_ABORT, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf, h->fail, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf + 1, h->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (ab) return HCOV_ERR_CUDA;
+    if (mem[2]) return HCOV_ERR_OUT_OF_MEMORY;
     return HCOV_OK;
 }
 
@@ -924,6 +948,9 @@ hcov_status hcov_tree_get_info(hcov_tree t, hcov_tree_info *info)
     info->n = P.n; info->n_pad = P.n_pad; info->depth = P.depth; info->leaf_size = HCOV_LEAF;
     info->n_leaves = P.n_leaves; info->n_dense_tiles = P.n_tiles(); info->n_lowrank = P.n_r();
     info->n_tasks = (int64_t)P.tasks.size(); info->n_waves = P.crit_len; info->eta = P.opt.eta;
+    info->uv_elems = P.uv_elems; info->w_elems = P.w_elems; info->slot_a = P.slot_a; info->slot_b = P.slot_b;
+    info->n_cores = P.n_cores; info->n_edges = (int64_t)P.succ.size(); info->n_xterm = (int64_t)P.xterm.size();
+    info->max_mq = P.max_mq;
     return HCOV_OK;
 }
 

@@ -5,10 +5,11 @@
 
 #define HCOV_LEAF 32
 #define HCOV_TILE (HCOV_LEAF * HCOV_LEAF)
-#define HCOV_GANG 16          // largest gang: CTAs cooperating on one task of the gang queue (queue 1)
-#define HCOV_GANG_CTAS 128    // CTAs serving queue 1 (>= HCOV_GANG, so every gang can form)
+#define HCOV_GANG 8           // largest gang (CTAs cooperating on one task); HCOV_BANDS * (HCOV_GANG - 1)
+                              // must stay below the number of engine CTAs (at most one partially
+                              // formed gang per band can hold CTAs, so every gang eventually forms)
 #define HCOV_DENSE_MAX 256    // low-rank blocks up to this size are recompressed from a dense accumulation
-#define HCOV_GANG_MIN 2048    // low-rank blocks from this size on are processed by gangs of m/1024 CTAs
+#define HCOV_GANG_MIN 512     // low-rank blocks from this size on are processed by gangs of min(8, m/256) CTAs
 
 // Block-tree node types (lower triangle incl. diagonal).
 enum NodeType : int32_t { ND_H = 0, ND_R = 1, ND_T = 2 };
@@ -50,7 +51,7 @@ enum TaskType : int32_t {
 struct DTask {
     int32_t type;
     int32_t a, b, c, d;
-    int32_t qcls;      // 0 = one CTA (queue 0); G > 1 = gang task of G CTAs (queue 1)
+    int32_t qcls;      // 0 = one CTA; G > 1 = gang task of G CTAs (G consecutive queue entries)
     int32_t band;      // queue 0 priority band (HCOV_BANDS - 1 = most urgent), by the task's bottom level
     int32_t pad;
 };

@@ -102,27 +102,42 @@ __device__ __forceinline__ void tile_gemm_nt_sub(double *S, const double *A, con
 // ------------------------------------------------------------------------------------------
 #define GEMM_JC 16
 __device__ void cta_gemm_nt(double *Cp, int64_t ldc, int64_t nr, int64_t nc, int kd, const double *Ap, int64_t lda,
-                            const double *Bp, int64_t bsj, int64_t bsl, double alpha, double *smem)
+                            const double *Bp, int64_t bsj, int64_t bsl, double alpha, double *smem,
+                            int64_t smem_dbl = 0)
 {
-    for (int64_t j0 = 0; j0 < nc; j0 += GEMM_JC) {
-        const int jc = (int)(nc - j0 < GEMM_JC ? nc - j0 : GEMM_JC);
+    // thread t: row group i = t % rp (rows i, i + rp, ...), column-chunk group g = t / rp; ng chunk
+    // groups are staged at once (when there are fewer rows than threads)
+    const int rp = (int)(nr < NT ? nr : NT);
+    int ng = NT / (rp > 0 ? rp : 1);
+    const int64_t per = (int64_t)GEMM_JC * (kd > 0 ? kd : 1);
+    if (smem_dbl < per * ng) ng = (int)(smem_dbl / per > 1 ? smem_dbl / per : 1);
+    const int g = threadIdx.x / (rp > 0 ? rp : 1);
+    const int i0 = threadIdx.x % (rp > 0 ? rp : 1);
+    for (int64_t j0 = 0; j0 < nc; j0 += (int64_t)GEMM_JC * ng) {
         __syncthreads();
-        for (int e = threadIdx.x; e < GEMM_JC * kd; e += NT) {
-            const int jj = e % GEMM_JC, l = e / GEMM_JC;
-            smem[e] = (jj < jc) ? __ldcg(Bp + (j0 + jj) * bsj + (int64_t)l * bsl) : 0.0;
+        for (int e = threadIdx.x; e < GEMM_JC * kd * ng; e += NT) {
+            const int gg = e / (GEMM_JC * kd), e2 = e % (GEMM_JC * kd);
+            const int jj = e2 % GEMM_JC, l = e2 / GEMM_JC;
+            const int64_t j = j0 + (int64_t)gg * GEMM_JC + jj;
+            smem[e] = (j < nc) ? __ldcg(Bp + j * bsj + (int64_t)l * bsl) : 0.0;
         }
         __syncthreads();
-        for (int64_t i = threadIdx.x; i < nr; i += NT) {
-            double acc[GEMM_JC];
+        const int64_t jg = j0 + (int64_t)g * GEMM_JC;
+        if (g < ng && jg < nc) {
+            const int jc = (int)(nc - jg < GEMM_JC ? nc - jg : GEMM_JC);
+            const double *sb = smem + (int64_t)g * GEMM_JC * kd;
+            for (int64_t i = i0; i < nr; i += rp) {
+                double acc[GEMM_JC];
 #pragma unroll
-            for (int jj = 0; jj < GEMM_JC; ++jj) acc[jj] = 0.0;
-            for (int l = 0; l < kd; ++l) {
-                const double a = __ldcg(Ap + i + (int64_t)l * lda);
-                const double *bl = smem + GEMM_JC * l;
+                for (int jj = 0; jj < GEMM_JC; ++jj) acc[jj] = 0.0;
+                for (int l = 0; l < kd; ++l) {
+                    const double a = __ldcg(Ap + i + (int64_t)l * lda);
+                    const double *bl = sb + GEMM_JC * l;
 #pragma unroll
-                for (int jj = 0; jj < GEMM_JC; ++jj) acc[jj] = fma(a, bl[jj], acc[jj]);
+                    for (int jj = 0; jj < GEMM_JC; ++jj) acc[jj] = fma(a, bl[jj], acc[jj]);
+                }
+                for (int jj = 0; jj < jc; ++jj) Cp[i + (jg + jj) * ldc] += alpha * acc[jj];
             }
-            for (int jj = 0; jj < jc; ++jj) Cp[i + (j0 + jj) * ldc] += alpha * acc[jj];
         }
     }
     __syncthreads();

@@ -23,7 +23,7 @@ namespace {
 inline int32_t gang_of(int64_t m)
 {
     if (m < HCOV_GANG_MIN) return 0;
-    return (int32_t)std::min<int64_t>(HCOV_GANG, m / 1024);
+    return (int32_t)std::min<int64_t>(HCOV_GANG, std::max<int64_t>(2, m / 256));
 }
 
 inline int64_t heap_id(int l, int64_t c) { return ((int64_t)1 << l) - 1 + c; }
@@ -289,7 +289,7 @@ struct Builder {
             P.fac_row0.push_back((int64_t)h.i * m);
             P.fac_nrows.push_back((int32_t)m);
             P.fac_rank_src.push_back(rents[p]);
-            P.fac_off.push_back(q.w_off + (int64_t)p * m);
+            P.fac_off.push_back(((int64_t)qid << 8) | p);   // W slice: (phw id, partner index), offset at run time
             P.fac_pool.push_back(1);
         }
         P.phw.push_back(q);
@@ -584,7 +584,7 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
             int b = (int)std::floor(HCOV_BANDS * bl[t] / (bmax + 1e-9));
             b = std::min(HCOV_BANDS - 1, std::max(0, b));
             P.tasks[t].band = b;
-            if (P.tasks[t].type != TK_NOP && P.tasks[t].qcls == 0) cnt[b]++;
+            if (P.tasks[t].type != TK_NOP) cnt[b] += std::max(1, P.tasks[t].qcls);
         }
         P.band_off.assign(HCOV_BANDS + 1, 0);
         for (int b = 0; b < HCOV_BANDS; ++b) P.band_off[b + 1] = P.band_off[b] + std::max(1, cnt[b]);
@@ -600,10 +600,9 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
                 if (mask[md] & (1 << P.phase[d])) ++cnt;
             P.indeg[md][t] = cnt;
             const DTask &k = P.tasks[t];
-            // queue 1 holds G tickets per gang task of G CTAs, encoded task * 32 + member
-            const int qc = k.qcls ? 1 : 0;
-            if (k.type != TK_NOP) P.n_q[md][qc] += k.qcls ? k.qcls : 1;
-            if (cnt == 0) rk[qc].push_back({key[t], t});   // (a NOP always has a dependency)
+            // one queue: a gang task of G CTAs occupies G consecutive entries (task * 32 + member)
+            if (k.type != TK_NOP) P.n_q[md][0] += 1;
+            if (cnt == 0) rk[0].push_back({key[t], t});   // (a NOP always has a dependency)
         }
         {
             // queue 0: roots placed in their bands in key order
@@ -612,7 +611,8 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
             P.q0tail[md].assign(HCOV_BANDS, 0);
             for (auto &pr : rk[0]) {
                 const int b = P.tasks[pr.second].band;
-                P.q0init[md][P.band_off[b] + P.q0tail[md][b]++] = pr.second;
+                const int G = std::max(1, P.tasks[pr.second].qcls);
+                for (int g = 0; g < G; ++g) P.q0init[md][P.band_off[b] + P.q0tail[md][b]++] = pr.second * 32 + g;
             }
         }
         for (int c = 0; c < 2; ++c) {

@@ -12,14 +12,14 @@ sys.path.insert(0, ".")
 NAMES = ["fill", "aca", "tapp", "potrf", "trsm", "rapp", "seg", "proj", "prr", "phwp", "phwr", "nop"]
 
 
-def run(tag, n, nu, ell, eps, kmax, kcap=0):
+def run(tag, n, nu, ell, eps, kmax, kcap=0, nugget=1e-6):
     import torch
     import synth
     import paper_1709_08625_b200 as H
     s = synth.uniform_points(n, 1005)
     T = H.Tree(torch.from_numpy(s).cuda())
     Z = torch.from_numpy(synth.xi(n, 2005)).cuda()
-    th = (1.0, ell, nu, 1e-6)
+    th = (1.0, ell, nu, nugget)
     r = H.eval_loglik(T, th, Z, eps, kmax, kcap)      # warm-up (allocations)
     path = f"/tmp/{tag}.bin"
     os.environ["HCOV_TIMELINE"] = path
@@ -119,6 +119,7 @@ def show(path):
 if __name__ == "__main__":
     if sys.argv[1] == "run":
         a = sys.argv[2:]
-        run(a[0], int(a[1]), float(a[2]), float(a[3]), float(a[4]), int(a[5]), int(a[6]) if len(a) > 6 else 0)
+        run(a[0], int(a[1]), float(a[2]), float(a[3]), float(a[4]), int(a[5]), int(a[6]) if len(a) > 6 else 0,
+            float(a[7]) if len(a) > 7 else 1e-6)
     else:
         show(sys.argv[2])
