@@ -170,6 +170,8 @@ typedef struct {
     double phase_ms[16];               /* CTA-time of truncation phases: 0 panel QRs, 1 core product,
                                           2 pivoted QR, 3 SVD, 4 Q applications, 5 full-pivot ACA,
                                           6 dense updates, 8 partial ACA */
+    double phase_cls_ms[64];           /* the same per block-size class (phase + 16 * class; classes
+                                          m <= 64, <= 256, <= 1024, larger) */
 } hcov_prof;
 hcov_status hcov_prof_control(int32_t enable_events, int32_t reset);
 hcov_status hcov_prof_read(hcov_prof *out);

@@ -62,7 +62,8 @@ class Prof(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("n_task_types", ctypes.c_int32),
                 ("count", ctypes.c_int64 * 16), ("ms", ctypes.c_double * 16),
                 ("task_busy_ms", ctypes.c_double * 16), ("task_count", ctypes.c_double * 16),
-                ("flop", ctypes.c_double * 8), ("phase_ms", ctypes.c_double * 16)]
+                ("flop", ctypes.c_double * 8), ("phase_ms", ctypes.c_double * 16),
+                ("phase_cls_ms", ctypes.c_double * 64)]
 
 
 # name -> (restype, argtypes) ; every symbol declared in include/hcov.h
@@ -298,7 +299,10 @@ def prof_read() -> dict:
             "task_busy_ms": {nm: p.task_busy_ms[k] for k, nm in enumerate(tnames)},
             "task_count": {nm: int(p.task_count[k]) for k, nm in enumerate(tnames)},
             "flop": {nm: p.flop[k] for k, nm in enumerate(FLOP_CLASSES)},
-            "phase_ms": {nm: p.phase_ms[k] for k, nm in enumerate(PHASES) if nm}}
+            "phase_ms": {nm: p.phase_ms[k] for k, nm in enumerate(PHASES) if nm},
+            "phase_cls_ms": {f"{cls}:{nm}": round(p.phase_cls_ms[k + 16 * ci], 1)
+                             for ci, cls in enumerate(["m<=64", "m<=256", "m<=1024", "m>1024"])
+                             for k, nm in enumerate(PHASES) if nm and p.phase_cls_ms[k + 16 * ci] > 0}}
 
 
 PHASES = ["panel_qr", "core_product", "pivoted_qr", "svd", "q_apply", "aca_full", "dense_updates", "",

@@ -66,8 +66,9 @@ __device__ __forceinline__ double ldg_cg(const double *p) { return __ldcg(p); }
 
 // Phase timers (diagnostics, hcov_prof with events enabled): thread 0 of a CTA accumulates
 // globaltimer spans of the truncation phases into g_phase_ns.
-__device__ unsigned long long g_phase_ns[16];
+__device__ unsigned long long g_phase_ns[64];   // phase + 16 * size class
 __device__ int g_phase_on;
+__shared__ int s_phase_cls;                      // size class of the running task (0..3)
 __device__ __forceinline__ unsigned long long ph_now()
 {
     unsigned long long t;
@@ -77,5 +78,5 @@ __device__ __forceinline__ unsigned long long ph_now()
 #define PH_BEGIN(v) const unsigned long long v = (g_phase_on && threadIdx.x == 0) ? ph_now() : 0ull
 #define PH_END(k, v)                                                  \
     do {                                                              \
-        if (g_phase_on && threadIdx.x == 0) atomicAdd(&g_phase_ns[k], ph_now() - (v)); \
+        if (g_phase_on && threadIdx.x == 0) atomicAdd(&g_phase_ns[(k) + 16 * s_phase_cls], ph_now() - (v)); \
     } while (0)

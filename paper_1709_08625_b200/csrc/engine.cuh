@@ -216,13 +216,7 @@ __device__ double tile_apply_term(const Ctx &c, const DTerm &t, int64_t R0, int6
         fl += 2.0 * 32 * ra * rb;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
-        int i = e & 31, j = e >> 5;
-        double s = 0.0;
-        for (int b = 0; b < rb; ++b) s += T1[i + 32 * b] * sm.B[j + 32 * b];
-        sm.S[e] -= s;
-    }
-    __syncthreads();
+    tile_gemm_nt_sub_k(sm.S, T1, sm.B, rb);   // DMMA
     return fl;
 }
 

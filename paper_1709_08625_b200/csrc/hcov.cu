@@ -60,7 +60,7 @@ struct Prof {
     double busy_ns[TK_NTYPES] = {};
     double tasks[TK_NTYPES] = {};
     double flop[FC_N] = {};
-    double phase_ns[16] = {};
+    double phase_ns[64] = {};
 };
 Prof g_prof;
 
@@ -247,6 +247,15 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
             gang.shared = c.scr + (int64_t)s_cta0 * c.scr_stride + c.gshared_off;
         }
         const unsigned long long t0 = gtimer();
+        if (threadIdx.x == 0) {
+            int pc = 0;
+            if (tk.type == TK_RAPP || tk.type == TK_ACA) {
+                const int64_t m = c.rblk[tk.a].m;
+                pc = m <= 64 ? 0 : m <= 256 ? 1 : m <= 1024 ? 2 : 3;
+            }
+            s_phase_cls = pc;
+        }
+        __syncthreads();
         switch (tk.type) {
         case TK_FILL: task_fill(c, tk, fl[FC_ASM]); break;
         case TK_ACA: task_aca(c, tk, tscr, smem, red, redv, redi, fl[FC_ASM], fl[FC_TRUNC], gg); break;
@@ -771,7 +780,7 @@ hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
     EngineStats *stats = g_prof.events ? h->stats : nullptr;
     if (stats) CK(cudaMemsetAsync(h->stats, 0, sizeof(EngineStats), st));
     {
-        static const unsigned long long zeros[16] = {};
+        static const unsigned long long zeros[64] = {};
         const int on = stats ? 1 : 0;
         CK(cudaMemcpyToSymbolAsync(g_phase_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
         if (on) CK(cudaMemcpyToSymbolAsync(g_phase_ns, zeros, sizeof(zeros), 0, cudaMemcpyHostToDevice, st));
@@ -803,9 +812,9 @@ hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
             g_prof.tasks[k] += (double)h->stats_host->tasks[k];
         }
         for (int k = 0; k < FC_N; ++k) g_prof.flop[k] += h->stats_host->flop[k];
-        unsigned long long ph[16];
+        unsigned long long ph[64];
         CK(cudaMemcpyFromSymbol(ph, g_phase_ns, sizeof(ph)));
-        for (int k = 0; k < 16; ++k) g_prof.phase_ns[k] += (double)ph[k];
+        for (int k = 0; k < 64; ++k) g_prof.phase_ns[k] += (double)ph[k];
     }
     return HCOV_OK;
 }
@@ -1174,7 +1183,7 @@ hcov_status hcov_prof_control(int32_t enable_events, int32_t reset)
         for (int k = 0; k < PC_N; ++k) { g_prof.count[k] = 0; g_prof.ms[k] = 0.0; }
         for (int k = 0; k < TK_NTYPES; ++k) { g_prof.busy_ns[k] = 0; g_prof.tasks[k] = 0; }
         for (int k = 0; k < FC_N; ++k) g_prof.flop[k] = 0;
-        for (int k = 0; k < 16; ++k) g_prof.phase_ns[k] = 0;
+        for (int k = 0; k < 64; ++k) g_prof.phase_ns[k] = 0;
     }
     g_prof.events = enable_events != 0;
     return HCOV_OK;
@@ -1197,7 +1206,10 @@ hcov_status hcov_prof_read(hcov_prof *out)
         out->task_count[k] = g_prof.tasks[k];
     }
     for (int k = 0; k < FC_N; ++k) out->flop[k] = g_prof.flop[k];
-    for (int k = 0; k < 16; ++k) out->phase_ms[k] = g_prof.phase_ns[k] * 1e-6;
+    for (int k = 0; k < 64; ++k) {
+        out->phase_ms[k % 16] += g_prof.phase_ns[k] * 1e-6;
+        out->phase_cls_ms[k] = g_prof.phase_ns[k] * 1e-6;
+    }
     return HCOV_OK;
 }
 

@@ -81,16 +81,41 @@ __device__ __forceinline__ void tile_trsm_rt(double *X, const double *L)
 }
 
 // S -= A B^T  (all 32x32 shared)
-__device__ __forceinline__ void tile_gemm_nt_sub(double *S, const double *A, const double *B)
+// FP64 tensor-core (DMMA) tile update on sm_100a: mma.sync.aligned.m8n8k4.row.col.f64.
+// Fragments (PTX ISA, m8n8k4 .f64): lane l, g = l / 4, t = l % 4:  a = A[g][t] (8x4 row),
+// b = B[t][g] (4x8 col), c = {C[g][2t], C[g][2t+1]}.
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b)
 {
-    for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
-        int i = e & 31, j = e >> 5;
-        double s = 0.0;
-#pragma unroll 8
-        for (int k = 0; k < 32; ++k) s += A[i + 32 * k] * B[j + 32 * k];
-        S[e] -= s;
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// S (32 x 32, ld 32) -= A (32 x kd, ld 32) B^T (B 32 x kd, ld 32), all in shared memory; kd is
+// padded to a multiple of 4 with zeros.  One warp per 8 x 8 output block (16 blocks).
+__device__ __forceinline__ void tile_gemm_nt_sub_k(double *S, const double *A, const double *B, int kd)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    for (int blk = warp; blk < 16; blk += NWARP) {
+        const int bi = blk >> 2, bj = blk & 3;
+        double c0 = 0.0, c1 = 0.0;
+        for (int k0 = 0; k0 < kd; k0 += 4) {
+            const int k = k0 + t;
+            const double a = (k < kd) ? A[(8 * bi + g) + 32 * k] : 0.0;
+            const double b = (k < kd) ? B[(8 * bj + g) + 32 * k] : 0.0;
+            dmma_8x8x4(c0, c1, a, b);
+        }
+        S[(8 * bi + g) + 32 * (8 * bj + 2 * t)] -= c0;
+        S[(8 * bi + g) + 32 * (8 * bj + 2 * t + 1)] -= c1;
     }
     __syncthreads();
+}
+
+// S -= A B^T  (all 32x32 shared)
+__device__ __forceinline__ void tile_gemm_nt_sub(double *S, const double *A, const double *B)
+{
+    tile_gemm_nt_sub_k(S, A, B, 32);
 }
 
 // ------------------------------------------------------------------------------------------

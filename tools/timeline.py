@@ -33,6 +33,7 @@ def run(tag, n, nu, ell, eps, kmax, kcap=0, nugget=1e-6):
     pr = H.prof_read()
     H.prof_control(False, True)
     print("phases ms:", {k: round(v, 1) for k, v in pr["phase_ms"].items()}, "flop:", pr["flop"], flush=True)
+    print("phases by class:", pr["phase_cls_ms"], flush=True)
     del os.environ["HCOV_TIMELINE"]
     tl = np.fromfile(path, dtype=np.uint64).reshape(-1, 3)
     off, sc = T.succ()
