@@ -341,7 +341,7 @@ struct GangWs {
     int64_t *pi;           // 2 x G partial indices
     double *ps;            // 2 x G x 2 partial sums
     double *urow, *vrow;   // K each: published pivot row of U / pivot column of V (ACA)
-    int32_t *ires;         // [0] r, [1] cb, [2] of
+    int32_t *ires;         // [0] r, [1] cb, [2] of, [3] CholeskyQR breakdown flag
 };
 __host__ __device__ inline int64_t gang_shared_doubles(int K, int G)
 {
@@ -367,17 +367,19 @@ __device__ __forceinline__ GangWs make_gws(double *base, int K, int G)
 }
 
 // Gang truncation of X Y^T (m x m, R columns; member rows in the local panels w.X, w.Y with
-// ld mq >= R): local Householder QR per member (TSQR leaves), QR of the stacked R factors and the
-// core (compress_core) by member 0, then every member applies its local Q to its rows of the
-// result U, V (global, ld ldo, rows q0..q0+mq).
+// ld mq >= R): local Householder QR per member (TSQR leaves); CholeskyQR3 of the stacked R factors
+// of X by member 0 and of Y by member 1 in parallel (explicit Q_s); the core M = R_X R_Y^T
+// (compress_core) by member 0; then every member forms its rows [(Q_s)_g U_core; 0] and applies
+// its local Q (rows q0..q0+mq of the result U, V; global, ld ldo).
 __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, int R, double eps, double tol_q,
                              bool svd, int kmax, int rlim, double *U, double *V, int64_t ldo, int *cb, int *of,
-                             double *red, double *redv, int64_t *redi)
+                             double *red, double *redv, int64_t *redi, double *smem, int64_t smem_dbl)
 {
     if (R == 0) { *cb = 0; *of = 0; return 0; }
     const int G = gg.G, g = gg.g;
     const int64_t mq = gg.mq, q0 = gg.q0;
     const int64_t GR = (int64_t)G * R;
+    // phase 1 (all members): local Householder QR of the member's rows (TSQR leaves)
     qr_house(w.X, mq, mq, R, w.tx, red);
     qr_house(w.Y, mq, mq, R, w.ty, red);
     for (int e = threadIdx.x; e < R * R; e += NT) {
@@ -385,26 +387,58 @@ __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, in
         __stcg(gw.RSX + (int64_t)g * R + i + GR * k, (k >= i) ? w.X[i + mq * k] : 0.0);
         __stcg(gw.RSY + (int64_t)g * R + i + GR * k, (k >= i) ? w.Y[i + mq * k] : 0.0);
     }
+    if (g == 0 && threadIdx.x == 0) gw.ires[3] = 0;
     gang_sync(gg);
-    if (g == 0) {
-        qr_house(gw.RSX, GR, GR, R, gw.tsx, red);
-        qr_house(gw.RSY, GR, GR, R, gw.tsy, red);
-        int c1 = 0, o1 = 0;
-        const int r = compress_core(w, gw.RSX, GR, gw.RSY, GR, R, eps, tol_q, svd, kmax, rlim, gw.UC, gw.VC, GR, GR,
-                                    &c1, &o1, red, redv, redi);
-        qr_apply_q(gw.RSX, GR, GR, R, gw.tsx, gw.UC, GR, r);
-        qr_apply_q(gw.RSY, GR, GR, R, gw.tsy, gw.VC, GR, r);
-        if (threadIdx.x == 0) { gw.ires[0] = r; gw.ires[1] = c1; gw.ires[2] = o1; }
+    // phase 2a: member 0 factors the stacked R_X's, member 1 the stacked R_Y's (CholeskyQR3,
+    // explicit Q_s in UC / VC); R_Y is published in RSY
+    __shared__ int s_ok;
+    if (g == 0 || g == 1) {
+        double *src = (g == 0) ? gw.RSX : gw.RSY;
+        double *pp = (g == 0) ? gw.UC : gw.VC;
+        double *Q = nullptr;
+        bool ok = cholqr3(src, pp, GR, R, (g == 0) ? w.RX : w.RY, w.M, w.G, w.Ri, w.dX, smem, smem_dbl, red, &Q);
+        if (threadIdx.x == 0) s_ok = ok;
+        __syncthreads();
+        if (g == 1) {
+            for (int e = threadIdx.x; e < R * R; e += NT) __stcg(gw.RSY + e, w.RY[e]);
+        }
+        if (threadIdx.x == 0 && !s_ok) atomicExch(gw.ires + 3, 1);
     }
     gang_sync(gg);
+    // phase 2b: member 0 truncates the core M = R_X R_Y^T; cores published in RSX / RSY + R^2
+    if (g == 0) {
+        int c1 = 0, o1 = 0, r = 0;
+        if (__ldcg(gw.ires + 3) == 0) {
+            for (int e = threadIdx.x; e < R * R; e += NT) w.RY[e] = __ldcg(gw.RSY + e);
+            __syncthreads();
+            r = compress_core(w, w.RX, R, w.RY, R, R, eps, tol_q, svd, kmax, rlim, w.UC, w.VC, R, R, &c1, &o1, red,
+                              redv, redi);
+            for (int e = threadIdx.x; e < R * r; e += NT) {
+                __stcg(gw.RSX + e, w.UC[e]);
+                __stcg(gw.RSY + (int64_t)R * R + e, w.VC[e]);
+            }
+        } else {
+            o1 = 1;
+        }
+        if (threadIdx.x == 0) { gw.ires[0] = r; gw.ires[1] = c1; gw.ires[2] = o1; gw.ires[3] = 0; }
+    }
+    gang_sync(gg);
+    // phase 3 (all members): rows of U = Q_Xg [ (Q_sx)_g U_core ; 0 ], V likewise
     const int r = __ldcg(gw.ires);
     *cb = __ldcg(gw.ires + 1);
     *of = __ldcg(gw.ires + 2);
     for (int64_t e = threadIdx.x; e < mq * r; e += NT) {
         const int64_t i = e % mq;
-        const int c = (int)(e / mq);
-        U[q0 + i + ldo * c] = (i < R) ? __ldcg(gw.UC + (int64_t)g * R + i + GR * c) : 0.0;
-        V[q0 + i + ldo * c] = (i < R) ? __ldcg(gw.VC + (int64_t)g * R + i + GR * c) : 0.0;
+        const int cc = (int)(e / mq);
+        double su = 0.0, sv = 0.0;
+        if (i < R) {
+            for (int l = 0; l < R; ++l) {
+                su += __ldcg(gw.UC + (int64_t)g * R + i + GR * l) * __ldcg(gw.RSX + l + (int64_t)R * cc);
+                sv += __ldcg(gw.VC + (int64_t)g * R + i + GR * l) * __ldcg(gw.RSY + (int64_t)R * R + l + (int64_t)R * cc);
+            }
+        }
+        U[q0 + i + ldo * cc] = su;
+        V[q0 + i + ldo * cc] = sv;
     }
     __syncthreads();
     qr_apply_q(w.X, mq, mq, R, w.tx, U + q0, ldo, r);
@@ -566,7 +600,7 @@ __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *sme
         k = gang_aca(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, (uint8_t *)w.tail, K, 0.1 * c.eps, gw, *gg, red,
                      redv, redi);
         rk = gang_compress(w, gw, *gg, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m,
-                           &cb, &of, red, redv, redi);
+                           &cb, &of, red, redv, redi, smem, c.smem_dbl);
         if (gg->g == 0) record_rank(c, r, rk, cb, of);
     }
     const double share = gg ? 1.0 / gg->G : 1.0;
@@ -712,7 +746,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
             int icb = 0, iof = 0, rk;
             if (gg)
                 rk = gang_compress(w, gw, *gg, cur, c.eps, interm_tol(c.eps), false, 0, K - maxw, X2 - q0, Y2 - q0, mq,
-                                   &icb, &iof, red, redv, redi);
+                                   &icb, &iof, red, redv, redi, smem, c.smem_dbl);
             else
                 rk = compress(w, m, cur, c.eps, interm_tol(c.eps), false, 0, K - maxw, X2, Y2, m, &icb, &iof, red,
                               redv, redi, smem, c.smem_dbl);
@@ -769,7 +803,8 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     const int kmx = fin ? c.kmax : 0, rl = fin ? c.kcap : 2 * c.kcap;
     int rk;
     if (gg) {
-        rk = gang_compress(w, gw, *gg, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi);
+        rk = gang_compress(w, gw, *gg, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi, smem,
+                           c.smem_dbl);
         fl += compress_flops(m, cur, rk) / gg->G;
     } else {
         rk = compress(w, m, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi, smem, c.smem_dbl);
