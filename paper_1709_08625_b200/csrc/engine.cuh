@@ -321,6 +321,7 @@ struct Gang {
 };
 __device__ __forceinline__ void gang_sync(Gang &gg)
 {
+    PH_BEGIN(tw);
     __syncthreads();
     ++gg.nb;
     if (threadIdx.x == 0) {
@@ -331,6 +332,7 @@ __device__ __forceinline__ void gang_sync(Gang &gg)
         __threadfence();
     }
     __syncthreads();
+    PH_END(13, tw);
 }
 
 struct GangWs {
@@ -367,10 +369,11 @@ __device__ __forceinline__ GangWs make_gws(double *base, int K, int G)
 }
 
 // Gang truncation of X Y^T (m x m, R columns; member rows in the local panels w.X, w.Y with
-// ld mq >= R): local Householder QR per member (TSQR leaves); CholeskyQR3 of the stacked R factors
-// of X by member 0 and of Y by member 1 in parallel (explicit Q_s); the core M = R_X R_Y^T
-// (compress_core) by member 0; then every member forms its rows [(Q_s)_g U_core; 0] and applies
-// its local Q (rows q0..q0+mq of the result U, V; global, ld ldo).
+// ld mq >= R): local Householder QR per member (TSQR leaves); QR of the stacked R factors of X by
+// member 0 and of Y by member 1 in parallel; the core M = R_X R_Y^T (compress_core) by member 0;
+// the stacked Q's applied to the cores (members 0 and 1); then every member applies its local Q
+// to its rows [core block g; 0] of the result U, V (global, ld ldo, rows q0..q0+mq).  Panels that
+// fit are factored in shared memory (qr_house_sm / apply_q_sm), larger ones in global memory.
 __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, int R, double eps, double tol_q,
                              bool svd, int kmax, int rlim, double *U, double *V, int64_t ldo, int *cb, int *of,
                              double *red, double *redv, int64_t *redi, double *smem, int64_t smem_dbl)
@@ -379,70 +382,111 @@ __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, in
     const int G = gg.G, g = gg.g;
     const int64_t mq = gg.mq, q0 = gg.q0;
     const int64_t GR = (int64_t)G * R;
+    const bool loc_sm = mq <= 1024 && mq * R + R <= smem_dbl;
+    const bool stk_sm = GR <= 1024 && GR * R + R <= smem_dbl;
+    double *As = smem, *ts = smem + (loc_sm ? mq * R : GR * R);
     // phase 1 (all members): local Householder QR of the member's rows (TSQR leaves)
-    qr_house(w.X, mq, mq, R, w.tx, red);
-    qr_house(w.Y, mq, mq, R, w.ty, red);
+    PH_BEGIN(t1);
+    if (loc_sm) {
+        ts = smem + mq * R;
+        panel_to_sm(As, w.X, mq, (int)mq, R);
+        qr_house_sm(As, (int)mq, (int)mq, R, ts);
+        for (int e = threadIdx.x; e < R; e += NT) w.tx[e] = ts[e];
+        panel_from_sm(w.X, mq, As, (int)mq, R);
+        panel_to_sm(As, w.Y, mq, (int)mq, R);
+        qr_house_sm(As, (int)mq, (int)mq, R, ts);
+        for (int e = threadIdx.x; e < R; e += NT) w.ty[e] = ts[e];
+        panel_from_sm(w.Y, mq, As, (int)mq, R);
+    } else {
+        qr_house(w.X, mq, mq, R, w.tx, red);
+        qr_house(w.Y, mq, mq, R, w.ty, red);
+    }
     for (int e = threadIdx.x; e < R * R; e += NT) {
         const int i = e % R, k = e / R;
         __stcg(gw.RSX + (int64_t)g * R + i + GR * k, (k >= i) ? w.X[i + mq * k] : 0.0);
         __stcg(gw.RSY + (int64_t)g * R + i + GR * k, (k >= i) ? w.Y[i + mq * k] : 0.0);
     }
-    if (g == 0 && threadIdx.x == 0) gw.ires[3] = 0;
+    PH_END(9, t1);
     gang_sync(gg);
-    // phase 2a: member 0 factors the stacked R_X's, member 1 the stacked R_Y's (CholeskyQR3,
-    // explicit Q_s in UC / VC); R_Y is published in RSY
-    __shared__ int s_ok;
-    if (g == 0 || g == 1) {
-        double *src = (g == 0) ? gw.RSX : gw.RSY;
-        double *pp = (g == 0) ? gw.UC : gw.VC;
-        double *Q = nullptr;
-        bool ok = cholqr3(src, pp, GR, R, (g == 0) ? w.RX : w.RY, w.M, w.G, w.Ri, w.dX, smem, smem_dbl, red, &Q);
-        if (threadIdx.x == 0) s_ok = ok;
-        __syncthreads();
-        if (g == 1) {
-            for (int e = threadIdx.x; e < R * R; e += NT) __stcg(gw.RSY + e, w.RY[e]);
-        }
-        if (threadIdx.x == 0 && !s_ok) atomicExch(gw.ires + 3, 1);
-    }
-    gang_sync(gg);
-    // phase 2b: member 0 truncates the core M = R_X R_Y^T; cores published in RSX / RSY + R^2
-    if (g == 0) {
-        int c1 = 0, o1 = 0, r = 0;
-        if (__ldcg(gw.ires + 3) == 0) {
-            for (int e = threadIdx.x; e < R * R; e += NT) w.RY[e] = __ldcg(gw.RSY + e);
+    // phase 2a: QR of the stacked R_X's (member 0) and R_Y's (member 1); the stacked panel stays
+    // in the member's shared memory for phase 2c
+    PH_BEGIN(t2);
+    if (g <= 1) {
+        double *S = (g == 0) ? gw.RSX : gw.RSY;
+        double *tg = (g == 0) ? gw.tsx : gw.tsy;
+        if (stk_sm) {
+            ts = smem + GR * R;
+            for (int e = threadIdx.x; e < GR * R; e += NT) As[e] = __ldcg(S + e);
             __syncthreads();
-            r = compress_core(w, w.RX, R, w.RY, R, R, eps, tol_q, svd, kmax, rlim, w.UC, w.VC, R, R, &c1, &o1, red,
-                              redv, redi);
-            for (int e = threadIdx.x; e < R * r; e += NT) {
-                __stcg(gw.RSX + e, w.UC[e]);
-                __stcg(gw.RSY + (int64_t)R * R + e, w.VC[e]);
+            qr_house_sm(As, (int)GR, (int)GR, R, ts);
+            for (int e = threadIdx.x; e < R * R; e += NT) {   // R factor for the core
+                const int i = e % R, k = e / R;
+                __stcg(S + i + GR * k, As[i + GR * k]);
             }
         } else {
-            o1 = 1;
+            qr_house(S, GR, GR, R, tg, red);
+            for (int e = threadIdx.x; e < R * R; e += NT) {
+                const int i = e % R, k = e / R;
+                __stcg(S + i + GR * k, S[i + GR * k]);
+            }
         }
-        if (threadIdx.x == 0) { gw.ires[0] = r; gw.ires[1] = c1; gw.ires[2] = o1; gw.ires[3] = 0; }
+    }
+    PH_END(10, t2);
+    gang_sync(gg);
+    // phase 2b: core truncation (member 0) into UC / VC (GR x r, rows >= R zero)
+    if (g == 0) {
+        PH_BEGIN(t3);
+        for (int e = threadIdx.x; e < R * R; e += NT) {
+            const int i = e % R, k = e / R;
+            w.RX[e] = __ldcg(gw.RSX + i + GR * k);
+            w.RY[e] = __ldcg(gw.RSY + i + GR * k);
+        }
+        __syncthreads();
+        int c1 = 0, o1 = 0;
+        const int rr = compress_core(w, w.RX, R, w.RY, R, R, eps, tol_q, svd, kmax, rlim, gw.UC, gw.VC, GR, GR, &c1,
+                                     &o1, red, redv, redi);
+        if (threadIdx.x == 0) { gw.ires[0] = rr; gw.ires[1] = c1; gw.ires[2] = o1; }
+        PH_END(11, t3);
     }
     gang_sync(gg);
-    // phase 3 (all members): rows of U = Q_Xg [ (Q_sx)_g U_core ; 0 ], V likewise
     const int r = __ldcg(gw.ires);
-    *cb = __ldcg(gw.ires + 1);
-    *of = __ldcg(gw.ires + 2);
+    // phase 2c: apply the stacked Q's (member 0: U core, member 1: V core)
+    PH_BEGIN(t4);
+    if (g <= 1 && r > 0) {
+        double *S = (g == 0) ? gw.RSX : gw.RSY;
+        double *tg = (g == 0) ? gw.tsx : gw.tsy;
+        double *B = (g == 0) ? gw.UC : gw.VC;
+        if (stk_sm) apply_q_sm(As, (int)GR, (int)GR, R, smem + GR * R, B, GR, r);
+        else qr_apply_q(S, GR, GR, R, tg, B, GR, r);
+    }
+    PH_END(10, t4);
+    gang_sync(gg);
+    // phase 3 (all members): rows of U = Q_g [UC block g; 0], V likewise
+    PH_BEGIN(t5);
     for (int64_t e = threadIdx.x; e < mq * r; e += NT) {
         const int64_t i = e % mq;
         const int cc = (int)(e / mq);
-        double su = 0.0, sv = 0.0;
-        if (i < R) {
-            for (int l = 0; l < R; ++l) {
-                su += __ldcg(gw.UC + (int64_t)g * R + i + GR * l) * __ldcg(gw.RSX + l + (int64_t)R * cc);
-                sv += __ldcg(gw.VC + (int64_t)g * R + i + GR * l) * __ldcg(gw.RSY + (int64_t)R * R + l + (int64_t)R * cc);
-            }
-        }
-        U[q0 + i + ldo * cc] = su;
-        V[q0 + i + ldo * cc] = sv;
+        U[q0 + i + ldo * cc] = (i < R) ? __ldcg(gw.UC + (int64_t)g * R + i + GR * cc) : 0.0;
+        V[q0 + i + ldo * cc] = (i < R) ? __ldcg(gw.VC + (int64_t)g * R + i + GR * cc) : 0.0;
     }
+    *cb = __ldcg(gw.ires + 1);
+    *of = __ldcg(gw.ires + 2);
     __syncthreads();
-    qr_apply_q(w.X, mq, mq, R, w.tx, U + q0, ldo, r);
-    qr_apply_q(w.Y, mq, mq, R, w.ty, V + q0, ldo, r);
+    if (r > 0) {
+        if (loc_sm) {
+            ts = smem + mq * R;
+            for (int e = threadIdx.x; e < R; e += NT) ts[e] = w.tx[e];
+            panel_to_sm(As, w.X, mq, (int)mq, R);
+            apply_q_sm(As, (int)mq, (int)mq, R, ts, U + q0, ldo, r);
+            for (int e = threadIdx.x; e < R; e += NT) ts[e] = w.ty[e];
+            panel_to_sm(As, w.Y, mq, (int)mq, R);
+            apply_q_sm(As, (int)mq, (int)mq, R, ts, V + q0, ldo, r);
+        } else {
+            qr_apply_q(w.X, mq, mq, R, w.tx, U + q0, ldo, r);
+            qr_apply_q(w.Y, mq, mq, R, w.ty, V + q0, ldo, r);
+        }
+    }
+    PH_END(12, t5);
     gang_sync(gg);
     return r;
 }
@@ -669,11 +713,15 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         // small block: exact dense accumulation S = U V^T - sum of terms (m x m), fully pivoted
         // cross approximation of S to 0.1 eps |S|_max / m (so |S - X Y^T|_2 <= 0.1 eps |S|_2), then
         // QR + SVD truncation to (eps, kmax)
-        double *S = scr;
+        // S lives in shared memory when it leaves room for the GEMM staging (m <= 128)
+        const bool s_sm = m * m + 4096 <= c.smem_dbl;
+        double *S = s_sm ? smem : scr;
+        double *gs = s_sm ? smem + m * m : smem;
+        const int64_t gs_dbl = s_sm ? c.smem_dbl - m * m : c.smem_dbl;
         CompressWs wd = make_ws(scr + m * m, m, K, &X2, &Y2);   // X, Y panels (m x K) follow S
         PH_BEGIN(tg);
         for (int64_t e = threadIdx.x; e < m * m; e += NT) S[e] = 0.0;
-        if (r0 > 0) cta_gemm_nt(S, m, m, m, r0, U, m, V, 1, m, 1.0, smem, c.smem_dbl);   // S = U V^T
+        if (r0 > 0) cta_gemm_nt(S, m, m, m, r0, U, m, V, 1, m, 1.0, gs, gs_dbl);   // S = U V^T
         fl += 2.0 * m * m * r0;
         __syncthreads();
         double *T1 = wd.Y;   // scratch for A K (m x rb), before Y is used by the ACA
@@ -683,7 +731,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
                 const DNode na = c.nodes[c.tile_node[t.a]], nb = c.nodes[c.tile_node[t.b]];
                 const int64_t ar = (int64_t)na.i * HCOV_LEAF - R0, br = (int64_t)nb.i * HCOV_LEAF - C0;
                 const double *A = c.tiles + (int64_t)t.a * HCOV_TILE, *B = c.tiles + (int64_t)t.b * HCOV_TILE;
-                cta_gemm_nt(S + ar + m * br, m, 32, 32, 32, A, 32, B, 1, 32, -1.0, smem, c.smem_dbl);
+                cta_gemm_nt(S + ar + m * br, m, 32, 32, 32, A, 32, B, 1, 32, -1.0, gs, gs_dbl);
                 fl += 2.0 * 32 * 32 * 32;
             } else {
                 Fac A = get_fac(c, t.a), B = get_fac(c, t.b);
@@ -698,13 +746,13 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
                     // T1 = A K (nr x rb): T1(i, b) = sum_a A(i, a) K(a, b), K(a, b) = Kc[a + kcap b]
                     const double *Kc = c.cores + (int64_t)t.core * c.kcap * c.kcap;
                     for (int64_t e = threadIdx.x; e < nr * (int64_t)rb; e += NT) T1[e] = 0.0;
-                    cta_gemm_nt(T1, nr, nr, rb, ra, Ap, A.ld, Kc, c.kcap, 1, 1.0, smem, c.smem_dbl);
-                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, T1, nr, Bq, 1, B.ld, -1.0, smem,
-                                c.smem_dbl);
+                    cta_gemm_nt(T1, nr, nr, rb, ra, Ap, A.ld, Kc, c.kcap, 1, 1.0, gs, gs_dbl);
+                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, T1, nr, Bq, 1, B.ld, -1.0, gs,
+                                gs_dbl);
                     fl += 2.0 * nr * ra * rb;
                 } else {
-                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, Ap, A.ld, Bq, 1, B.ld, -1.0, smem,
-                                c.smem_dbl);
+                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, Ap, A.ld, Bq, 1, B.ld, -1.0, gs,
+                                gs_dbl);
                 }
                 fl += 2.0 * nr * nc * rb;
             }
@@ -1140,6 +1188,6 @@ __host__ __device__ inline int64_t engine_smem_doubles(int kcap)
     int64_t cc = 32 * (int64_t)kcap + HCOV_TILE + 32 * k + 32 * (int64_t)kcap + 8;
     int64_t m = a > b ? a : b;
     m = m > cc ? m : cc;
-    const int64_t floor_dbl = (NT >= 512) ? 16384 : 0;   // one CTA per SM: room for wider GEMM staging
+    const int64_t floor_dbl = (NT >= 512) ? HCOV_SMEM_DBL : 0;   // one CTA per SM: panels resident in shared memory
     return m > floor_dbl ? m : floor_dbl;
 }

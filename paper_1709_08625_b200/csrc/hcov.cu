@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(NT) k_test_truncate(double *scr, int64_t m, in
     CompressWs w = make_ws(scr, m, K, &X2, &Y2);
     int cb = 0, of = 0;
     const int r = compress(w, m, R, eps, final_tol(eps, R), true, kmax, rlim, U, V, m, &cb, &of, red, redv, redi,
-                           path == 1 ? smem : nullptr, smem_dbl);
+                           path >= 1 ? smem : nullptr, smem_dbl, path);
     if (threadIdx.x == 0) { rank[0] = r; rank[1] = cb; rank[2] = of; }
 }
 
@@ -1236,9 +1236,9 @@ hcov_status hcov_test_truncate(const double *X_dev, const double *Y_dev, int64_t
     CK(cudaMalloc(&rk, 3 * sizeof(int)));
     CK(cudaMemcpy(scr, X_dev, m * (int64_t)R * sizeof(double), cudaMemcpyDeviceToDevice));
     CK(cudaMemcpy(scr + m * K, Y_dev, m * (int64_t)R * sizeof(double), cudaMemcpyDeviceToDevice));
-    const int64_t smem = 16384 * sizeof(double);
+    const int64_t smem = HCOV_SMEM_DBL * sizeof(double);
     CK(cudaFuncSetAttribute(k_test_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_test_truncate<<<1, NT, smem, 0>>>(scr, m, R, K, eps, kmax, rlim, path, U_dev, V_dev, rk, 16384);
+    k_test_truncate<<<1, NT, smem, 0>>>(scr, m, R, K, eps, kmax, rlim, path, U_dev, V_dev, rk, HCOV_SMEM_DBL);
     cudaError_t e = cudaDeviceSynchronize();
     if (e == cudaSuccess) e = cudaMemcpy(out3_host, rk, 3 * sizeof(int), cudaMemcpyDeviceToHost);
     cudaFree(scr);

@@ -264,6 +264,199 @@ __device__ void qr_apply_q(const double *A, int64_t lda, int64_t m, int R, const
 }
 
 // ------------------------------------------------------------------------------------------
+// Shared-memory resident Householder QR (one CTA per SM: the engine has ~224 KB of dynamic
+// shared memory, enough for a 256 x 96 panel).  Column k is owned by warp k mod NWARP; step j
+// applies H_j to every column k > j, and the owner of column j + 1 updates that column first and
+// computes reflector j + 1 (look-ahead), so each step costs one CTA barrier.  Same reflector
+// convention as qr_house (v_j = [1; A[j+1:m, j]], tau_j, R in the upper triangle).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void house_col_warp(double *A, int lda, int m, int j, double *tau)
+{
+    const int lane = threadIdx.x & 31;
+    double *aj = A + (int64_t)lda * j;
+    double s = 0.0;
+    for (int i = j + 1 + lane; i < m; i += 32) s = fma(aj[i], aj[i], s);
+    s = warp_sum(s);
+    const double alpha = aj[j];
+    double t = 0.0, beta = alpha, scale = 0.0;
+    if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        t = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+        for (int i = j + 1 + lane; i < m; i += 32) aj[i] *= scale;
+    }
+    __syncwarp();
+    if (lane == 0) { aj[j] = beta; tau[j] = t; }
+    __syncwarp();
+}
+
+// Apply H = I - t v v^T (v = [1; v[j+1:m]]) to nk <= 4 columns c0, c0 + cs, ... of B (one warp).
+__device__ __forceinline__ void house_apply4(const double *v, int j, int m, double t, double *B, int ldb, int c0,
+                                             int cs, int nk)
+{
+    const int lane = threadIdx.x & 31;
+    double *b0 = B + (int64_t)ldb * c0;
+    double *b1 = (nk > 1) ? b0 + (int64_t)ldb * cs : b0;
+    double *b2 = (nk > 2) ? b0 + (int64_t)ldb * 2 * cs : b0;
+    double *b3 = (nk > 3) ? b0 + (int64_t)ldb * 3 * cs : b0;
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+    for (int i = j + 1 + lane; i < m; i += 32) {
+        const double x = v[i];
+        w0 = fma(x, b0[i], w0);
+        w1 = fma(x, b1[i], w1);
+        w2 = fma(x, b2[i], w2);
+        w3 = fma(x, b3[i], w3);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        w0 += __shfl_xor_sync(0xffffffffu, w0, o);
+        w1 += __shfl_xor_sync(0xffffffffu, w1, o);
+        w2 += __shfl_xor_sync(0xffffffffu, w2, o);
+        w3 += __shfl_xor_sync(0xffffffffu, w3, o);
+    }
+    w0 = t * (w0 + b0[j]);
+    w1 = t * (w1 + b1[j]);
+    w2 = t * (w2 + b2[j]);
+    w3 = t * (w3 + b3[j]);
+    __syncwarp();
+    if (lane == 0) {
+        b0[j] -= w0;
+        if (nk > 1) b1[j] -= w1;
+        if (nk > 2) b2[j] -= w2;
+        if (nk > 3) b3[j] -= w3;
+    }
+    for (int i = j + 1 + lane; i < m; i += 32) {
+        const double x = v[i];
+        b0[i] -= x * w0;
+        if (nk > 1) b1[i] -= x * w1;
+        if (nk > 2) b2[i] -= x * w2;
+        if (nk > 3) b3[i] -= x * w3;
+    }
+    __syncwarp();
+}
+
+// QR of A (m x R, ld lda, shared memory, R <= m) in place; tau: R doubles (shared memory).
+__device__ void qr_house_sm(double *A, int lda, int m, int R, double *tau)
+{
+    const int warp = threadIdx.x >> 5;
+    if (R <= 0) return;
+    if (warp == 0) house_col_warp(A, lda, m, 0, tau);
+    __syncthreads();
+    for (int j = 0; j < R; ++j) {
+        const double t = tau[j];
+        const double *v = A + (int64_t)lda * j;
+        const int la = j + 1;
+        if (la < R && warp == la % NWARP) {
+            if (t != 0.0) house_apply4(v, j, m, t, A, lda, la, NWARP, 1);
+            house_col_warp(A, lda, m, la, tau);
+        }
+        if (t != 0.0) {
+            // this warp's columns k > la (k = warp mod NWARP), four at a time
+            int k0 = warp;
+            if (k0 <= la) k0 += NWARP * ((la - warp) / NWARP + 1);
+            for (int k = k0; k < R; k += 4 * NWARP) {
+                const int nk = min(4, (R - 1 - k) / NWARP + 1);
+                house_apply4(v, j, m, t, A, lda, k, NWARP, nk);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// B <- Q B, Q = H_0 ... H_{R-1} from qr_house(_sm) (reflectors in shared memory, ld lda, m rows),
+// B: m x r (global or shared, ld ldb).  Each warp carries NC columns of B in registers (rows
+// lane + 32 q, q < QM, m <= 32 QM) through all R reflectors: no CTA barriers.
+template <int QM, int NC>
+__device__ void apply_q_reg(const double *A, int lda, int m, int R, const double *tau, double *B, int64_t ldb,
+                            int r)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int c0 = NC * warp; c0 < r; c0 += NC * NWARP) {
+        double b[NC][QM];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int q = 0; q < QM; ++q) {
+                const int i = lane + 32 * q;
+                b[c][q] = (c0 + c < r && i < m) ? __ldcg(B + i + ldb * (c0 + c)) : 0.0;
+            }
+        for (int j = R - 1; j >= 0; --j) {
+            const double t = tau[j];
+            if (t == 0.0) continue;
+            const double *v = A + (int64_t)lda * j;
+            double cf[QM];
+#pragma unroll
+            for (int q = 0; q < QM; ++q) {
+                const int i = lane + 32 * q;
+                cf[q] = (i > j && i < m) ? v[i] : (i == j ? 1.0 : 0.0);
+            }
+            double w[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                double s = 0.0;
+#pragma unroll
+                for (int q = 0; q < QM; ++q) s = fma(cf[q], b[c][q], s);
+                w[c] = s;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const double tw = t * w[c];
+#pragma unroll
+                for (int q = 0; q < QM; ++q) b[c][q] = fma(-cf[q], tw, b[c][q]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int q = 0; q < QM; ++q) {
+                const int i = lane + 32 * q;
+                if (c0 + c < r && i < m) B[i + ldb * (c0 + c)] = b[c][q];
+            }
+    }
+    __syncthreads();
+}
+
+// Dispatch of apply_q_reg by panel height (m <= 1024); returns false if m is too large.
+__device__ bool apply_q_sm(const double *A, int lda, int m, int R, const double *tau, double *B, int64_t ldb, int r)
+{
+    if (m <= 256) {
+        if (r <= NWARP) apply_q_reg<8, 1>(A, lda, m, R, tau, B, ldb, r);
+        else if (r <= 2 * NWARP) apply_q_reg<8, 2>(A, lda, m, R, tau, B, ldb, r);
+        else apply_q_reg<8, 4>(A, lda, m, R, tau, B, ldb, r);
+    } else if (m <= 512) {
+        if (r <= NWARP) apply_q_reg<16, 1>(A, lda, m, R, tau, B, ldb, r);
+        else apply_q_reg<16, 2>(A, lda, m, R, tau, B, ldb, r);
+    } else if (m <= 1024) {
+        apply_q_reg<32, 1>(A, lda, m, R, tau, B, ldb, r);
+    } else {
+        return false;
+    }
+    return true;
+}
+
+// Copy a panel (m x R) between global (ld ldg) and shared (ld m) memory.
+__device__ __forceinline__ void panel_to_sm(double *S, const double *Gp, int64_t ldg, int m, int R)
+{
+    for (int e = threadIdx.x; e < m * R; e += NT) {
+        const int i = e % m, c = e / m;
+        S[e] = Gp[i + ldg * c];
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void panel_from_sm(double *Gp, int64_t ldg, const double *S, int m, int R)
+{
+    for (int e = threadIdx.x; e < m * R; e += NT) {
+        const int i = e % m, c = e / m;
+        Gp[i + ldg * c] = S[e];
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------
 // One-sided Jacobi SVD of G (K x nc, ld K, global scratch): on return G <- G J (columns mutually
 // orthogonal, ||col_i|| = sigma_i) and J (nc x nc, ld nc) orthogonal, so G_in = (G J) J^T.
 // Round-robin parallel ordering (nc/2 disjoint pairs per round, one warp per pair).
@@ -676,10 +869,40 @@ __device__ int compress_core(const CompressWs &w, const double *RX, int64_t ldx,
 // alias X, Y.  Returns r.
 __device__ int compress(const CompressWs &w, int64_t m, int R, double eps, double tol_q, bool svd, int kmax,
                         int rlim, double *U, double *V, int64_t ldo, int *cap_bound, int *overflow, double *red,
-                        double *redv, int64_t *redi, double *smem = nullptr, int64_t smem_dbl = 0)
+                        double *redv, int64_t *redi, double *smem = nullptr, int64_t smem_dbl = 0,
+                        int qr_path = 2)
 {
     if (R == 0) { if (threadIdx.x == 0) { *cap_bound = 0; *overflow = 0; } __syncthreads(); return 0; }
-    if (smem && m >= 2 * R) {
+    if (smem && qr_path == 2 && m <= 1024 && m * (int64_t)R + R <= smem_dbl) {
+        // shared-memory path: Householder QR of X and Y in shared memory (reflectors written back),
+        // core, then Q_X / Q_Y applied to [U_core; 0] / [V_core; 0] held in registers
+        const int mi = (int)m;
+        double *As = smem, *ts = smem + m * (int64_t)R;
+        PH_BEGIN(tc);
+        panel_to_sm(As, w.X, m, mi, R);
+        qr_house_sm(As, mi, mi, R, ts);
+        for (int e = threadIdx.x; e < R; e += NT) w.tx[e] = ts[e];
+        panel_from_sm(w.X, m, As, mi, R);
+        panel_to_sm(As, w.Y, m, mi, R);
+        qr_house_sm(As, mi, mi, R, ts);
+        for (int e = threadIdx.x; e < R; e += NT) w.ty[e] = ts[e];
+        panel_from_sm(w.Y, m, As, mi, R);
+        PH_END(0, tc);
+        const int r = compress_core(w, w.X, m, w.Y, m, R, eps, tol_q, svd, kmax, rlim, U, V, ldo, m, cap_bound,
+                                    overflow, red, redv, redi);
+        PH_BEGIN(t4);
+        if (r > 0) {
+            for (int e = threadIdx.x; e < R; e += NT) ts[e] = w.tx[e];
+            panel_to_sm(As, w.X, m, mi, R);
+            apply_q_sm(As, mi, mi, R, ts, U, ldo, r);
+            for (int e = threadIdx.x; e < R; e += NT) ts[e] = w.ty[e];
+            panel_to_sm(As, w.Y, m, mi, R);
+            apply_q_sm(As, mi, mi, R, ts, V, ldo, r);
+        }
+        PH_END(4, t4);
+        return r;
+    }
+    if (smem && qr_path != 0 && m >= 2 * R) {
         // BLAS-3 path: shifted CholeskyQR3 of X and Y, core, U = Q_X U_core, V = Q_Y V_core
         PH_BEGIN(tc);
         double *QX = nullptr, *QY = nullptr;

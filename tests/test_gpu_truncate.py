@@ -1,5 +1,6 @@
 """GPU unit tests of the truncation step (A6) against numpy's SVD:
-||X Y^T - U V^T||_2 <= 10 eps ||X Y^T||_2 (SURVEY Sec. 8(c) pin; SPEC acceptance), both QR paths."""
+||X Y^T - U V^T||_2 <= 10 eps ||X Y^T||_2 (SURVEY Sec. 8(c) pin; SPEC acceptance), all QR paths
+(0 global Householder, 1 shifted CholeskyQR3, 2 shared-memory Householder)."""
 import numpy as np
 import pytest
 
@@ -29,6 +30,19 @@ def _panel(m, R, seed, kind):
 @pytest.mark.parametrize("kind", ["decay", "dependent", "scaled"])
 @pytest.mark.parametrize("m,R,eps", [(512, 60, 1e-6), (256, 80, 1e-8), (1024, 92, 1e-5)])
 def test_truncation_error_bound(path, kind, m, R, eps):
+    _check(path, kind, m, R, eps)
+
+
+# shared-memory Householder path (panel m x R resident in the engine's 224 KB): sizes across the
+# register-apply variants (m <= 256, m <= 512), ragged m, R = m
+@pytest.mark.parametrize("kind", ["decay", "dependent", "scaled"])
+@pytest.mark.parametrize("m,R,eps", [(256, 80, 1e-8), (200, 92, 1e-6), (300, 90, 1e-5), (64, 40, 1e-6),
+                                     (100, 100, 1e-7), (33, 7, 1e-6)])
+def test_truncation_smem_path(kind, m, R, eps):
+    _check(2, kind, m, R, eps)
+
+
+def _check(path, kind, m, R, eps):
     X, Y = _panel(m, R, 7 + m + R, kind)
     S = X @ Y.T
     U, V, r, cb, of = H.test_truncate(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda(), eps, rlim=R, path=path)

@@ -107,6 +107,15 @@ def show(path):
     def msize(t):
         return int(rm[tasks[t, 2]]) if rm is not None and ty[t] in (1, 5) else 0
     print("  longest on chain (type, m, ms):", [(NAMES[ty[t]], msize(t), round(dur[t] / 1e6, 3)) for t in cc])
+    comp = {}
+    for t in chain:
+        if ty[t] == 11:
+            continue
+        key = f"{NAMES[ty[t]]}{msize(t) or ''}" + ("f" if ty[t] == 5 and tasks[t, 4] == 1 else "")
+        cnt, tot = comp.get(key, (0, 0))
+        comp[key] = (cnt + 1, tot + dur[t])
+    print("  chain composition (type+m[f=final chunk]: count, total ms):",
+          {k: (v[0], round(v[1] / 1e6, 1)) for k, v in sorted(comp.items(), key=lambda x: -x[1][1])})
     if rm is not None:
         for k in (1, 5):
             m = (ty == k) & ran
