@@ -390,11 +390,11 @@ __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, in
     if (loc_sm) {
         ts = smem + mq * R;
         panel_to_sm(As, w.X, mq, (int)mq, R);
-        qr_house_sm(As, (int)mq, (int)mq, R, ts);
+        qr_sm(As, (int)mq, (int)mq, R, ts);
         for (int e = threadIdx.x; e < R; e += NT) w.tx[e] = ts[e];
         panel_from_sm(w.X, mq, As, (int)mq, R);
         panel_to_sm(As, w.Y, mq, (int)mq, R);
-        qr_house_sm(As, (int)mq, (int)mq, R, ts);
+        qr_sm(As, (int)mq, (int)mq, R, ts);
         for (int e = threadIdx.x; e < R; e += NT) w.ty[e] = ts[e];
         panel_from_sm(w.Y, mq, As, (int)mq, R);
     } else {
@@ -418,10 +418,15 @@ __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, in
             ts = smem + GR * R;
             for (int e = threadIdx.x; e < GR * R; e += NT) As[e] = __ldcg(S + e);
             __syncthreads();
-            qr_house_sm(As, (int)GR, (int)GR, R, ts);
-            for (int e = threadIdx.x; e < R * R; e += NT) {   // R factor for the core
-                const int i = e % R, k = e / R;
-                __stcg(S + i + GR * k, As[i + GR * k]);
+            qr_sm(As, (int)GR, (int)GR, R, ts);
+            if (g == 0) {   // member 0 needs its shared memory for the core: whole panel back
+                for (int e = threadIdx.x; e < R; e += NT) tg[e] = ts[e];
+                for (int e = threadIdx.x; e < GR * R; e += NT) __stcg(S + e, As[e]);
+            } else {        // R factor for the core
+                for (int e = threadIdx.x; e < R * R; e += NT) {
+                    const int i = e % R, k = e / R;
+                    __stcg(S + i + GR * k, As[i + GR * k]);
+                }
             }
         } else {
             qr_house(S, GR, GR, R, tg, red);
@@ -443,8 +448,8 @@ __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, in
         }
         __syncthreads();
         int c1 = 0, o1 = 0;
-        const int rr = compress_core(w, w.RX, R, w.RY, R, R, eps, tol_q, svd, kmax, rlim, gw.UC, gw.VC, GR, GR, &c1,
-                                     &o1, red, redv, redi);
+        const int rr = compress_core(core_ws_sm(w, smem, smem_dbl, R), w.RX, R, w.RY, R, R, eps, tol_q, svd, kmax,
+                                     rlim, gw.UC, gw.VC, GR, GR, &c1, &o1, red, redv, redi);
         if (threadIdx.x == 0) { gw.ires[0] = rr; gw.ires[1] = c1; gw.ires[2] = o1; }
         PH_END(11, t3);
     }
@@ -456,7 +461,14 @@ __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, in
         double *S = (g == 0) ? gw.RSX : gw.RSY;
         double *tg = (g == 0) ? gw.tsx : gw.tsy;
         double *B = (g == 0) ? gw.UC : gw.VC;
-        if (stk_sm) apply_q_sm(As, (int)GR, (int)GR, R, smem + GR * R, B, GR, r);
+        if (stk_sm) {
+            if (g == 0) {
+                for (int e = threadIdx.x; e < R; e += NT) smem[GR * R + e] = tg[e];
+                for (int e = threadIdx.x; e < GR * R; e += NT) As[e] = __ldcg(S + e);
+                __syncthreads();
+            }
+            apply_q_sm(As, (int)GR, (int)GR, R, smem + GR * R, B, GR, r);
+        }
         else qr_apply_q(S, GR, GR, R, tg, B, GR, r);
     }
     PH_END(10, t4);

@@ -363,6 +363,186 @@ __device__ void qr_house_sm(double *A, int lda, int m, int R, double *tau)
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Blocked variant for panels of m <= 32 QM rows (shared memory, ld lda): panels of 4 columns are
+// factored by warp 0 in registers (no CTA barrier inside a panel); the other warps apply the 4
+// reflectors to the trailing columns two at a time in registers (one shared-memory read and
+// write of the trailing matrix per panel instead of per reflector); warp 0 updates and factors
+// the next panel while they do (look-ahead), so each panel costs one CTA barrier.
+// ------------------------------------------------------------------------------------------
+template <int QM>
+__device__ __forceinline__ void hh_coef(const double *A, int lda, int m, int j, double (&cf)[QM])
+{
+    const int lane = threadIdx.x & 31;
+    const double *v = A + (int64_t)lda * j;
+#pragma unroll
+    for (int q = 0; q < QM; ++q) {
+        const int i = lane + 32 * q;
+        cf[q] = (i > j && i < m) ? v[i] : (i == j ? 1.0 : 0.0);
+    }
+}
+
+// Apply H_j (coefficients cf, tau t) to NC register columns b.
+template <int QM, int NC>
+__device__ __forceinline__ void hh_apply_reg(const double (&cf)[QM], double t, double (&b)[NC][QM])
+{
+    double w[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < QM; ++q) s = fma(cf[q], b[c][q], s);
+        w[c] = s;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const double tw = t * w[c];
+#pragma unroll
+        for (int q = 0; q < QM; ++q) b[c][q] = fma(-cf[q], tw, b[c][q]);
+    }
+}
+
+// Warp-level factorization of the panel columns j0 .. j0+nb-1 (nb <= 4; already updated by all
+// earlier reflectors): reflectors and R written to A, tau[j0 ..].
+template <int QM>
+__device__ __forceinline__ void hh_panel(double *A, int lda, int m, int j0, int nb, double *tau)
+{
+    const int lane = threadIdx.x & 31;
+    double p[4][QM];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+            const int i = lane + 32 * q;
+            p[c][q] = (c < nb && i < m) ? A[i + (int64_t)lda * (j0 + c)] : 0.0;
+        }
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+        if (jj >= nb) break;
+        const int j = j0 + jj;
+        double s = 0.0, av = 0.0;
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+            const int i = lane + 32 * q;
+            if (i > j && i < m) s = fma(p[jj][q], p[jj][q], s);
+            if (q == (j >> 5)) av = p[jj][q];
+        }
+        s = warp_sum(s);
+        const double alpha = __shfl_sync(0xffffffffu, av, j & 31);
+        double t = 0.0, beta = alpha, scale = 1.0;
+        if (s > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + s), alpha);
+            t = (beta - alpha) / beta;
+            scale = 1.0 / (alpha - beta);
+        }
+        double cf[QM];
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+            const int i = lane + 32 * q;
+            if (i > j && i < m) p[jj][q] *= scale;
+            if (i == j) p[jj][q] = beta;
+            cf[q] = (i > j && i < m) ? p[jj][q] : (i == j ? 1.0 : 0.0);
+            if (i < m) A[i + (int64_t)lda * j] = p[jj][q];
+        }
+        if (lane == 0) tau[j] = t;
+        if (t != 0.0) {
+            // remaining panel columns jj+1 .. nb-1
+            double w[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                double sw = 0.0;
+                if (c > jj) {
+#pragma unroll
+                    for (int q = 0; q < QM; ++q) sw = fma(cf[q], p[c][q], sw);
+                }
+                w[c] = sw;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c > jj) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (c > jj) {
+                    const double tw = t * w[c];
+#pragma unroll
+                    for (int q = 0; q < QM; ++q) p[c][q] = fma(-cf[q], tw, p[c][q]);
+                }
+        }
+    }
+    __syncwarp();
+}
+
+// Columns k0 .. k1-1 (taken in pairs by the warps w0, w0 + ws, ...): apply H_j0 .. H_{j0+nb-1}.
+template <int QM>
+__device__ __forceinline__ void hh_trail(double *A, int lda, int m, int j0, int nb, const double *tau, int k0,
+                                         int k1, int w0, int ws)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp < w0) return;
+    for (int k = k0 + 2 * (warp - w0); k < k1; k += 2 * ws) {
+        const bool two = k + 1 < k1;
+        double b[2][QM];
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+            const int i = lane + 32 * q;
+            b[0][q] = (i < m) ? A[i + (int64_t)lda * k] : 0.0;
+            b[1][q] = (two && i < m) ? A[i + (int64_t)lda * (k + 1)] : 0.0;
+        }
+        for (int jj = 0; jj < nb; ++jj) {
+            const double t = tau[j0 + jj];
+            if (t == 0.0) continue;
+            double cf[QM];
+            hh_coef<QM>(A, lda, m, j0 + jj, cf);
+            hh_apply_reg<QM, 2>(cf, t, b);
+        }
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+            const int i = lane + 32 * q;
+            if (i < m) {
+                A[i + (int64_t)lda * k] = b[0][q];
+                if (two) A[i + (int64_t)lda * (k + 1)] = b[1][q];
+            }
+        }
+    }
+}
+
+template <int QM>
+__device__ void qr_house_blk(double *A, int lda, int m, int R, double *tau)
+{
+    constexpr int NB = 4;
+    const int warp = threadIdx.x >> 5;
+    if (R <= 0) return;
+    if (warp == 0) hh_panel<QM>(A, lda, m, 0, min(NB, R), tau);
+    __syncthreads();
+    for (int j0 = 0; j0 < R; j0 += NB) {
+        const int nb = min(NB, R - j0);
+        const int n0 = j0 + nb;
+        const int nn = min(NB, R - n0);
+        if (nn > 0) {
+            if (warp == 0) {   // look-ahead: next panel updated and factored by warp 0
+                hh_trail<QM>(A, lda, m, j0, nb, tau, n0, n0 + nn, 0, 1);
+                __syncwarp();
+                hh_panel<QM>(A, lda, m, n0, nn, tau);
+            }
+            hh_trail<QM>(A, lda, m, j0, nb, tau, n0 + nn, R, 1, NWARP - 1);
+        }
+        __syncthreads();
+    }
+}
+
+// Householder QR in shared memory: blocked register variant for m <= 256, else qr_house_sm.
+__device__ __forceinline__ void qr_sm(double *A, int lda, int m, int R, double *tau)
+{
+    if (m <= 256) qr_house_blk<8>(A, lda, m, R, tau);
+    else qr_house_sm(A, lda, m, R, tau);
+}
+
 // B <- Q B, Q = H_0 ... H_{R-1} from qr_house(_sm) (reflectors in shared memory, ld lda, m rows),
 // B: m x r (global or shared, ld ldb).  Each warp carries NC columns of B in registers (rows
 // lane + 32 q, q < QM, m <= 32 QM) through all R reflectors: no CTA barriers.
@@ -425,8 +605,7 @@ __device__ bool apply_q_sm(const double *A, int lda, int m, int R, const double 
 {
     if (m <= 256) {
         if (r <= NWARP) apply_q_reg<8, 1>(A, lda, m, R, tau, B, ldb, r);
-        else if (r <= 2 * NWARP) apply_q_reg<8, 2>(A, lda, m, R, tau, B, ldb, r);
-        else apply_q_reg<8, 4>(A, lda, m, R, tau, B, ldb, r);
+        else apply_q_reg<8, 2>(A, lda, m, R, tau, B, ldb, r);
     } else if (m <= 512) {
         if (r <= NWARP) apply_q_reg<16, 1>(A, lda, m, R, tau, B, ldb, r);
         else apply_q_reg<16, 2>(A, lda, m, R, tau, B, ldb, r);
@@ -767,6 +946,23 @@ struct CompressWs {
     double *tail;       // first free (8-byte aligned) double after the workspace
 };
 
+// The core's K x K work arrays (M, G, J and vectors) in shared memory when they fit (R x R each).
+__device__ __forceinline__ CompressWs core_ws_sm(const CompressWs &w, double *sm, int64_t dbl, int R)
+{
+    const int64_t RR = (int64_t)R * R;
+    if (!sm || 3 * RR + 6 * (int64_t)R + 8 > dbl) return w;
+    CompressWs c = w;
+    c.M = sm;
+    c.G = c.M + RR;
+    c.J = c.G + RR;
+    c.tm = c.J + RR;
+    c.sig = c.tm + R;
+    c.cn = c.sig + R;
+    c.ord = (int *)(c.cn + R);
+    c.piv = (int *)(c.cn + 2 * R);
+    return c;
+}
+
 // Core of the truncation (A6).  Input: upper-triangular R_X, R_Y (R x R, the
 // top R rows of RX / RY with leading dimensions ldx / ldy).
 //   M = R_X R_Y^T (R x R);  M Pi = Q_M R_M by pivoted QR stopped at tol_q (rank-revealing
@@ -880,16 +1076,16 @@ __device__ int compress(const CompressWs &w, int64_t m, int R, double eps, doubl
         double *As = smem, *ts = smem + m * (int64_t)R;
         PH_BEGIN(tc);
         panel_to_sm(As, w.X, m, mi, R);
-        qr_house_sm(As, mi, mi, R, ts);
+        qr_sm(As, mi, mi, R, ts);
         for (int e = threadIdx.x; e < R; e += NT) w.tx[e] = ts[e];
         panel_from_sm(w.X, m, As, mi, R);
         panel_to_sm(As, w.Y, m, mi, R);
-        qr_house_sm(As, mi, mi, R, ts);
+        qr_sm(As, mi, mi, R, ts);
         for (int e = threadIdx.x; e < R; e += NT) w.ty[e] = ts[e];
         panel_from_sm(w.Y, m, As, mi, R);
         PH_END(0, tc);
-        const int r = compress_core(w, w.X, m, w.Y, m, R, eps, tol_q, svd, kmax, rlim, U, V, ldo, m, cap_bound,
-                                    overflow, red, redv, redi);
+        const int r = compress_core(core_ws_sm(w, smem, smem_dbl, R), w.X, m, w.Y, m, R, eps, tol_q, svd, kmax, rlim,
+                                    U, V, ldo, m, cap_bound, overflow, red, redv, redi);
         PH_BEGIN(t4);
         if (r > 0) {
             for (int e = threadIdx.x; e < R; e += NT) ts[e] = w.tx[e];
