@@ -245,12 +245,26 @@ __host__ __device__ inline int aca_kmax(int64_t m, int kcap)
     return (int)(k < m ? k : m);
 }
 __host__ __device__ inline int kbuf_of(int kcap) { return 3 * kcap + 32; }
-__host__ __device__ inline int64_t task_scratch(int64_t m, int kcap, int npanels = 6)
+// In-CTA TSQR of a member's rows (> 256): chunks of <= 256 rows, per side nc x K taus and nc
+// node slots of (2 K x K panel + K taus).
+__host__ __device__ inline int ts_nchunks(int64_t mq) { return (int)((mq + 255) / 256); }
+__host__ __device__ inline int64_t ts_slot(int K) { return 2 * (int64_t)K * K + K; }
+__host__ __device__ inline int64_t ts_region_doubles(int64_t mq, int K)
+{
+    if (mq <= 256) return 0;
+    return 2 * (int64_t)ts_nchunks(mq) * (K + ts_slot(K));
+}
+__host__ __device__ inline int64_t task_scratch_base(int64_t m, int kcap, int npanels)
 {
     int64_t K = kbuf_of(kcap);
     int64_t panels = npanels * m * K;
     if (m <= HCOV_DENSE_MAX) panels = m * m + npanels * m * K;
     return panels + 8 * K * K + 10 * K + m / 8 + 64;
+}
+__host__ __device__ inline int64_t task_scratch(int64_t m, int kcap, int npanels = 6)
+{
+    const int64_t b = task_scratch_base(m, kcap, npanels);
+    return npanels == 4 ? b + ts_region_doubles(m, kbuf_of(kcap)) : b;
 }
 
 
@@ -281,6 +295,8 @@ __device__ __forceinline__ CompressWs make_ws(double *base, int64_t m, int K, do
     w.ord = (int *)(w.dY + K);
     w.piv = (int *)(w.dY + 2 * K);
     w.tail = w.dY + 3 * K;
+    w.tsr = nullptr;
+    w.K = K;
     return w;
 }
 
@@ -319,6 +335,13 @@ struct Gang {
     int64_t mq, q0;
     double *shared;
 };
+// Rows of a gang member: m / G each, the last member also takes the remainder.
+__device__ __forceinline__ void gang_rows(Gang &gg, int64_t m)
+{
+    const int64_t base = m / gg.G;
+    gg.q0 = (int64_t)gg.g * base;
+    gg.mq = (gg.g == gg.G - 1) ? m - (int64_t)(gg.G - 1) * base : base;
+}
 __device__ __forceinline__ void gang_sync(Gang &gg)
 {
     PH_BEGIN(tw);
@@ -336,30 +359,33 @@ __device__ __forceinline__ void gang_sync(Gang &gg)
 }
 
 struct GangWs {
-    double *RSX, *RSY;     // (G K) x K each, ld G*R
-    double *UC, *VC;       // (G K) x K each, ld G*R
-    double *tsx, *tsy;     // K each
+    // per side (X, Y): G blocks of R x R (ld R: the current R factors of the TSQR tree), G node
+    // slots of (2K x K panel + K taus) (tree node (g, s) in slot g + s), G blocks of R x r (ld R:
+    // the cores pushed down the tree)
+    double *BX, *BY, *NX, *NY, *CX, *CY;
     double *pv;            // 2 x G partial values
     int64_t *pi;           // 2 x G partial indices
     double *ps;            // 2 x G x 2 partial sums
     double *urow, *vrow;   // K each: published pivot row of U / pivot column of V (ACA)
-    int32_t *ires;         // [0] r, [1] cb, [2] of, [3] CholeskyQR breakdown flag
+    int32_t *ires;         // [0] r, [1] cb, [2] of
+    int64_t nslot;         // doubles per node slot
 };
 __host__ __device__ inline int64_t gang_shared_doubles(int K, int G)
 {
-    return 4 * (int64_t)G * K * K + 4 * (int64_t)K + 8 * (int64_t)G + 64;
+    return 2 * (int64_t)G * (2 * (int64_t)K * K + (2 * (int64_t)K * K + K)) + 2 * (int64_t)K + 8 * (int64_t)G + 64;
 }
 __device__ __forceinline__ GangWs make_gws(double *base, int K, int G)
 {
     GangWs gw;
-    const int64_t GK = (int64_t)G * K;
-    gw.RSX = base;
-    gw.RSY = gw.RSX + GK * K;
-    gw.UC = gw.RSY + GK * K;
-    gw.VC = gw.UC + GK * K;
-    gw.tsx = gw.VC + GK * K;
-    gw.tsy = gw.tsx + K;
-    gw.urow = gw.tsy + K;
+    const int64_t GK2 = (int64_t)G * K * K;
+    gw.nslot = 2 * (int64_t)K * K + K;
+    gw.BX = base;
+    gw.BY = gw.BX + GK2;
+    gw.CX = gw.BY + GK2;
+    gw.CY = gw.CX + GK2;
+    gw.NX = gw.CY + GK2;
+    gw.NY = gw.NX + G * gw.nslot;
+    gw.urow = gw.NY + G * gw.nslot;
     gw.vrow = gw.urow + K;
     gw.pv = gw.vrow + K;
     gw.pi = (int64_t *)(gw.pv + 2 * G);
@@ -368,12 +394,193 @@ __device__ __forceinline__ GangWs make_gws(double *base, int K, int G)
     return gw;
 }
 
+// Local Householder QR of a member's panel (mq x R, ld mq): in shared memory when mq <= 256,
+// else an in-CTA TSQR over nc chunks of <= 256 rows (chunk QRs in shared memory, then a binary
+// tree of 2R x R node QRs; region: nc x K taus, then nc node slots (node (b, s) in slot b + s)).
+// The R factor of the whole panel ends in the upper triangle of rows 0..R-1.
+__device__ __forceinline__ int64_t ts_c0(int64_t mq, int nc, int c) { return (mq * c) / nc; }
+
+// 0: global Householder, 1: one shared-memory panel, 2: in-CTA TSQR over chunks
+__device__ __forceinline__ int local_mode(int64_t mq, int R, const double *reg, int64_t smem_dbl)
+{
+    if (mq <= 256) return (R <= mq && mq * R + R <= smem_dbl) ? 1 : 0;
+    const int nc = ts_nchunks(mq);
+    if (reg && 256 * (int64_t)R + R <= smem_dbl && 2 * (int64_t)R * R + R <= smem_dbl && mq / nc >= R) return 2;
+    return 0;
+}
+
+__device__ void local_qr(double *P, int64_t mq, int R, double *tau, double *reg, int K, double *smem,
+                         int64_t smem_dbl, double *red)
+{
+    const int mode = local_mode(mq, R, reg, smem_dbl);
+    if (mode == 0) {
+        qr_house(P, mq, mq, R, tau, red);
+        return;
+    }
+    if (mode == 1) {
+        double *ts = smem + mq * R;
+        panel_to_sm(smem, P, mq, (int)mq, R);
+        qr_sm(smem, (int)mq, (int)mq, R, ts);
+        for (int e = threadIdx.x; e < R; e += NT) tau[e] = ts[e];
+        panel_from_sm(P, mq, smem, (int)mq, R);
+        return;
+    }
+    const int nc = ts_nchunks(mq);
+    const int64_t nslot = ts_slot(K);
+    double *taus = reg, *nodes = reg + (int64_t)nc * K;
+    for (int cix = 0; cix < nc; ++cix) {
+        const int64_t r0 = ts_c0(mq, nc, cix);
+        const int rows = (int)(ts_c0(mq, nc, cix + 1) - r0);
+        double *ts = smem + (int64_t)rows * R;
+        panel_to_sm(smem, P + r0, mq, rows, R);
+        qr_sm(smem, rows, rows, R, ts);
+        for (int e = threadIdx.x; e < R; e += NT) taus[(int64_t)cix * K + e] = ts[e];
+        panel_from_sm(P + r0, mq, smem, rows, R);
+    }
+    const int R2 = 2 * R;
+    for (int s = 1; s < nc; s *= 2)
+        for (int b = 0; b + s < nc; b += 2 * s) {
+            double *Pb = P + ts_c0(mq, nc, b), *Pc = P + ts_c0(mq, nc, b + s);
+            double *slot = nodes + (int64_t)(b + s) * nslot;
+            double *ts = smem + (int64_t)R2 * R;
+            for (int e = threadIdx.x; e < R2 * R; e += NT) {
+                const int i = e % R2, k = e / R2;
+                const int ii = i < R ? i : i - R;
+                smem[e] = (k >= ii) ? (i < R ? Pb : Pc)[ii + mq * k] : 0.0;
+            }
+            __syncthreads();
+            qr_sm(smem, R2, R2, R, ts);
+            for (int e = threadIdx.x; e < R2 * R; e += NT) slot[e] = smem[e];
+            for (int e = threadIdx.x; e < R; e += NT) slot[2 * (int64_t)R * R + e] = ts[e];
+            for (int e = threadIdx.x; e < R * R; e += NT) {
+                const int i = e % R, k = e / R;
+                if (k >= i) Pb[i + mq * k] = smem[i + (int64_t)R2 * k];
+            }
+            __syncthreads();
+        }
+}
+
+// B <- Q B for the local QR above (B: mq x r, ld ldb; only rows 0..R-1 nonzero on entry).
+__device__ void local_apply(const double *P, int64_t mq, int R, const double *tau, const double *reg, int K,
+                            double *B, int64_t ldb, int r, double *tmp, double *smem, int64_t smem_dbl)
+{
+    const int mode = local_mode(mq, R, reg, smem_dbl);
+    if (mode == 0) {
+        qr_apply_q(P, mq, mq, R, tau, B, ldb, r);
+        return;
+    }
+    if (mode == 1) {
+        double *ts = smem + mq * R;
+        for (int e = threadIdx.x; e < R; e += NT) ts[e] = tau[e];
+        panel_to_sm(smem, P, mq, (int)mq, R);
+        apply_q_sm(smem, (int)mq, (int)mq, R, ts, B, ldb, r);
+        return;
+    }
+    const int nc = ts_nchunks(mq);
+    const int64_t nslot = ts_slot(K);
+    const double *taus = reg, *nodes = reg + (int64_t)nc * K;
+    const int R2 = 2 * R;
+    int top = 1;
+    while (2 * top < nc) top *= 2;
+    for (int s = top; s >= 1; s /= 2)
+        for (int b = 0; b + s < nc; b += 2 * s) {
+            double *Bb = B + ts_c0(mq, nc, b), *Bc = B + ts_c0(mq, nc, b + s);
+            const double *slot = nodes + (int64_t)(b + s) * nslot;
+            double *ts = smem + (int64_t)R2 * R;
+            for (int e = threadIdx.x; e < R2 * r; e += NT) {
+                const int i = e % R2, cc = e / R2;
+                tmp[e] = (i < R) ? Bb[i + ldb * cc] : 0.0;
+            }
+            for (int e = threadIdx.x; e < R2 * R; e += NT) smem[e] = slot[e];
+            for (int e = threadIdx.x; e < R; e += NT) ts[e] = slot[2 * (int64_t)R * R + e];
+            __syncthreads();
+            apply_q_sm(smem, R2, R2, R, ts, tmp, R2, r);
+            for (int e = threadIdx.x; e < R2 * r; e += NT) {
+                const int i = e % R2, cc = e / R2;
+                if (i < R) Bb[i + ldb * cc] = tmp[e];
+                else Bc[(i - R) + ldb * cc] = tmp[e];
+            }
+            __syncthreads();
+        }
+    for (int cix = 0; cix < nc; ++cix) {
+        const int64_t r0 = ts_c0(mq, nc, cix);
+        const int rows = (int)(ts_c0(mq, nc, cix + 1) - r0);
+        double *ts = smem + (int64_t)rows * R;
+        for (int e = threadIdx.x; e < R; e += NT) ts[e] = taus[(int64_t)cix * K + e];
+        panel_to_sm(smem, P + r0, mq, rows, R);
+        apply_q_sm(smem, rows, rows, R, ts, B + r0, ldb, r);
+    }
+}
+
+// TSQR tree node (b, s) of one side: [B_b; B_{b+s}] = Q_node [R'; 0]; panel + taus -> slot b + s,
+// R' -> B_b.  2R x R in shared memory (2R <= 1024 rows fits for R <= 96 with the engine's 224 KB).
+__device__ void tsqr_node_up(double *Bk, double *Nd, int64_t nslot, int b, int s, int R, double *smem,
+                             int64_t smem_dbl, double *red)
+{
+    const int R2 = 2 * R;
+    const int64_t RR = (int64_t)R * R;
+    double *slot = Nd + (int64_t)(b + s) * nslot;
+    const bool sm = (int64_t)R2 * R + R <= smem_dbl;
+    double *P = sm ? smem : slot;
+    double *ts = sm ? smem + (int64_t)R2 * R : slot + 2 * RR;
+    for (int e = threadIdx.x; e < R2 * R; e += NT) {
+        const int i = e % R2, k = e / R2;
+        const double *src = (i < R) ? Bk + (int64_t)b * RR + i + (int64_t)R * k
+                                    : Bk + (int64_t)(b + s) * RR + (i - R) + (int64_t)R * k;
+        P[e] = __ldcg(src);
+    }
+    __syncthreads();
+    if (sm) qr_sm(P, R2, R2, R, ts);
+    else qr_house(P, R2, R2, R, ts, red);
+    for (int e = threadIdx.x; e < RR; e += NT) {
+        const int i = e % R, k = e / R;
+        __stcg(Bk + (int64_t)b * RR + e, (k >= i) ? P[i + (int64_t)R2 * k] : 0.0);
+    }
+    if (sm) {
+        for (int e = threadIdx.x; e < R2 * R; e += NT) __stcg(slot + e, P[e]);
+        for (int e = threadIdx.x; e < R; e += NT) __stcg(slot + 2 * RR + e, ts[e]);
+    }
+    __syncthreads();
+}
+
+// Push the core down node (b, s): [C_b; 0] (2R x r) <- Q_node [C_b; 0]; top half -> C_b, bottom
+// half -> C_{b+s}.  tmp: 2R x r private scratch.
+__device__ void tsqr_node_down(double *Ck, const double *Nd, int64_t nslot, int b, int s, int R, int r, double *tmp,
+                               double *smem, int64_t smem_dbl)
+{
+    const int R2 = 2 * R;
+    const int64_t RR = (int64_t)R * R, Rr = (int64_t)R * r;
+    const double *slot = Nd + (int64_t)(b + s) * nslot;
+    for (int e = threadIdx.x; e < R2 * r; e += NT) {
+        const int i = e % R2, c = e / R2;
+        tmp[e] = (i < R) ? __ldcg(Ck + (int64_t)b * Rr + i + (int64_t)R * c) : 0.0;
+    }
+    const bool sm = (int64_t)R2 * R + R <= smem_dbl;
+    if (sm) {
+        double *ts = smem + (int64_t)R2 * R;
+        for (int e = threadIdx.x; e < R2 * R; e += NT) smem[e] = __ldcg(slot + e);
+        for (int e = threadIdx.x; e < R; e += NT) ts[e] = __ldcg(slot + 2 * RR + e);
+        __syncthreads();
+        apply_q_sm(smem, R2, R2, R, ts, tmp, R2, r);
+    } else {
+        __syncthreads();
+        qr_apply_q(slot, R2, R2, R, slot + 2 * RR, tmp, R2, r);
+    }
+    for (int e = threadIdx.x; e < R2 * r; e += NT) {
+        const int i = e % R2, c = e / R2;
+        double *dst = (i < R) ? Ck + (int64_t)b * Rr + i + (int64_t)R * c
+                              : Ck + (int64_t)(b + s) * Rr + (i - R) + (int64_t)R * c;
+        __stcg(dst, tmp[e]);
+    }
+    __syncthreads();
+}
+
 // Gang truncation of X Y^T (m x m, R columns; member rows in the local panels w.X, w.Y with
-// ld mq >= R): local Householder QR per member (TSQR leaves); QR of the stacked R factors of X by
-// member 0 and of Y by member 1 in parallel; the core M = R_X R_Y^T (compress_core) by member 0;
-// the stacked Q's applied to the cores (members 0 and 1); then every member applies its local Q
-// to its rows [core block g; 0] of the result U, V (global, ld ldo, rows q0..q0+mq).  Panels that
-// fit are factored in shared memory (qr_house_sm / apply_q_sm), larger ones in global memory.
+// ld mq >= R).  TSQR: every member factors its rows (local QR); the R factors are combined by a
+// binary tree (node (b, s) merges blocks b and b + s; the X tree runs on member b, the Y tree on
+// member b + s, so both proceed in parallel); member 0 truncates the core M = R_X R_Y^T
+// (compress_core); the core factors are pushed down the trees, and every member applies its local
+// Q to its block [C_g; 0] of the result U, V (global, ld ldo, rows q0..q0+mq).
 __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, int R, double eps, double tol_q,
                              bool svd, int kmax, int rlim, double *U, double *V, int64_t ldo, int *cb, int *of,
                              double *red, double *redv, int64_t *redi, double *smem, int64_t smem_dbl)
@@ -381,122 +588,72 @@ __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, in
     if (R == 0) { *cb = 0; *of = 0; return 0; }
     const int G = gg.G, g = gg.g;
     const int64_t mq = gg.mq, q0 = gg.q0;
-    const int64_t GR = (int64_t)G * R;
-    const bool loc_sm = mq <= 1024 && mq * R + R <= smem_dbl;
-    const bool stk_sm = GR <= 1024 && GR * R + R <= smem_dbl;
-    double *As = smem, *ts = smem + (loc_sm ? mq * R : GR * R);
-    // phase 1 (all members): local Householder QR of the member's rows (TSQR leaves)
+    const int64_t RR = (int64_t)R * R;
+    // phase 1 (all members): local QR, R factor -> B_g
     PH_BEGIN(t1);
-    if (loc_sm) {
-        ts = smem + mq * R;
-        panel_to_sm(As, w.X, mq, (int)mq, R);
-        qr_sm(As, (int)mq, (int)mq, R, ts);
-        for (int e = threadIdx.x; e < R; e += NT) w.tx[e] = ts[e];
-        panel_from_sm(w.X, mq, As, (int)mq, R);
-        panel_to_sm(As, w.Y, mq, (int)mq, R);
-        qr_sm(As, (int)mq, (int)mq, R, ts);
-        for (int e = threadIdx.x; e < R; e += NT) w.ty[e] = ts[e];
-        panel_from_sm(w.Y, mq, As, (int)mq, R);
-    } else {
-        qr_house(w.X, mq, mq, R, w.tx, red);
-        qr_house(w.Y, mq, mq, R, w.ty, red);
-    }
-    for (int e = threadIdx.x; e < R * R; e += NT) {
+    const int K = w.K;
+    local_qr(w.X, mq, R, w.tx, w.tsr, K, smem, smem_dbl, red);
+    local_qr(w.Y, mq, R, w.ty, w.tsr ? w.tsr + ts_region_doubles(mq, K) / 2 : nullptr, K, smem, smem_dbl, red);
+    for (int e = threadIdx.x; e < RR; e += NT) {
         const int i = e % R, k = e / R;
-        __stcg(gw.RSX + (int64_t)g * R + i + GR * k, (k >= i) ? w.X[i + mq * k] : 0.0);
-        __stcg(gw.RSY + (int64_t)g * R + i + GR * k, (k >= i) ? w.Y[i + mq * k] : 0.0);
+        __stcg(gw.BX + (int64_t)g * RR + e, (k >= i) ? w.X[i + mq * k] : 0.0);
+        __stcg(gw.BY + (int64_t)g * RR + e, (k >= i) ? w.Y[i + mq * k] : 0.0);
     }
     PH_END(9, t1);
     gang_sync(gg);
-    // phase 2a: QR of the stacked R_X's (member 0) and R_Y's (member 1); the stacked panel stays
-    // in the member's shared memory for phase 2c
+    // phase 2: up the trees
     PH_BEGIN(t2);
-    if (g <= 1) {
-        double *S = (g == 0) ? gw.RSX : gw.RSY;
-        double *tg = (g == 0) ? gw.tsx : gw.tsy;
-        if (stk_sm) {
-            ts = smem + GR * R;
-            for (int e = threadIdx.x; e < GR * R; e += NT) As[e] = __ldcg(S + e);
-            __syncthreads();
-            qr_sm(As, (int)GR, (int)GR, R, ts);
-            if (g == 0) {   // member 0 needs its shared memory for the core: whole panel back
-                for (int e = threadIdx.x; e < R; e += NT) tg[e] = ts[e];
-                for (int e = threadIdx.x; e < GR * R; e += NT) __stcg(S + e, As[e]);
-            } else {        // R factor for the core
-                for (int e = threadIdx.x; e < R * R; e += NT) {
-                    const int i = e % R, k = e / R;
-                    __stcg(S + i + GR * k, As[i + GR * k]);
-                }
-            }
-        } else {
-            qr_house(S, GR, GR, R, tg, red);
-            for (int e = threadIdx.x; e < R * R; e += NT) {
-                const int i = e % R, k = e / R;
-                __stcg(S + i + GR * k, S[i + GR * k]);
-            }
-        }
+    int top = 1;
+    while (2 * top < G) top *= 2;
+    for (int s = 1; s < G; s *= 2) {
+        if (g % (2 * s) == 0 && g + s < G) tsqr_node_up(gw.BX, gw.NX, gw.nslot, g, s, R, smem, smem_dbl, red);
+        if (g % (2 * s) == s) tsqr_node_up(gw.BY, gw.NY, gw.nslot, g - s, s, R, smem, smem_dbl, red);
+        gang_sync(gg);
     }
     PH_END(10, t2);
-    gang_sync(gg);
-    // phase 2b: core truncation (member 0) into UC / VC (GR x r, rows >= R zero)
+    // phase 3: core truncation (member 0) -> C_0 (R x r each side)
     if (g == 0) {
         PH_BEGIN(t3);
-        for (int e = threadIdx.x; e < R * R; e += NT) {
-            const int i = e % R, k = e / R;
-            w.RX[e] = __ldcg(gw.RSX + i + GR * k);
-            w.RY[e] = __ldcg(gw.RSY + i + GR * k);
+        for (int e = threadIdx.x; e < RR; e += NT) {
+            w.RX[e] = __ldcg(gw.BX + e);
+            w.RY[e] = __ldcg(gw.BY + e);
         }
         __syncthreads();
         int c1 = 0, o1 = 0;
         const int rr = compress_core(core_ws_sm(w, smem, smem_dbl, R), w.RX, R, w.RY, R, R, eps, tol_q, svd, kmax,
-                                     rlim, gw.UC, gw.VC, GR, GR, &c1, &o1, red, redv, redi);
+                                     rlim, gw.CX, gw.CY, R, R, &c1, &o1, red, redv, redi);
         if (threadIdx.x == 0) { gw.ires[0] = rr; gw.ires[1] = c1; gw.ires[2] = o1; }
         PH_END(11, t3);
     }
     gang_sync(gg);
     const int r = __ldcg(gw.ires);
-    // phase 2c: apply the stacked Q's (member 0: U core, member 1: V core)
+    // phase 4: down the trees
     PH_BEGIN(t4);
-    if (g <= 1 && r > 0) {
-        double *S = (g == 0) ? gw.RSX : gw.RSY;
-        double *tg = (g == 0) ? gw.tsx : gw.tsy;
-        double *B = (g == 0) ? gw.UC : gw.VC;
-        if (stk_sm) {
-            if (g == 0) {
-                for (int e = threadIdx.x; e < R; e += NT) smem[GR * R + e] = tg[e];
-                for (int e = threadIdx.x; e < GR * R; e += NT) As[e] = __ldcg(S + e);
-                __syncthreads();
-            }
-            apply_q_sm(As, (int)GR, (int)GR, R, smem + GR * R, B, GR, r);
+    if (r > 0) {
+        for (int s = top; s >= 1; s /= 2) {
+            if (g % (2 * s) == 0 && g + s < G)
+                tsqr_node_down(gw.CX, gw.NX, gw.nslot, g, s, R, r, w.G, smem, smem_dbl);
+            if (g % (2 * s) == s) tsqr_node_down(gw.CY, gw.NY, gw.nslot, g - s, s, R, r, w.G, smem, smem_dbl);
+            gang_sync(gg);
         }
-        else qr_apply_q(S, GR, GR, R, tg, B, GR, r);
     }
     PH_END(10, t4);
-    gang_sync(gg);
-    // phase 3 (all members): rows of U = Q_g [UC block g; 0], V likewise
+    // phase 5 (all members): rows of U = Q_g [C_g; 0], V likewise
     PH_BEGIN(t5);
+    const int64_t Rr = (int64_t)R * r;
     for (int64_t e = threadIdx.x; e < mq * r; e += NT) {
         const int64_t i = e % mq;
         const int cc = (int)(e / mq);
-        U[q0 + i + ldo * cc] = (i < R) ? __ldcg(gw.UC + (int64_t)g * R + i + GR * cc) : 0.0;
-        V[q0 + i + ldo * cc] = (i < R) ? __ldcg(gw.VC + (int64_t)g * R + i + GR * cc) : 0.0;
+        U[q0 + i + ldo * cc] = (i < R) ? __ldcg(gw.CX + (int64_t)g * Rr + i + (int64_t)R * cc) : 0.0;
+        V[q0 + i + ldo * cc] = (i < R) ? __ldcg(gw.CY + (int64_t)g * Rr + i + (int64_t)R * cc) : 0.0;
     }
     *cb = __ldcg(gw.ires + 1);
     *of = __ldcg(gw.ires + 2);
     __syncthreads();
     if (r > 0) {
-        if (loc_sm) {
-            ts = smem + mq * R;
-            for (int e = threadIdx.x; e < R; e += NT) ts[e] = w.tx[e];
-            panel_to_sm(As, w.X, mq, (int)mq, R);
-            apply_q_sm(As, (int)mq, (int)mq, R, ts, U + q0, ldo, r);
-            for (int e = threadIdx.x; e < R; e += NT) ts[e] = w.ty[e];
-            panel_to_sm(As, w.Y, mq, (int)mq, R);
-            apply_q_sm(As, (int)mq, (int)mq, R, ts, V + q0, ldo, r);
-        } else {
-            qr_apply_q(w.X, mq, mq, R, w.tx, U + q0, ldo, r);
-            qr_apply_q(w.Y, mq, mq, R, w.ty, V + q0, ldo, r);
-        }
+        local_apply(w.X, mq, R, w.tx, w.tsr, K, U + q0, ldo, r, w.G, smem, smem_dbl);
+        local_apply(w.Y, mq, R, w.ty, w.tsr ? w.tsr + ts_region_doubles(mq, K) / 2 : nullptr, K, V + q0, ldo, r, w.G,
+                    smem, smem_dbl);
     }
     PH_END(12, t5);
     gang_sync(gg);
@@ -649,9 +806,9 @@ __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *sme
                       red, redv, redi, smem, c.smem_dbl);
         record_rank(c, r, rk, cb, of);
     } else {
-        gg->mq = m / gg->G;
-        gg->q0 = (int64_t)gg->g * gg->mq;
+        gang_rows(*gg, m);
         CompressWs w = make_ws(scr, gg->mq, KB, &X2, &Y2, 4);
+        w.tsr = scr + task_scratch_base(gg->mq, c.kcap, 4);
         GangWs gw = make_gws(gg->shared, KB, gg->G);
         k = gang_aca(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, (uint8_t *)w.tail, K, 0.1 * c.eps, gw, *gg, red,
                      redv, redi);
@@ -717,10 +874,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     const int K = kbuf_of(c.kcap);
     const int maxw = max(32, c.kcap);
     double *X2, *Y2;
-    if (gg) {
-        gg->mq = m / gg->G;
-        gg->q0 = (int64_t)gg->g * gg->mq;
-    }
+    if (gg) gang_rows(*gg, m);
     if (m <= HCOV_DENSE_MAX) {
         // small block: exact dense accumulation S = U V^T - sum of terms (m x m), fully pivoted
         // cross approximation of S to 0.1 eps |S|_max / m (so |S - X Y^T|_2 <= 0.1 eps |S|_2), then
@@ -785,6 +939,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     // factor mode (m > HCOV_DENSE_MAX); rows [q0, q0 + mq) belong to this CTA (the whole block
     // without a gang); the panels w.X, w.Y, X2, Y2 hold those rows (ld mq).
     CompressWs w = make_ws(scr, gg ? gg->mq : m, K, &X2, &Y2, gg ? 4 : 6);
+    if (gg) w.tsr = scr + task_scratch_base(gg->mq, c.kcap, 4);
     const int64_t mq = gg ? gg->mq : m, q0 = gg ? gg->q0 : 0;
     GangWs gw{};
     if (gg) gw = make_gws(gg->shared, K, gg->G);

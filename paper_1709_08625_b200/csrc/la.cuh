@@ -944,6 +944,8 @@ struct CompressWs {
     double *T1, *T2;    // m x K each: Cholesky-QR ping-pong panels (Q_X ends in T1, Q_Y in T2)
     double *dX, *dY;    // K each (column scales)
     double *tail;       // first free (8-byte aligned) double after the workspace
+    double *tsr;        // gang members with more than 256 rows: in-CTA TSQR region (ts_region_doubles)
+    int K;              // column capacity of the panels and K x K arrays
 };
 
 // The core's K x K work arrays (M, G, J and vectors) in shared memory when they fit (R x R each).

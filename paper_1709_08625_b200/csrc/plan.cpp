@@ -628,7 +628,7 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
     for (const DRBlk &r : P.rblk) {
         P.max_rm = std::max<int64_t>(P.max_rm, r.m);
         const int32_t g = gang_of(r.m);
-        if (g > 0) P.max_mq = std::max<int64_t>(P.max_mq, r.m / g);
+        if (g > 0) P.max_mq = std::max<int64_t>(P.max_mq, r.m - (int64_t)(g - 1) * (r.m / g));   // last member
     }
     return 0;
 }

@@ -178,6 +178,35 @@ def test_collinear_ou_exact_large():
     assert _rel(r["loglik"], ref[0]) <= 1e-8, (r, ref)
 
 
+@pytest.mark.parametrize("n", [50001, 300007])
+def test_collinear_ou_exact_ragged_gangs(n):
+    """Exact Markov likelihood at n not a power of two: gangs with a remainder row split
+    (the last member takes m - (G-1) floor(m/G) rows) and, at 300,007, member panels above 256 rows
+    (in-CTA chunked TSQR)."""
+    s = synth.collinear_points(n, 43)
+    Z = oracle.sample_ou_collinear(s[:, 0], synth.xi(n, 44), 1.0, 0.05)
+    ref = oracle.loglik_ou_collinear(s[:, 0], Z, 1.0, 0.05)
+    T = H.Tree(_dev(s))
+    r = H.eval_loglik(T, (1.0, 0.05, 0.5, 0.0), _dev(Z), eps=1e-6, kmax=20)
+    assert r["status"] == 0
+    assert _rel(r["logdet"], ref[1]) <= 1e-8, (r, ref)
+    assert _rel(r["quad"], ref[2]) <= 1e-8, (r, ref)
+
+
+def test_ragged_n_dense_oracle():
+    """n = 12,345 uniform points (ragged clusters, gangs with remainders) vs the dense oracle."""
+    n = 12345
+    s = synth.uniform_points(n, 45)
+    th = (1.0, 0.05, 0.5, 1e-6)
+    Z = oracle.sample_dense(s, synth.xi(n, 46), *th)
+    ref = oracle.loglik_dense(s, Z, *th)
+    T = H.Tree(_dev(s))
+    r = H.eval_loglik(T, th, _dev(Z), eps=1e-8)
+    assert r["status"] == 0
+    err = min(_rel(r["loglik"], ref[0]), _scaled_err(r, ref, n))
+    assert err <= 1e-6, (r, ref)
+
+
 def test_sample_then_solve_gives_xi():
     """Z = L~ xi with the same factor => v = L~^{-1} Z = xi, q = xi^T xi (to round-off)."""
     n = 20000
