@@ -857,6 +857,170 @@ __device__ void task_tile(const Ctx &c, const DTask &tk, double *smem, double &f
     for (int e = threadIdx.x; e < HCOV_TILE; e += NT) __stcg(Tg + e, sm.S[e]);
 }
 
+// S (m x m, ld m) += XA YB^T, XA and YB m x W (ld m, global).  Row blocks of 16 MA rows per pass;
+// thread (ty, tx) of the 16 x 32 grid owns rows ty + 16 a and columns tx + 32 b; k staged through
+// shared memory (sb: 16 (16 MA + 32 NB) doubles).
+template <int MA, int NB>
+__device__ void dense_gemm_add(double *S, int m, const double *XA, const double *YB, int W, double *sb)
+{
+    constexpr int KC = 16, PR = 16 * MA, CN = 32 * NB;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    double *xs = sb, *ys = sb + KC * PR;
+    for (int p0 = 0; p0 < m; p0 += PR) {
+        double acc[MA][NB];
+#pragma unroll
+        for (int a = 0; a < MA; ++a)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) acc[a][b] = 0.0;
+        for (int k0 = 0; k0 < W; k0 += KC) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < KC * PR; e += NT) {
+                const int k = e / PR, i = e % PR;
+                xs[e] = (p0 + i < m && k0 + k < W) ? __ldcg(XA + (p0 + i) + (int64_t)m * (k0 + k)) : 0.0;
+            }
+            for (int e = threadIdx.x; e < KC * CN; e += NT) {
+                const int k = e / CN, j = e % CN;
+                ys[e] = (j < m && k0 + k < W) ? __ldcg(YB + j + (int64_t)m * (k0 + k)) : 0.0;
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int k = 0; k < KC; ++k) {
+                double xa[MA], yb[NB];
+#pragma unroll
+                for (int a = 0; a < MA; ++a) xa[a] = xs[k * PR + ty + 16 * a];
+#pragma unroll
+                for (int b = 0; b < NB; ++b) yb[b] = ys[k * CN + tx + 32 * b];
+#pragma unroll
+                for (int a = 0; a < MA; ++a)
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) acc[a][b] = fma(xa[a], yb[b], acc[a][b]);
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < MA; ++a)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                const int i = p0 + ty + 16 * a, j = tx + 32 * b;
+                if (i < m && j < m) S[i + (int64_t)m * j] += acc[a][b];
+            }
+    }
+    __syncthreads();
+}
+
+// Columns of one pending term in the dense accumulation (0 if a factor has rank 0).
+__device__ __forceinline__ int term_width(const Ctx &c, const DTerm &t)
+{
+    if (t.kind == TM_TT) return 32;
+    const int ra = __ldcg(c.rank + c.fac_rank_src[t.a]), rb = __ldcg(c.rank + c.fac_rank_src[t.b]);
+    return (ra == 0 || rb == 0) ? 0 : rb;
+}
+
+// Dense-mode accumulation (m <= HCOV_DENSE_MAX): S += U V^T - sum_k terms_k (S zero on entry),
+// in batches of at most Wcap columns gathered into XA / YB (m x Wcap each, global scratch).
+// Returns the flops.
+#define DENSE_BATCH 128
+__device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int64_t m, int64_t R0, int64_t C0,
+                                   const double *U, const double *V, int r0, double *XA, int64_t Wcap, double *sb)
+{
+    __shared__ int s_off[DENSE_BATCH + 1], s_kk[DENSE_BATCH];
+    __shared__ int s_nt, s_next, s_w;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *YB = XA + m * Wcap;
+    double fl = 0.0;
+    int kk = tk.b;
+    bool first = true;
+    while (first || kk < tk.c) {
+        if (threadIdx.x == 0) {
+            int W = (first ? r0 : 0), nt = 0, q = kk;
+            while (q < tk.c && nt < DENSE_BATCH) {
+                const int w = term_width(c, c.terms[c.xterm[q]]);
+                if (W + w > Wcap) break;
+                s_off[nt] = W;
+                s_kk[nt] = q;
+                W += w;
+                ++nt;
+                ++q;
+            }
+            s_off[nt] = W;
+            s_nt = nt;
+            s_next = q;
+            s_w = W;
+        }
+        __syncthreads();
+        const int nt = s_nt, W = s_w;
+        if (first && r0 > 0)
+            for (int64_t e = threadIdx.x; e < m * r0; e += NT) {
+                XA[e] = __ldcg(U + e);
+                YB[e] = __ldcg(V + e);
+            }
+        for (int j = warp; j < nt; j += NWARP) {
+            const DTerm t = c.terms[c.xterm[s_kk[j]]];
+            const int off = s_off[j], w = s_off[j + 1] - off;
+            if (w == 0) continue;
+            double *xc = XA + m * off, *yc = YB + m * off;
+            if (t.kind == TM_TT) {
+                const DNode na = c.nodes[c.tile_node[t.a]], nb = c.nodes[c.tile_node[t.b]];
+                const int64_t ar = (int64_t)na.i * HCOV_LEAF - R0, br = (int64_t)nb.i * HCOV_LEAF - C0;
+                const double *A = c.tiles + (int64_t)t.a * HCOV_TILE, *B = c.tiles + (int64_t)t.b * HCOV_TILE;
+                for (int k = 0; k < 32; ++k)
+                    for (int64_t i = lane; i < m; i += 32) {
+                        xc[i + m * k] = (i >= ar && i < ar + 32) ? -__ldcg(A + (i - ar) + 32 * k) : 0.0;
+                        yc[i + m * k] = (i >= br && i < br + 32) ? __ldcg(B + (i - br) + 32 * k) : 0.0;
+                    }
+            } else {
+                const Fac A = get_fac(c, t.a), B = get_fac(c, t.b);
+                const int ra = A.ncols;
+                const int64_t r_lo = max(R0, A.row0), r_hi = min(R0 + m, A.row0 + A.nrows);
+                const int64_t c_lo = max(C0, B.row0), c_hi = min(C0 + m, B.row0 + B.nrows);
+                const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcap * c.kcap : nullptr;
+                for (int64_t i = lane; i < m; i += 32) {
+                    const int64_t gi = R0 + i, gj = C0 + i;
+                    const bool inr = gi >= r_lo && gi < r_hi, inc = gj >= c_lo && gj < c_hi;
+                    const double *Ar = A.p + (gi - A.row0);
+                    for (int b0 = 0; b0 < w; b0 += 8) {
+                        double acc[8];
+#pragma unroll
+                        for (int bb = 0; bb < 8; ++bb) acc[bb] = 0.0;
+                        if (inr) {
+                            if (Kc) {
+                                for (int a = 0; a < ra; ++a) {
+                                    const double x = __ldcg(Ar + A.ld * a);
+                                    const double *kr = Kc + a + (int64_t)c.kcap * b0;
+#pragma unroll
+                                    for (int bb = 0; bb < 8; ++bb)
+                                        if (b0 + bb < w) acc[bb] = fma(x, __ldcg(kr + (int64_t)c.kcap * bb), acc[bb]);
+                                }
+                            } else {
+#pragma unroll
+                                for (int bb = 0; bb < 8; ++bb)
+                                    if (b0 + bb < w) acc[bb] = __ldcg(Ar + A.ld * (b0 + bb));
+                            }
+                        }
+#pragma unroll
+                        for (int bb = 0; bb < 8; ++bb)
+                            if (b0 + bb < w) {
+                                xc[i + m * (b0 + bb)] = -acc[bb];
+                                yc[i + m * (b0 + bb)] = inc ? __ldcg(B.p + (gj - B.row0) + B.ld * (b0 + bb)) : 0.0;
+                            }
+                    }
+                }
+                if (Kc) fl += 2.0 * (r_hi - r_lo) * ra * w;
+            }
+        }
+        __syncthreads();
+        if (W > 0) {
+            if (m <= 64) dense_gemm_add<4, 2>(S, (int)m, XA, YB, W, sb);
+            else if (m <= 128) dense_gemm_add<8, 4>(S, (int)m, XA, YB, W, sb);
+            else dense_gemm_add<4, 8>(S, (int)m, XA, YB, W, sb);
+            fl += 2.0 * m * m * W;
+        }
+        kk = s_next;
+        first = false;
+        __syncthreads();
+    }
+    return fl;
+}
+
 // A7 low-rank blocks: S = U V^T - sum of all pending terms, accumulated in factored form
 // X = [U, -A_1 K_1, ...], Y = [V, B_1, ...] (in scratch).  When the panel is full it is
 // recompressed near-losslessly (pivoted QR at eps*1e-4, no SVD); at the end X Y^T is truncated
@@ -883,46 +1047,13 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         const bool s_sm = m * m + 4096 <= c.smem_dbl;
         double *S = s_sm ? smem : scr;
         double *gs = s_sm ? smem + m * m : smem;
-        const int64_t gs_dbl = s_sm ? c.smem_dbl - m * m : c.smem_dbl;
         CompressWs wd = make_ws(scr + m * m, m, K, &X2, &Y2);   // X, Y panels (m x K) follow S
         PH_BEGIN(tg);
+        // S = U V^T - sum of terms as S = XA YB^T, batch by batch: the factor columns of a batch of
+        // terms (XA = [U, -A_1 K_1, -T_a, ...], YB = [V, B_1, T_b, ...], zero outside each term's
+        // rows) are gathered warp-parallel into the panel scratch, then one CTA GEMM adds them
         for (int64_t e = threadIdx.x; e < m * m; e += NT) S[e] = 0.0;
-        if (r0 > 0) cta_gemm_nt(S, m, m, m, r0, U, m, V, 1, m, 1.0, gs, gs_dbl);   // S = U V^T
-        fl += 2.0 * m * m * r0;
-        __syncthreads();
-        double *T1 = wd.Y;   // scratch for A K (m x rb), before Y is used by the ACA
-        for (int kk = tk.b; kk < tk.c; ++kk) {
-            const DTerm t = c.terms[c.xterm[kk]];
-            if (t.kind == TM_TT) {
-                const DNode na = c.nodes[c.tile_node[t.a]], nb = c.nodes[c.tile_node[t.b]];
-                const int64_t ar = (int64_t)na.i * HCOV_LEAF - R0, br = (int64_t)nb.i * HCOV_LEAF - C0;
-                const double *A = c.tiles + (int64_t)t.a * HCOV_TILE, *B = c.tiles + (int64_t)t.b * HCOV_TILE;
-                cta_gemm_nt(S + ar + m * br, m, 32, 32, 32, A, 32, B, 1, 32, -1.0, gs, gs_dbl);
-                fl += 2.0 * 32 * 32 * 32;
-            } else {
-                Fac A = get_fac(c, t.a), B = get_fac(c, t.b);
-                const int ra = A.ncols, rb = B.ncols;
-                if (ra == 0 || rb == 0) continue;
-                const int64_t r_lo = max(R0, A.row0), r_hi = min(R0 + m, A.row0 + A.nrows);
-                const int64_t c_lo = max(C0, B.row0), c_hi = min(C0 + m, B.row0 + B.nrows);
-                const int64_t nr = r_hi - r_lo, nc = c_hi - c_lo;
-                const double *Ap = A.p + (r_lo - A.row0);
-                const double *Bq = B.p + (c_lo - B.row0);
-                if (t.core >= 0) {
-                    // T1 = A K (nr x rb): T1(i, b) = sum_a A(i, a) K(a, b), K(a, b) = Kc[a + kcap b]
-                    const double *Kc = c.cores + (int64_t)t.core * c.kcap * c.kcap;
-                    for (int64_t e = threadIdx.x; e < nr * (int64_t)rb; e += NT) T1[e] = 0.0;
-                    cta_gemm_nt(T1, nr, nr, rb, ra, Ap, A.ld, Kc, c.kcap, 1, 1.0, gs, gs_dbl);
-                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, T1, nr, Bq, 1, B.ld, -1.0, gs,
-                                gs_dbl);
-                    fl += 2.0 * nr * ra * rb;
-                } else {
-                    cta_gemm_nt(S + (r_lo - R0) + m * (c_lo - C0), m, nr, nc, rb, Ap, A.ld, Bq, 1, B.ld, -1.0, gs,
-                                gs_dbl);
-                }
-                fl += 2.0 * nr * nc * rb;
-            }
-        }
+        fl += dense_accumulate(c, tk, S, m, R0, C0, U, V, r0, wd.X, 3 * (int64_t)K, gs);
         PH_END(6, tg);
         const int KA = (int)(m < K ? m : K);
         PH_BEGIN(ta);

@@ -225,7 +225,6 @@ __device__ __forceinline__ void householder_update(const double *aj, int64_t j, 
 
 __device__ void qr_house(double *A, int64_t lda, int64_t m, int R, double *tau, double *red)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int j = 0; j < R; ++j) {
         double *aj = A + lda * j;
         double s = 0.0;
@@ -254,7 +253,6 @@ __device__ void qr_house(double *A, int64_t lda, int64_t m, int R, double *tau, 
 __device__ void qr_apply_q(const double *A, int64_t lda, int64_t m, int R, const double *tau,
                            double *B, int64_t ldb, int r)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int j = R - 1; j >= 0; --j) {
         const double t = tau[j];
         if (t == 0.0) continue;

@@ -111,9 +111,32 @@ def show(path):
     for t in chain:
         if ty[t] == 11:
             continue
-        key = f"{NAMES[ty[t]]}{msize(t) or ''}" + ("f" if ty[t] == 5 and tasks[t, 4] == 1 else "")
+        key = f"{NAMES[ty[t]]}{msize(t) or ''}" + ("f" if ty[t] == 5 and tasks[t, 5] == 1 else "")
         cnt, tot = comp.get(key, (0, 0))
         comp[key] = (cnt + 1, tot + dur[t])
+    # how the chain moves: critical predecessor of each chain rapp (same block's previous chunk or other)
+    rch = [t for t in chain if ty[t] == 5]
+    chain_nn = [t for t in chain if ty[t] != 11]
+    if rch:
+        same = sum(1 for a, b in zip(chain_nn[:-1], chain_nn[1:])
+                   if ty[a] == 5 and ty[b] == 5 and tasks[a, 2] == tasks[b, 2])
+        blocks = len(set(int(tasks[t, 2]) for t in rch))
+        runs, cur = [], 1
+        for a, b in zip(rch[:-1], rch[1:]):
+            if tasks[a, 2] == tasks[b, 2]:
+                cur += 1
+            else:
+                runs.append(cur)
+                cur = 1
+        runs.append(cur)
+        print(f"  chain rapp: {len(rch)} tasks over {blocks} blocks; same-block chunk->chunk edges {same}; "
+              f"run lengths mean {np.mean(runs):.1f} max {max(runs)}")
+        preds_ty = {}
+        for a, b in zip(chain_nn[:-1], chain_nn[1:]):
+            if ty[b] == 5:
+                k = NAMES[ty[a]] + ("(same)" if ty[a] == 5 and tasks[a, 2] == tasks[b, 2] else "")
+                preds_ty[k] = preds_ty.get(k, 0) + 1
+        print("  critical predecessor of chain rapps:", preds_ty)
     print("  chain composition (type+m[f=final chunk]: count, total ms):",
           {k: (v[0], round(v[1] / 1e6, 1)) for k, v in sorted(comp.items(), key=lambda x: -x[1][1])})
     if rm is not None:
