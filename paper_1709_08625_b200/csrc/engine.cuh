@@ -1075,12 +1075,14 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     GangWs gw{};
     if (gg) gw = make_gws(gg->shared, K, gg->G);
     int cur = r0;
+    PH_BEGIN(tl0);
     for (int64_t e = threadIdx.x; e < mq * (int64_t)r0; e += NT) {
         const int64_t i = e % mq, l = e / mq;
         w.X[i + mq * l] = __ldcg(U + q0 + i + m * l);
         w.Y[i + mq * l] = __ldcg(V + q0 + i + m * l);
     }
     __syncthreads();
+    PH_END(14, tl0);
     for (int kk = tk.b; kk < tk.c; ++kk) {
         const DTerm t = c.terms[c.xterm[kk]];
         int width;
@@ -1102,6 +1104,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
             w.X = X2; w.Y = Y2; X2 = tx; Y2 = ty;
             cur = rk;
         }
+        PH_BEGIN(tap);
         double *xc = w.X + mq * cur, *yc = w.Y + mq * cur;
         for (int64_t e = threadIdx.x; e < mq * (int64_t)width; e += NT) { xc[e] = 0.0; yc[e] = 0.0; }
         __syncthreads();
@@ -1141,6 +1144,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
                 }
         }
         __syncthreads();
+        PH_END(14, tap);
         cur += width;
     }
     // last chunk: truncation to (eps, kmax) into capacity kcap; else near-lossless into 2 kcap

@@ -523,10 +523,12 @@ __device__ void qr_house_blk(double *A, int lda, int m, int R, double *tau)
         const int n0 = j0 + nb;
         const int nn = min(NB, R - n0);
         if (nn > 0) {
-            if (warp == 0) {   // look-ahead: next panel updated and factored by warp 0
-                hh_trail<QM>(A, lda, m, j0, nb, tau, n0, n0 + nn, 0, 1);
-                __syncwarp();
-                hh_panel<QM>(A, lda, m, n0, nn, tau);
+            // look-ahead: warps 0..3 update one column of the next panel each, then warp 0
+            // factors it while warps 1.. finish the trailing update
+            if (warp < 4) {
+                if (warp < nn) hh_trail<QM>(A, lda, m, j0, nb, tau, n0 + warp, n0 + warp + 1, warp, 1);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (warp == 0) hh_panel<QM>(A, lda, m, n0, nn, tau);
             }
             hh_trail<QM>(A, lda, m, j0, nb, tau, n0 + nn, R, 1, NWARP - 1);
         }
@@ -754,6 +756,92 @@ __device__ int qrcp_trunc(double *M, int K, double tol, int rmax, double *tau, i
                 w *= t;
                 if (lane == 0) ak[j] -= w;
                 for (int i = j + 1 + lane; i < K; i += 32) ak[i] -= aj[i] * w;
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    return j;
+}
+
+// Same contract as qrcp_trunc with two CTA barriers per step: warp 0 selects the pivot (exact
+// remaining column norms kept in cn), swaps and forms the reflector; then every warp applies it
+// to its columns (k mod NWARP) and recomputes their exact remaining norms.
+__device__ int qrcp_fast(double *M, int K, double tol, int rmax, double *tau, int *piv, double *cn)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ double s_n1;
+    __shared__ int s_stop;
+    for (int k = threadIdx.x; k < K; k += NT) piv[k] = k;
+    for (int k = warp; k < K; k += NWARP) {
+        const double *mk = M + (int64_t)K * k;
+        double sq = 0.0;
+        for (int i = lane; i < K; i += 32) sq = fma(mk[i], mk[i], sq);
+        sq = warp_sum(sq);
+        if (lane == 0) cn[k] = sq;
+    }
+    __syncthreads();
+    const int jmax = min(K, rmax);
+    int j = 0;
+    for (; j < jmax; ++j) {
+        if (warp == 0) {
+            double bv = -1.0;
+            int bi = K;
+            for (int k = j + lane; k < K; k += 32)
+                if (cn[k] > bv || (cn[k] == bv && k < bi)) { bv = cn[k]; bi = k; }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+            }
+            const double nrm = sqrt(fmax(bv, 0.0));
+            if (j == 0 && lane == 0) s_n1 = nrm;
+            __syncwarp();
+            const bool stop = !(nrm > tol * s_n1) || !(nrm > 0.0);
+            if (lane == 0) s_stop = stop;
+            if (!stop) {
+                const int p = bi;
+                double *aj = M + (int64_t)K * j;
+                if (p != j) {
+                    double *ap = M + (int64_t)K * p;
+                    for (int i = lane; i < K; i += 32) { const double t = aj[i]; aj[i] = ap[i]; ap[i] = t; }
+                    if (lane == 0) {
+                        const int t = piv[j]; piv[j] = piv[p]; piv[p] = t;
+                        cn[p] = cn[j];
+                    }
+                    __syncwarp();
+                }
+                double sq = 0.0;
+                for (int i = j + 1 + lane; i < K; i += 32) sq = fma(aj[i], aj[i], sq);
+                sq = warp_sum(sq);
+                const double alpha = aj[j];
+                double t = 0.0, beta = alpha;
+                if (sq > 0.0) {
+                    beta = -copysign(sqrt(alpha * alpha + sq), alpha);
+                    t = (beta - alpha) / beta;
+                    const double scale = 1.0 / (alpha - beta);
+                    for (int i = j + 1 + lane; i < K; i += 32) aj[i] *= scale;
+                }
+                __syncwarp();
+                if (lane == 0) { aj[j] = beta; tau[j] = t; }
+            }
+        }
+        __syncthreads();
+        if (s_stop) break;
+        const double t = tau[j];
+        const double *v = M + (int64_t)K * j;
+        int k0 = warp;
+        if (k0 <= j) k0 += NWARP * ((j - warp) / NWARP + 1);
+        for (int k = k0; k < K; k += 4 * NWARP) {
+            const int nk = min(4, (K - 1 - k) / NWARP + 1);
+            if (t != 0.0) house_apply4(v, j, K, t, M, K, k, NWARP, nk);
+            for (int q = 0; q < nk; ++q) {
+                const double *mk = M + (int64_t)K * (k + q * NWARP);
+                double sq = 0.0;
+                for (int i = j + 1 + lane; i < K; i += 32) sq = fma(mk[i], mk[i], sq);
+                sq = warp_sum(sq);
+                if (lane == 0) cn[k + q * NWARP] = sq;
             }
         }
         __syncthreads();
@@ -991,7 +1079,7 @@ __device__ int compress_core(const CompressWs &w, const double *RX, int64_t ldx,
     __syncthreads();
     PH_END(1, t1);
     PH_BEGIN(t2);
-    const int rq = qrcp_trunc(w.M, K, tol_q, svd ? K : rlim + 1, w.tm, w.piv, w.cn, redv, redi, red);
+    const int rq = qrcp_fast(w.M, K, tol_q, svd ? K : rlim + 1, w.tm, w.piv, w.cn);
     PH_END(2, t2);
     PH_BEGIN(t3);
     for (int e = threadIdx.x; e < K * rq; e += NT) {
