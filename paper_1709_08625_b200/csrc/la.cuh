@@ -836,13 +836,19 @@ __device__ int qrcp_fast(double *M, int K, double tol, int rmax, double *tau, in
         for (int k = k0; k < K; k += 4 * NWARP) {
             const int nk = min(4, (K - 1 - k) / NWARP + 1);
             if (t != 0.0) house_apply4(v, j, K, t, M, K, k, NWARP, nk);
-            for (int q = 0; q < nk; ++q) {
-                const double *mk = M + (int64_t)K * (k + q * NWARP);
-                double sq = 0.0;
-                for (int i = j + 1 + lane; i < K; i += 32) sq = fma(mk[i], mk[i], sq);
-                sq = warp_sum(sq);
-                if (lane == 0) cn[k + q * NWARP] = sq;
-            }
+            double sq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q < nk) {
+                    const double *mk = M + (int64_t)K * (k + q * NWARP);
+                    for (int i = j + 1 + lane; i < K; i += 32) sq[q] = fma(mk[i], mk[i], sq[q]);
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) sq[q] += __shfl_xor_sync(0xffffffffu, sq[q], o);
+            if (lane == 0)
+                for (int q = 0; q < nk; ++q) cn[k + q * NWARP] = sq[q];
         }
         __syncthreads();
     }
@@ -1142,7 +1148,8 @@ __device__ int compress_core(const CompressWs &w, const double *RX, int64_t ldx,
     }
     __syncthreads();
     PH_END(3, t3);
-    qr_apply_q(w.M, K, K, rq, w.tm, U, ldo, r);   // U_core <- Q_M U_core (rows < K)
+    // U_core <- Q_M U_core (rows < K): registers when K <= 1024, else the global sweep
+    if (!apply_q_sm(w.M, K, K, rq, w.tm, U, ldo, r)) qr_apply_q(w.M, K, K, rq, w.tm, U, ldo, r);
     if (threadIdx.x == 0) { *cap_bound = s_cb; *overflow = s_of; }
     __syncthreads();
     return r;
