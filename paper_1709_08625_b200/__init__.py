@@ -306,7 +306,7 @@ def prof_read() -> dict:
 
 
 PHASES = ["panel_qr", "core_product", "pivoted_qr", "svd", "q_apply", "aca_full", "dense_updates", "",
-          "aca_partial", "gang_local_qr", "gang_stack_qr", "gang_core", "gang_rows", "gang_wait", "rapp_append", ""]
+          "aca_partial", "gang_local_qr", "gang_stack_qr", "gang_core", "gang_rows", "gang_wait", "rapp_append", "dense_gemm"]
 
 
 FLOP_CLASSES = ["assembly_evals", "tile", "truncation", "solve", "products"]

@@ -859,11 +859,11 @@ __device__ void task_tile(const Ctx &c, const DTask &tk, double *smem, double &f
 
 // S (m x m, ld m) += XA YB^T, XA and YB m x W (ld m, global).  Row blocks of 16 MA rows per pass;
 // thread (ty, tx) of the 16 x 32 grid owns rows ty + 16 a and columns tx + 32 b; k staged through
-// shared memory (sb: 16 (16 MA + 32 NB) doubles).
+// shared memory (sb: 32 (16 MA + 32 NB) doubles).
 template <int MA, int NB>
 __device__ void dense_gemm_add(double *S, int m, const double *XA, const double *YB, int W, double *sb)
 {
-    constexpr int KC = 16, PR = 16 * MA, CN = 32 * NB;
+    constexpr int KC = 32, PR = 16 * MA, CN = 32 * NB;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     double *xs = sb, *ys = sb + KC * PR;
     for (int p0 = 0; p0 < m; p0 += PR) {
@@ -920,8 +920,10 @@ __device__ __forceinline__ int term_width(const Ctx &c, const DTerm &t)
 // Returns the flops.
 #define DENSE_BATCH 128
 __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int64_t m, int64_t R0, int64_t C0,
-                                   const double *U, const double *V, int r0, double *XA, int64_t Wcap, double *sb)
+                                   const double *U, const double *V, int r0, double *XA, int64_t Wcap, double *sb,
+                                   int64_t sb_dbl)
 {
+    const int kbw = (int)min((int64_t)512, sb_dbl / NWARP);   // per-warp core staging (gather phase)
     __shared__ int s_off[DENSE_BATCH + 1], s_kk[DENSE_BATCH];
     __shared__ int s_nt, s_next, s_w;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -930,20 +932,22 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
     int kk = tk.b;
     bool first = true;
     while (first || kk < tk.c) {
+        // widths of the next DENSE_BATCH terms in parallel, then the batch's prefix by thread 0
+        const int cand = min(DENSE_BATCH, tk.c - kk);
+        for (int q = threadIdx.x; q < cand; q += NT) s_kk[q] = term_width(c, c.terms[c.xterm[kk + q]]);
+        __syncthreads();
         if (threadIdx.x == 0) {
-            int W = (first ? r0 : 0), nt = 0, q = kk;
-            while (q < tk.c && nt < DENSE_BATCH) {
-                const int w = term_width(c, c.terms[c.xterm[q]]);
+            int W = (first ? r0 : 0), nt = 0;
+            while (nt < cand) {
+                const int w = s_kk[nt];
                 if (W + w > Wcap) break;
                 s_off[nt] = W;
-                s_kk[nt] = q;
                 W += w;
                 ++nt;
-                ++q;
             }
             s_off[nt] = W;
             s_nt = nt;
-            s_next = q;
+            s_next = kk + nt;
             s_w = W;
         }
         __syncthreads();
@@ -954,7 +958,7 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
                 YB[e] = __ldcg(V + e);
             }
         for (int j = warp; j < nt; j += NWARP) {
-            const DTerm t = c.terms[c.xterm[s_kk[j]]];
+            const DTerm t = c.terms[c.xterm[kk + j]];
             const int off = s_off[j], w = s_off[j + 1] - off;
             if (w == 0) continue;
             double *xc = XA + m * off, *yc = YB + m * off;
@@ -973,47 +977,64 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
                 const int64_t r_lo = max(R0, A.row0), r_hi = min(R0 + m, A.row0 + A.nrows);
                 const int64_t c_lo = max(C0, B.row0), c_hi = min(C0 + m, B.row0 + B.nrows);
                 const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcap * c.kcap : nullptr;
+                // the core K (ra x w) staged in this warp's slice of shared memory: kb[a + ra b]
+                double *kb = sb + (int64_t)warp * kbw;
+                const bool kstaged = Kc && ra * w <= kbw;
+                if (kstaged) {
+                    for (int e = lane; e < ra * w; e += 32) kb[e] = __ldcg(Kc + (e % ra) + (int64_t)c.kcap * (e / ra));
+                    __syncwarp();
+                }
                 for (int64_t i = lane; i < m; i += 32) {
                     const int64_t gi = R0 + i, gj = C0 + i;
                     const bool inr = gi >= r_lo && gi < r_hi, inc = gj >= c_lo && gj < c_hi;
                     const double *Ar = A.p + (gi - A.row0);
-                    for (int b0 = 0; b0 < w; b0 += 8) {
-                        double acc[8];
+                    if (!inr) {
+                        for (int b = 0; b < w; ++b) xc[i + m * b] = 0.0;
+                    } else if (!Kc) {
+                        for (int b = 0; b < w; ++b) xc[i + m * b] = -__ldcg(Ar + A.ld * b);
+                    } else {
+                        for (int b0 = 0; b0 < w; b0 += 8) {
+                            double acc[8];
 #pragma unroll
-                        for (int bb = 0; bb < 8; ++bb) acc[bb] = 0.0;
-                        if (inr) {
-                            if (Kc) {
-                                for (int a = 0; a < ra; ++a) {
-                                    const double x = __ldcg(Ar + A.ld * a);
-                                    const double *kr = Kc + a + (int64_t)c.kcap * b0;
+                            for (int bb = 0; bb < 8; ++bb) acc[bb] = 0.0;
+                            for (int a0 = 0; a0 < ra; a0 += 4) {
+                                double xa[4];
 #pragma unroll
-                                    for (int bb = 0; bb < 8; ++bb)
-                                        if (b0 + bb < w) acc[bb] = fma(x, __ldcg(kr + (int64_t)c.kcap * bb), acc[bb]);
+                                for (int u = 0; u < 4; ++u) xa[u] = (a0 + u < ra) ? __ldcg(Ar + A.ld * (a0 + u)) : 0.0;
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const int a = a0 + u;
+                                    if (a < ra) {
+#pragma unroll
+                                        for (int bb = 0; bb < 8; ++bb)
+                                            if (b0 + bb < w) {
+                                                const double kv = kstaged ? kb[a + ra * (b0 + bb)]
+                                                                          : __ldcg(Kc + a + (int64_t)c.kcap * (b0 + bb));
+                                                acc[bb] = fma(xa[u], kv, acc[bb]);
+                                            }
+                                    }
                                 }
-                            } else {
-#pragma unroll
-                                for (int bb = 0; bb < 8; ++bb)
-                                    if (b0 + bb < w) acc[bb] = __ldcg(Ar + A.ld * (b0 + bb));
                             }
+#pragma unroll
+                            for (int bb = 0; bb < 8; ++bb)
+                                if (b0 + bb < w) xc[i + m * (b0 + bb)] = -acc[bb];
                         }
-#pragma unroll
-                        for (int bb = 0; bb < 8; ++bb)
-                            if (b0 + bb < w) {
-                                xc[i + m * (b0 + bb)] = -acc[bb];
-                                yc[i + m * (b0 + bb)] = inc ? __ldcg(B.p + (gj - B.row0) + B.ld * (b0 + bb)) : 0.0;
-                            }
                     }
+                    for (int b = 0; b < w; ++b)
+                        yc[i + m * b] = inc ? __ldcg(B.p + (gj - B.row0) + B.ld * b) : 0.0;
                 }
                 if (Kc) fl += 2.0 * (r_hi - r_lo) * ra * w;
             }
         }
         __syncthreads();
+        PH_BEGIN(tdg);
         if (W > 0) {
             if (m <= 64) dense_gemm_add<4, 2>(S, (int)m, XA, YB, W, sb);
             else if (m <= 128) dense_gemm_add<8, 4>(S, (int)m, XA, YB, W, sb);
             else dense_gemm_add<4, 8>(S, (int)m, XA, YB, W, sb);
             fl += 2.0 * m * m * W;
         }
+        PH_END(15, tdg);
         kk = s_next;
         first = false;
         __syncthreads();
@@ -1044,7 +1065,8 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         // cross approximation of S to 0.1 eps |S|_max / m (so |S - X Y^T|_2 <= 0.1 eps |S|_2), then
         // QR + SVD truncation to (eps, kmax)
         // S lives in shared memory when it leaves room for the GEMM staging (m <= 128)
-        const bool s_sm = m * m + 4096 <= c.smem_dbl;
+        const int64_t stage = m <= 64 ? 32 * 128 : m <= 128 ? 32 * 256 : 32 * 320;   // dense_gemm_add staging
+        const bool s_sm = m * m + stage <= c.smem_dbl;
         double *S = s_sm ? smem : scr;
         double *gs = s_sm ? smem + m * m : smem;
         CompressWs wd = make_ws(scr + m * m, m, K, &X2, &Y2);   // X, Y panels (m x K) follow S
@@ -1053,7 +1075,8 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         // terms (XA = [U, -A_1 K_1, -T_a, ...], YB = [V, B_1, T_b, ...], zero outside each term's
         // rows) are gathered warp-parallel into the panel scratch, then one CTA GEMM adds them
         for (int64_t e = threadIdx.x; e < m * m; e += NT) S[e] = 0.0;
-        fl += dense_accumulate(c, tk, S, m, R0, C0, U, V, r0, wd.X, 3 * (int64_t)K, gs);
+        fl += dense_accumulate(c, tk, S, m, R0, C0, U, V, r0, wd.X, 3 * (int64_t)K, gs,
+                               s_sm ? c.smem_dbl - m * m : c.smem_dbl);
         PH_END(6, tg);
         const int KA = (int)(m < K ? m : K);
         PH_BEGIN(ta);

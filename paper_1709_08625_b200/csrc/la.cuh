@@ -1243,16 +1243,16 @@ __device__ int compress(const CompressWs &w, int64_t m, int R, double eps, doubl
 __device__ int aca_full(double *S, int64_t m, double *X, double *Y, int Kmax, double rel_tol, double rel_fro,
                         double *red, double *redv, int64_t *redi)
 {
-    // rows i = threadIdx.x + NT q are owned by one thread for all columns (no index divisions)
+    // entries e = threadIdx.x + NT q (all threads busy for any m); the argmax ties go to the
+    // lowest e, so the pivots do not depend on the traversal
     double bv = 0.0, ss = 0.0;
     int64_t bi = 0;
-    for (int64_t j = 0; j < m; ++j)
-        for (int64_t i = threadIdx.x; i < m; i += NT) {
-            const int64_t e = i + m * j;
-            const double v = S[e], a = fabs(v);
-            ss += v * v;
-            if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
-        }
+    const int64_t mm = m * m;
+    for (int64_t e = threadIdx.x; e < mm; e += NT) {
+        const double v = S[e], a = fabs(v);
+        ss += v * v;
+        if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
+    }
     ValIdx b = block_argmax(bv, bi, redv, redi);
     const double fro0 = sqrt(block_sum(ss, red));
     const double tol = rel_tol * b.v, tolf = rel_fro * fro0;
@@ -1268,16 +1268,13 @@ __device__ int aca_full(double *S, int64_t m, double *X, double *Y, int Kmax, do
         __syncthreads();
         bv = 0.0; bi = 0; ss = 0.0;
         const double *xk = X + m * k, *yk = Y + m * k;
-        for (int64_t j = 0; j < m; ++j) {
-            const double yj = yk[j];
-            for (int64_t i = threadIdx.x; i < m; i += NT) {
-                const int64_t e = i + m * j;
-                const double v = S[e] - xk[i] * yj;
-                S[e] = v;
-                ss += v * v;
-                const double a = fabs(v);
-                if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
-            }
+        for (int64_t e = threadIdx.x; e < mm; e += NT) {
+            const int64_t j = e / m, i = e - j * m;
+            const double v = S[e] - xk[i] * yk[j];
+            S[e] = v;
+            ss += v * v;
+            const double a = fabs(v);
+            if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
         }
         b = block_argmax(bv, bi, redv, redi);
         fro = sqrt(block_sum(ss, red));
