@@ -1075,7 +1075,9 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         // terms (XA = [U, -A_1 K_1, -T_a, ...], YB = [V, B_1, T_b, ...], zero outside each term's
         // rows) are gathered warp-parallel into the panel scratch, then one CTA GEMM adds them
         for (int64_t e = threadIdx.x; e < m * m; e += NT) S[e] = 0.0;
-        fl += dense_accumulate(c, tk, S, m, R0, C0, U, V, r0, wd.X, 3 * (int64_t)K, gs,
+        // batch capacity: the whole per-CTA scratch after S (sized for the largest gang member)
+        const int64_t wcap = max((int64_t)3 * K, (c.scr_stride - m * m - 64) / (2 * m));
+        fl += dense_accumulate(c, tk, S, m, R0, C0, U, V, r0, wd.X, wcap, gs,
                                s_sm ? c.smem_dbl - m * m : c.smem_dbl);
         PH_END(6, tg);
         const int KA = (int)(m < K ? m : K);
