@@ -23,7 +23,10 @@ namespace {
 inline int32_t gang_of(int64_t m)
 {
     if (m < HCOV_GANG_MIN) return 0;
-    return (int32_t)std::min<int64_t>(HCOV_GANG, std::max<int64_t>(2, m / 256));
+    // gangs of up to 4 CTAs (faster to form, fewer idle members in the serial phases); 8 only for
+    // the largest blocks, which bounds a member's rows (and the per-CTA scratch) at m/8
+    const int64_t gmax = m >= 65536 ? HCOV_GANG : 4;
+    return (int32_t)std::min<int64_t>(gmax, std::max<int64_t>(2, m / 256));
 }
 
 inline int64_t heap_id(int l, int64_t c) { return ((int64_t)1 << l) - 1 + c; }
