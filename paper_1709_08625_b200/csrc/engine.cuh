@@ -1243,6 +1243,7 @@ __device__ int rhs_columns(const Ctx &c, const Rhs &h, int k0, double **colp, in
 
 // A7 (V <- L_ss^{-1} V) and A9 (v = L^{-1} z): rows of one leaf segment i of solve s.
 //   Y_i -= sum_{tiles (i,j), j < i} L_ij Y_j + sum_{low-rank b over row i} U_b[i] P_b;  Y_i <- L_ii^{-1} Y_i
+#define SEG_BATCH 32
 __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl)
 {
     const Rhs h = get_rhs(c, tk.a);
@@ -1253,7 +1254,8 @@ __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl
     double *Xs = Ts + HCOV_TILE;                  // 32 x SEG_MAXCOL (Y_j) / kcap x SEG_MAXCOL (P)
     double *Us = Xs + (int64_t)max(32, c.kcap) * SEG_MAXCOL;   // 32 x kcap
     double **colp = (double **)(Us + 32 * (int64_t)c.kcap);
-    __shared__ int s_nk, s_total;
+    __shared__ int s_nk, s_total, s_bn;
+    __shared__ int s_boff[SEG_BATCH], s_brk[SEG_BATCH];
     int k0 = 0;
     double q = 0.0;
     while (true) {
@@ -1266,49 +1268,69 @@ __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl
             Ys[e] = __ldcg(colp[k] + ro + rr);
         }
         __syncthreads();
-        for (int z = tk.c; z < tk.d; ++z) {
-            const DCtr ct = c.ctr[z];
-            if (ct.kind == 0) {
-                tile_load(Ts, c.tiles + (int64_t)ct.id * HCOV_TILE);
-                const int64_t jo = (int64_t)ct.aux * HCOV_LEAF - h.row0;
-                for (int e = threadIdx.x; e < 32 * nk; e += NT) {
-                    int rr = e & 31, k = e >> 5;
-                    Xs[e] = __ldcg(colp[k] + jo + rr);
+        // contributions in batches: all operands of a batch are loaded into shared memory at once
+        // (independent loads, one latency), then each thread accumulates its entries over the batch
+        double *bb = (double *)(colp + SEG_MAXCOL);   // batch area (the rest of shared memory)
+        const int64_t bcap = c.smem_dbl - (int64_t)(bb - smem) - 8;
+        for (int z0 = tk.c; z0 < tk.d;) {
+            if (threadIdx.x == 0) {
+                int64_t off = 0;
+                int z = z0, nb = 0;
+                while (z < tk.d && nb < SEG_BATCH) {
+                    const DCtr ct = c.ctr[z];
+                    const int rk = (ct.kind == 0) ? 32 : __ldcg(c.rank + ct.id);
+                    const int64_t need = (ct.kind == 0) ? HCOV_TILE + 32 * nk : 32 * (int64_t)rk + (int64_t)rk * nk;
+                    if (off + need > bcap && nb > 0) break;
+                    s_boff[nb] = (int)off;
+                    s_brk[nb] = rk;
+                    off += need;
+                    ++nb;
+                    ++z;
                 }
-                __syncthreads();
-                for (int e = threadIdx.x; e < 32 * nk; e += NT) {
-                    int rr = e & 31, k = e >> 5;
-                    double s = 0.0;
-#pragma unroll 8
-                    for (int l = 0; l < 32; ++l) s += Ts[rr + 32 * l] * Xs[l + 32 * k];
-                    Ys[e] -= s;
-                }
-                fl += 2.0 * 32 * 32 * nk;
-            } else {
-                const int r = ct.id;
-                const int rk = __ldcg(c.rank + r);
-                if (rk == 0) continue;
-                const DRBlk b = c.rblk[r];
-                const double *Ub = r_U(c, r);
-                const double *Pb = slot_get(c, ct.aux);
-                const int64_t uo = i * HCOV_LEAF - b.row0;
-                for (int e = threadIdx.x; e < 32 * rk; e += NT) {
-                    int rr = e & 31, l = e >> 5;
-                    Us[e] = __ldcg(Ub + uo + rr + (int64_t)b.m * l);
-                }
-                for (int e = threadIdx.x; e < rk * nk; e += NT) {
-                    int l = e % rk, k = e / rk;
-                    Xs[e] = __ldcg(Pb + l + (int64_t)rk * (k0 + k));
-                }
-                __syncthreads();
-                for (int e = threadIdx.x; e < 32 * nk; e += NT) {
-                    int rr = e & 31, k = e >> 5;
-                    double s = 0.0;
-                    for (int l = 0; l < rk; ++l) s += Us[rr + 32 * l] * Xs[l + rk * k];
-                    Ys[e] -= s;
-                }
-                fl += 2.0 * 32 * rk * nk;
+                s_bn = nb;
             }
+            __syncthreads();
+            const int nbt = s_bn;
+            for (int j = 0; j < nbt; ++j) {
+                const DCtr ct = c.ctr[z0 + j];
+                double *A = bb + s_boff[j];
+                const int rk = s_brk[j];
+                if (ct.kind == 0) {
+                    const double *T = c.tiles + (int64_t)ct.id * HCOV_TILE;
+                    double *X = A + HCOV_TILE;
+                    const int64_t jo = (int64_t)ct.aux * HCOV_LEAF - h.row0;
+                    for (int e = threadIdx.x; e < HCOV_TILE; e += NT) A[e] = __ldcg(T + e);
+                    for (int e = threadIdx.x; e < 32 * nk; e += NT) X[e] = __ldcg(colp[e >> 5] + jo + (e & 31));
+                } else if (rk > 0) {
+                    const DRBlk b = c.rblk[ct.id];
+                    const double *Ub = r_U(c, ct.id);
+                    const double *Pb = slot_get(c, ct.aux);
+                    const int64_t uo = i * HCOV_LEAF - b.row0;
+                    double *X = A + 32 * rk;
+                    for (int e = threadIdx.x; e < 32 * rk; e += NT)
+                        A[e] = __ldcg(Ub + uo + (e & 31) + (int64_t)b.m * (e >> 5));
+                    for (int e = threadIdx.x; e < rk * nk; e += NT) {
+                        const int l = e % rk, k = e / rk;
+                        X[e] = __ldcg(Pb + l + (int64_t)rk * (k0 + k));
+                    }
+                }
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < 32 * nk; e += NT) {
+                const int rr = e & 31, k = e >> 5;
+                double sacc = 0.0;
+                for (int j = 0; j < nbt; ++j) {
+                    const double *A = bb + s_boff[j];
+                    const int rk = s_brk[j];
+                    if (rk == 0) continue;
+                    const double *X = A + 32 * rk;   // dense: rk = 32, A = tile
+#pragma unroll 8
+                    for (int l = 0; l < rk; ++l) sacc = fma(A[rr + 32 * l], X[l + rk * k], sacc);
+                }
+                Ys[e] -= sacc;
+            }
+            for (int j = 0; j < nbt; ++j) fl += 2.0 * 32 * s_brk[j] * nk;
+            z0 += nbt;
             __syncthreads();
         }
         // Y_i <- L_ii^{-1} Y_i (forward substitution, one thread per column)
