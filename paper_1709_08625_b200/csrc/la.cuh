@@ -638,7 +638,9 @@ __device__ __forceinline__ void panel_from_sm(double *Gp, int64_t ldg, const dou
 // ------------------------------------------------------------------------------------------
 // One-sided Jacobi SVD of G (K x nc, ld K, global scratch): on return G <- G J (columns mutually
 // orthogonal, ||col_i|| = sigma_i) and J (nc x nc, ld nc) orthogonal, so G_in = (G J) J^T.
-// Round-robin parallel ordering (nc/2 disjoint pairs per round, one warp per pair).
+// Round-robin parallel ordering (nc/2 disjoint pairs per round, one warp per pair).  A pair is
+// rotated while |g_p^T g_q| > 1e-13 ||g_p|| ||g_q||: the column norms are then the singular values
+// to ~1e-13 relative, far below any truncation threshold used (eps >= 1e-11).
 // ------------------------------------------------------------------------------------------
 __device__ void jacobi_svd(double *G, int64_t K, double *J, int nc)
 {
@@ -663,7 +665,7 @@ __device__ void jacobi_svd(double *G, int64_t K, double *J, int nc)
                     al += x * x; be += y * y; ga += x * y;
                 }
                 al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-                if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+                if (ga != 0.0 && fabs(ga) > 1e-13 * sqrt(al * be)) {
                     double zeta = (be - al) / (2.0 * ga);
                     double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                     double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
