@@ -312,7 +312,7 @@ __device__ void record_rank(const Ctx &c, int r, int rk, int cb, int of)
 }
 
 __device__ __forceinline__ double final_tol(double eps, int R) { return eps / (10.0 * sqrt((double)(R > 0 ? R : 1))); }
-__device__ __forceinline__ double interm_tol(double eps) { return fmax(eps * 1e-4, 1e-15); }
+__device__ __forceinline__ double interm_tol(double eps) { return fmax(eps * 1e-2, 1e-15); }
 
 __device__ __forceinline__ double compress_flops(int64_t m, int R, int r)
 {
