@@ -1217,7 +1217,7 @@ __device__ __forceinline__ Rhs get_rhs(const Ctx &c, int s)
     return h;
 }
 
-#define SEG_MAXCOL 64   // right-hand-side columns processed per pass of a SEG / PHWR task
+#define SEG_MAXCOL 128  // right-hand-side columns processed per pass of a SEG task
 
 // Column map of a pass: smem arrays colp[k] = base pointer of column k of Y (rows relative to
 // the solve's row0), for columns [k0, k0 + nk) of the concatenated right-hand side.
@@ -1250,10 +1250,8 @@ __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl
     const int64_t i = tk.b;
     const int64_t ro = i * HCOV_LEAF - h.row0;   // local row offset of the segment
     double *Ys = smem;                            // 32 x SEG_MAXCOL
-    double *Ts = Ys + 32 * SEG_MAXCOL;            // 32 x 32 tile
-    double *Xs = Ts + HCOV_TILE;                  // 32 x SEG_MAXCOL (Y_j) / kcap x SEG_MAXCOL (P)
-    double *Us = Xs + (int64_t)max(32, c.kcap) * SEG_MAXCOL;   // 32 x kcap
-    double **colp = (double **)(Us + 32 * (int64_t)c.kcap);
+    double *Ts = Ys + 32 * SEG_MAXCOL;            // 32 x 32 tile (diagonal block)
+    double **colp = (double **)(Ts + HCOV_TILE);  // SEG_MAXCOL column pointers, then the batch area
     __shared__ int s_nk, s_total, s_bn;
     __shared__ int s_boff[SEG_BATCH], s_brk[SEG_BATCH];
     int k0 = 0;
