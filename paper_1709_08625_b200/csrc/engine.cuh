@@ -1334,12 +1334,28 @@ __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl
         // Y_i <- L_ii^{-1} Y_i (forward substitution, one thread per column)
         tile_load(Ts, c.tiles + (int64_t)c.diag_tile[i] * HCOV_TILE);
         __syncthreads();
-        for (int k = threadIdx.x; k < nk; k += NT) {
-            double *y = Ys + 32 * k;
-            for (int a = 0; a < 32; ++a) {
-                double s = y[a];
-                for (int l = 0; l < a; ++l) s -= Ts[a + 32 * l] * y[l];
-                y[a] = s / Ts[a + 32 * a];
+        // one warp per group of 4 columns, lane = row: 32 steps of (broadcast y_a, update rows > a)
+        {
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            const double dinv = 1.0 / Ts[lane + 32 * lane];
+            for (int k0c = 4 * warp; k0c < nk; k0c += 4 * NWARP) {
+                double y[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) y[u] = (k0c + u < nk) ? Ys[lane + 32 * (k0c + u)] : 0.0;
+#pragma unroll 4
+                for (int a = 0; a < 32; ++a) {
+                    const double da = __shfl_sync(0xffffffffu, dinv, a);
+                    const double la = Ts[lane + 32 * a];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const double ya = __shfl_sync(0xffffffffu, y[u], a) * da;
+                        if (lane == a) y[u] = ya;
+                        else if (lane > a) y[u] = fma(-la, ya, y[u]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (k0c + u < nk) Ys[lane + 32 * (k0c + u)] = y[u];
             }
         }
         __syncthreads();
