@@ -1244,6 +1244,7 @@ __device__ int rhs_columns(const Ctx &c, const Rhs &h, int k0, double **colp, in
 // A7 (V <- L_ss^{-1} V) and A9 (v = L^{-1} z): rows of one leaf segment i of solve s.
 //   Y_i -= sum_{tiles (i,j), j < i} L_ij Y_j + sum_{low-rank b over row i} U_b[i] P_b;  Y_i <- L_ii^{-1} Y_i
 #define SEG_BATCH 32
+#define SEG_RHS_MAX 128   // right-hand-side blocks whose ranks / bases a SEG task caches
 __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl)
 {
     const Rhs h = get_rhs(c, tk.a);
@@ -1254,10 +1255,34 @@ __device__ void task_seg(const Ctx &c, const DTask &tk, double *smem, double &fl
     double **colp = (double **)(Ts + HCOV_TILE);  // SEG_MAXCOL column pointers, then the batch area
     __shared__ int s_nk, s_total, s_bn;
     __shared__ int s_boff[SEG_BATCH], s_brk[SEG_BATCH];
+    __shared__ int s_rrk[SEG_RHS_MAX];
+    __shared__ double *s_rvp[SEG_RHS_MAX];
     int k0 = 0;
     double q = 0.0;
     while (true) {
-        if (threadIdx.x == 0) { int tot; s_nk = rhs_columns(c, h, k0, colp, &tot); s_total = tot; }
+        if (h.cnt > 0 && h.cnt <= SEG_RHS_MAX) {
+            // ranks and V bases of the right-hand-side blocks loaded in parallel (once per task)
+            if (k0 == 0) {
+                for (int q = threadIdx.x; q < h.cnt; q += NT) {
+                    const int r = c.solve_rhs[h.off + q];
+                    s_rrk[q] = __ldcg(c.rank + r);
+                    s_rvp[q] = r_V(c, r);
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                int k = 0, nk = 0;
+                for (int q = 0; q < h.cnt; ++q)
+                    for (int j = 0; j < s_rrk[q]; ++j, ++k)
+                        if (k >= k0 && nk < SEG_MAXCOL) colp[nk++] = s_rvp[q] + h.m * (int64_t)j;
+                s_nk = nk;
+                s_total = k;
+            }
+        } else if (threadIdx.x == 0) {
+            int tot;
+            s_nk = rhs_columns(c, h, k0, colp, &tot);
+            s_total = tot;
+        }
         __syncthreads();
         const int nk = s_nk;
         if (nk == 0) break;
@@ -1393,10 +1418,34 @@ __device__ void task_proj(const Ctx &c, const DTask &tk, double *smem, double &f
     double *Pb = slot_alloc(c, tk.c, (int64_t)rk * total + 1);
     double **colp = (double **)smem;
     __shared__ int s_nk, s_total;
+    __shared__ int s_rrk[SEG_RHS_MAX];
+    __shared__ double *s_rvp[SEG_RHS_MAX];
     const int64_t co = b.col0 - h.row0;
     int k0 = 0;
     while (true) {
-        if (threadIdx.x == 0) { int tot; s_nk = rhs_columns(c, h, k0, colp, &tot); s_total = tot; }
+        if (h.cnt > 0 && h.cnt <= SEG_RHS_MAX) {
+            // ranks and V bases of the right-hand-side blocks loaded in parallel (once per task)
+            if (k0 == 0) {
+                for (int q = threadIdx.x; q < h.cnt; q += NT) {
+                    const int r = c.solve_rhs[h.off + q];
+                    s_rrk[q] = __ldcg(c.rank + r);
+                    s_rvp[q] = r_V(c, r);
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                int k = 0, nk = 0;
+                for (int q = 0; q < h.cnt; ++q)
+                    for (int j = 0; j < s_rrk[q]; ++j, ++k)
+                        if (k >= k0 && nk < SEG_MAXCOL) colp[nk++] = s_rvp[q] + h.m * (int64_t)j;
+                s_nk = nk;
+                s_total = k;
+            }
+        } else if (threadIdx.x == 0) {
+            int tot;
+            s_nk = rhs_columns(c, h, k0, colp, &tot);
+            s_total = tot;
+        }
         __syncthreads();
         const int nk = s_nk;
         if (nk == 0) break;

@@ -9,7 +9,7 @@
                               // must stay below the number of engine CTAs (at most one partially
                               // formed gang per band can hold CTAs, so every gang eventually forms)
 #define HCOV_DENSE_MAX 256    // low-rank blocks up to this size are recompressed from a dense accumulation
-#define HCOV_SMEM_DBL 28672 // dynamic shared memory of the engine CTA (224 KB; one 512-thread CTA per SM)
+#define HCOV_SMEM_DBL 28160 // dynamic shared memory of the engine CTA (220 KB + static <= 227 KB; one 512-thread CTA per SM)
 #define HCOV_GANG_MIN 512     // low-rank blocks from this size on are processed by gangs of min(8, m/256) CTAs
 
 // Block-tree node types (lower triangle incl. diagonal).
