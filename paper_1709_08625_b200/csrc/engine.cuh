@@ -513,7 +513,7 @@ __device__ void local_apply(const double *P, int64_t mq, int R, const double *ta
 }
 
 // TSQR tree node (b, s) of one side: [B_b; B_{b+s}] = Q_node [R'; 0]; panel + taus -> slot b + s,
-// R' -> B_b.  2R x R in shared memory (2R <= 1024 rows fits for R <= 96 with the engine's 224 KB).
+// R' -> B_b.  2R x R in shared memory (2R <= 1024 rows fits for R <= 96 with the engine's 220 KB).
 __device__ void tsqr_node_up(double *Bk, double *Nd, int64_t nslot, int b, int s, int R, double *smem,
                              int64_t smem_dbl, double *red)
 {

@@ -262,7 +262,7 @@ __device__ void qr_apply_q(const double *A, int64_t lda, int64_t m, int R, const
 }
 
 // ------------------------------------------------------------------------------------------
-// Shared-memory resident Householder QR (one CTA per SM: the engine has ~224 KB of dynamic
+// Shared-memory resident Householder QR (one CTA per SM: the engine has ~220 KB of dynamic
 // shared memory, enough for a 256 x 96 panel).  Column k is owned by warp k mod NWARP; step j
 // applies H_j to every column k > j, and the owner of column j + 1 updates that column first and
 // computes reflector j + 1 (look-ahead), so each step costs one CTA barrier.  Same reflector

@@ -33,7 +33,7 @@ def test_truncation_error_bound(path, kind, m, R, eps):
     _check(path, kind, m, R, eps)
 
 
-# shared-memory Householder path (panel m x R resident in the engine's 224 KB): sizes across the
+# shared-memory Householder path (panel m x R resident in the engine's 220 KB): sizes across the
 # register-apply variants (m <= 256, m <= 512), ragged m, R = m
 @pytest.mark.parametrize("kind", ["decay", "dependent", "scaled"])
 @pytest.mark.parametrize("m,R,eps", [(256, 80, 1e-8), (200, 92, 1e-6), (300, 90, 1e-5), (64, 40, 1e-6),
