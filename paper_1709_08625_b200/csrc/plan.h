@@ -11,7 +11,7 @@ struct PlanOpts {
     double eta = 2.0;
     int dense_below = 32;   // admissible blocks of cluster size <= dense_below are dense tiles
     int chunk = 4;          // pending terms applied per TAPP task
-    int rchunk = 2;         // pending terms appended per RAPP task of a large low-rank block
+    int rchunk = 3;         // pending terms appended per RAPP task of a large low-rank block
     int fill_tiles = 8;     // tiles per FILL task
     int64_t big_m = HCOV_DENSE_MAX;   // larger low-rank blocks: chunked recompression, capacity 2 kcap
 };
