@@ -48,6 +48,10 @@ def _args():
     p.add_argument("--n", type=int, default=0, help="override n (debug only; not a bench line)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="oracle sample size (default: auto)")
+    p.add_argument("--eps", type=float, default=0.0, help="override eps (0 = the workload's)")
+    p.add_argument("--kmax", type=int, default=-1, help="override the rank cap (-1 = the workload's)")
+    p.add_argument("--acc-cols", type=int, default=64, help="sampled columns for ||C - C~||_F / ||C||_F")
+    p.add_argument("--out", default="", help="also write the JSON line to this file")
     return p.parse_args()
 
 
@@ -102,7 +106,8 @@ def _theta_for(cfg, j: int, m: int):
 
 def _oracle_cpu(cfg, n_s: int, th, reps: int = 1):
     """The oracle as it stands (dense Matern fill + LAPACK Cholesky + solve) on the first n_s
-    points of the config at theta th; returns (seconds per evaluation, threads)."""
+    points of the config at theta th, on every host core; returns (seconds per evaluation, threads)."""
+    os.environ.setdefault("HCOV_ORACLE_THREADS", str(os.cpu_count() or 1))
     import oracle
     s = synth.points(cfg)[:n_s]
     Z = synth.xi(n_s, cfg.seed_xi)
@@ -129,7 +134,7 @@ def run_reference(args, cfg, rank: int, world: int):
     if rank != 0:
         return
     n = cfg.n
-    th, eps, kmax, note = bench_params(args, cfg)
+    th, eps, kmax, note, wl = bench_params(args, cfg)
     n_s = args.cpu_sample or _cpu_sample_size(cfg, th, budget_s=8.0)
     for _ in range(args.warmup):
         _oracle_cpu(cfg, min(n_s, 2048), th)
@@ -144,9 +149,9 @@ def run_reference(args, cfg, rank: int, world: int):
            "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": cfg.name, "n": n, "nu": cfg.nu, "ell": th[1], "sigma2": th[0], "nu_used": th[2],
+           "config": {"workload": wl, "n": n, "nu": th[2], "ell": th[1], "sigma2": th[0],
                       "nugget": th[3], "eps": eps, "kmax": kmax, "theta_note": note},
-           "cpu_baseline": {"value": v, "unit": "evals/s", "cores": thr, "kind": "oracle",
+           "cpu_baseline": {"value": v, "unit": "evals/s", "cores": thr, "nproc": os.cpu_count(), "kind": "oracle",
                             "sample": f"dense oracle L(theta) on the first {n_s} of the {n} points, "
                                       f"{t_step:.2f} s/eval, extrapolated x(n/{n_s})^3"},
            "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -154,12 +159,43 @@ def run_reference(args, cfg, rank: int, world: int):
 
 
 def bench_params(args, cfg):
-    """(theta, eps, kmax, note) of the benchmarked evaluation (R24)."""
+    """(theta, eps, kmax, note, workload label) of the benchmarked evaluation (R24)."""
+    eps = args.eps if args.eps > 0 else None
+    kmax = args.kmax if args.kmax >= 0 else cfg.kmax
     if args.theta == "config" or cfg.name != "C5":
-        return (cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget), cfg.eps[0], cfg.kmax, "config theta"
+        return ((cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget), eps or cfg.eps[0], kmax,
+                "config theta as written" + ("" if eps is None else f" with eps={eps}"), cfg.name)
     c4 = synth.CONFIGS["C4"]
-    return ((c4.sigma2, c4.ell, c4.nu, c4.nugget), 1e-6, cfg.kmax,
-            "C5 points/n/k with C4's kernel (nu=0.5, ell=0.1) and eps=1e-6: C5's theta is not SPD (DESIGN.md R24)")
+    return ((c4.sigma2, c4.ell, c4.nu, c4.nugget), eps or 1e-6, kmax,
+            "C5's points, n and k with C4's kernel (nu=0.5, ell=0.1, sigma2=1, tau2=1e-6) and eps=1e-6: "
+            "C5's own theta (nu=1, ell=0.05) is not SPD under the method at eps=1e-5 (DESIGN.md R24)",
+            "C5-points/C4-kernel")
+
+
+def _peaks():
+    peaks, fp64 = {}, {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    try:
+        fp64 = json.load(open(os.path.join(ROOT, "profiles", "r1_fp64_peak.json")))
+    except OSError:
+        pass
+    return peaks, fp64
+
+
+def _traffic(workload: str, n: int):
+    """ncu dram bytes per launch of k_engine for this workload, from the committed capture summary
+    (profiles/r2_engine_traffic.json, written by tools/ncu_traffic.py from an `ncu --set full` run)."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r2_engine_traffic.json")))
+    except OSError:
+        return None, None
+    for e in t.get("entries", []):
+        if e.get("workload") == workload and int(e.get("n", -1)) == n:
+            return float(e["dram_bytes"]), e.get("source")
+    return None, None
 
 
 def run_hcov(args, cfg, rank: int, world: int):
@@ -174,19 +210,38 @@ def run_hcov(args, cfg, rank: int, world: int):
         dist.init_process_group("nccl", device_id=dev)
     n = args.n or cfg.n
     s = synth.points(cfg)[:n] if args.n else synth.points(cfg)
-    th0, eps, kmax, note = bench_params(args, cfg)
+    th0, eps, kmax, note, wl = bench_params(args, cfg)
+    if args.n:
+        wl = f"{wl}[n={n}]"
     stream = torch.cuda.current_stream()
     s_dev = torch.from_numpy(s).to(dev)
     tree = H.Tree(s_dev)                       # A1-A2: theta-independent, untimed
     info = tree.info()
-    # data: Z = L~ xi from the H-Cholesky factor at the config's theta (Sec. 5.1)
+    # data: Z = L~_gen xi from a TIGHTER H-Cholesky factor than the one
+    # evaluated (eps_gen = 1e-8, same rank cap), so v = L~^{-1} Z is not xi by construction
+    eps_gen = min(1e-8, eps)
     xi = torch.from_numpy(synth.xi(n, cfg.seed_xi)).to(dev)
-    hgen = H.HMatrix(tree, th0, eps, kmax)
+    hgen = H.HMatrix(tree, th0, eps_gen, kmax)
     hgen.cholesky()
     Z = hgen.sample(xi)
     del hgen
     m_total = max(1, world)
     my_theta = th0 if m_total == 1 else (th0[0], th0[1] * 0.8 * (1.25 / 0.8) ** (rank / (m_total - 1)), th0[2], th0[3])
+
+    # accuracy of the evaluated C~ (north_star: ||C - C~||_F / ||C||_F <= 10 eps on sampled columns),
+    # both sides on the device: C~ e_j from the assembled H-matrix, C e_j by direct Eq. (3) evaluation
+    acc = None
+    if args.acc_cols > 0:
+        hacc = H.HMatrix(tree, my_theta, eps, kmax)
+        cols = np.random.default_rng(7000 + rank).choice(n, args.acc_cols, replace=False)
+        ct = hacc.columns(cols)
+        ce = H.cov_columns(tree, my_theta, cols)
+        fro = float(torch.linalg.norm(ct - ce) / torch.linalg.norm(ce))
+        st_c = hacc.storage()
+        del hacc, ct, ce
+        acc = {"fro_rel_sampled": fro, "columns": int(args.acc_cols), "bar_10eps": 10 * eps, "ok": fro <= 10 * eps,
+               "C_tilde_kB_per_dof": (st_c["dense_bytes"] + st_c["lowrank_bytes"]) / n / 1024.0,
+               "C_tilde_max_rank": st_c["max_rank"]}
 
     def step():
         return H.eval_loglik(tree, my_theta, Z, eps, kmax)
@@ -203,14 +258,12 @@ def run_hcov(args, cfg, rank: int, world: int):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    gathered = []
     for _ in range(args.steps):
         r = step()
         if dist:
             t = torch.tensor([r["loglik"]], dtype=torch.float64, device=dev)
             g = torch.empty(world, dtype=torch.float64, device=dev)
             dist.all_gather_into_tensor(g, t)
-            gathered.append(g)
     e1.record(stream)
     torch.cuda.synchronize()
     if dist:
@@ -225,6 +278,9 @@ def run_hcov(args, cfg, rank: int, world: int):
         ms = float(t.item())
     ms_step = ms / args.steps
     value = world * args.steps / (ms * 1e-3)
+    last = H.last_eval(tree)
+    model = last.model_flops()
+    st_l = last.storage()
 
     # ---- e2e: host Z (pinned) -> device inside the timed region, result back to host -----------
     Zh = Z.cpu().pin_memory()
@@ -233,7 +289,6 @@ def run_hcov(args, cfg, rank: int, world: int):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
     e0.record(stream)
     for _ in range(k_e):
         Zd.copy_(Zh, non_blocking=True)
@@ -248,28 +303,25 @@ def run_hcov(args, cfg, rank: int, world: int):
     e2e = {"value": world * k_e / (ms_e2e * 1e-3), "unit": "evals/s", "h2d_bytes_per_step": 8 * n,
            "d2h_bytes_per_step": 3 * 8}
 
-    # ---- roofline of the dominant kernel class ------------------------------------------------
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    # dominant kernel = the persistent engine (one launch per step); algorithmic flop counted by the
-    # tasks (LAPACK counts at actual shapes) / engine CUDA-event time vs the measured fp64 FMA peak
+    # ---- roofline of the dominant kernel (k_engine, one launch per step) ---------------------
+    # achieved = SURVEY Sec. 8(d)'s method-work model at the measured ranks (hcov_model_flops) per
+    # launch / the engine's CUDA-event time per launch; peak = measured fp64 FMA rate
+    peaks, fp64 = _peaks()
     eng_ms = prof["ms"].get("engine", 0.0) / args.steps
-    fl = sum(v for k, v in prof["flop"].items() if k != "assembly_evals") / args.steps
-    fp64 = {}
-    try:
-        fp64 = json.load(open(os.path.join(ROOT, "profiles", "r1_fp64_peak.json")))
-    except OSError:
-        pass
+    impl_fl = sum(v for k, v in prof["flop"].items() if k != "assembly_evals") / args.steps
     peak = float(fp64.get("dfma_tflops", 36.85))
-    ach = fl / (eng_ms * 1e-3) / 1e12 if eng_ms > 0 else 0.0
+    ach = model["total"] / (eng_ms * 1e-3) / 1e12 if eng_ms > 0 else 0.0
+    traffic, tsrc = _traffic(wl, n)
     roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-            "traffic": None, "kernel": "k_engine (persistent DAG engine, 1 launch/step)",
-            "flop_per_launch": fl, "ms_per_launch": eng_ms,
-            "peak_source": "profiles/r1_fp64_peak.json: measured DFMA loop on this pool's B200 (fp64 not in "
-                           "MEASURED_PEAKS.json)"}
+            "traffic": traffic, "traffic_source": tsrc,
+            "kernel": "k_engine (persistent DAG engine, 1 launch/step)",
+            "model_flop_per_launch": model["total"], "model_breakdown": model,
+            "impl_flop_per_launch": impl_fl, "impl_frac": impl_fl / (eng_ms * 1e-3) / 1e12 / peak if eng_ms else 0.0,
+            "ms_per_launch": eng_ms,
+            # C~ written once, L~ rewritten in place, L~ read by the solve: ~3 x bytes of L~
+            "algorithmic_bytes_per_launch": 3.0 * (st_l["dense_bytes"] + st_l["lowrank_bytes"]),
+            "peak_source": "profiles/r1_fp64_peak.json: measured DFMA loop on this pool's B200 (fp64 is not in "
+                           "MEASURED_PEAKS.json; nominal 148 SM x 64 DFMA x 2 x 1.965 GHz = 37.2 TF/s)"}
 
     if rank != 0:
         if dist:
@@ -278,13 +330,19 @@ def run_hcov(args, cfg, rank: int, world: int):
     out = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": cfg.name if not args.n else f"{cfg.name}[n={n}]", "n": n, "nu": cfg.nu,
-                      "ell": th0[1], "sigma2": th0[0], "nu_used": th0[2], "nugget": th0[3], "eps": eps, "kmax": kmax,
-                      "theta_note": note,
+           "config": {"workload": wl, "n": n, "nu": my_theta[2], "ell": my_theta[1], "sigma2": my_theta[0],
+                      "nugget": my_theta[3], "eps": eps, "kmax": kmax, "eps_gen_Z": eps_gen,
+                      "theta_note": note, "config_as_written": {"name": cfg.name, "nu": cfg.nu, "ell": cfg.ell,
+                                                                "eps": cfg.eps[0], "kmax": cfg.kmax},
                       "leaf": 32, "eta": 2.0, "parallelism": f"theta-batch dp{world}",
                       "l2": "inputs larger than L2 (H-matrix >> 126 MB)",
                       "tree": {k: info[k] for k in ("depth", "n_dense_tiles", "n_lowrank", "n_tasks", "n_waves")}},
-           "loglik": r["loglik"], "max_rank": r["max_rank"], "cap_binds": r["cap_binds"],
+           "loglik": r["loglik"], "logdet": r["logdet"], "quad": r["quad"], "max_rank": r["max_rank"],
+           "cap_binds": r["cap_binds"], "acc_loss": r["acc_loss"], "min_pivot": r["min_pivot"],
+           "accuracy": acc,
+           "storage": {"L_tilde_kB_per_dof": (st_l["dense_bytes"] + st_l["lowrank_bytes"]) / n / 1024.0,
+                       "C_tilde_kB_per_dof": acc["C_tilde_kB_per_dof"] if acc else None,
+                       "paper_table4_C_tilde_kB_per_dof_at_2M": 7.4},
            "gpu_launches": int(prof["launches"] // max(1, args.steps)),
            "e2e": e2e, "roofline": roof, "clocks": clk,
            "stages_ms_per_step": {k: v / args.steps for k, v in prof["ms"].items()},
@@ -294,20 +352,39 @@ def run_hcov(args, cfg, rank: int, world: int):
         n_s = args.cpu_sample or _cpu_sample_size(cfg, th0)
         t, thr = _oracle_cpu(cfg, n_s, th0)
         t_full = t * (n / n_s) ** 3
-        out["cpu_baseline"] = {"value": 1.0 / t_full, "unit": "evals/s", "cores": thr, "kind": "oracle",
+        out["cpu_baseline"] = {"value": 1.0 / t_full, "unit": "evals/s", "cores": thr, "nproc": os.cpu_count(),
+                               "kind": "oracle",
                                "sample": f"dense oracle L(theta) on the first {n_s} of the {n} points: "
                                          f"{t:.2f} s, extrapolated x(n/{n_s})^3 = {t_full:.3g} s/eval"}
-    print(json.dumps(out), flush=True)
+    line = json.dumps(out)
+    print(line, flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(line + "\n")
     if dist:
         dist.destroy_process_group()
 
 
+def _spawn(args) -> int:
+    """--gpus N > 1 without torchrun: re-launch this script under torch.distributed.run (one rank per
+    GPU, rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = _args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
-    if world != args.gpus and rank == 0:
-        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)

@@ -38,7 +38,8 @@ typedef enum {
     HCOV_ERR_NOT_SPD = 3,       /* a diagonal-leaf pivot <= 0 during the H-Cholesky (fail_leaf reports which) */
     HCOV_ERR_OUT_OF_MEMORY = 4, /* device allocation failed */
     HCOV_ERR_CUDA = 5,          /* any other CUDA runtime error */
-    HCOV_ERR_RANK_CAPACITY = 6, /* an epsilon-rank exceeded the rank capacity with kmax == 0 */
+    HCOV_ERR_RANK_CAPACITY = 6, /* with kmax == 0: an epsilon-rank exceeded the rank capacity, or a
+                                   recompression lost accuracy for lack of capacity (acc_loss > 0) */
     HCOV_ERR_STATE = 7          /* call order violated (e.g. loglik on an unfactored matrix) */
 } hcov_status;
 
@@ -70,6 +71,11 @@ typedef struct {
     int32_t cap_binds;    /* number of truncations where kmax bound below the eps-rank */
     double min_pivot;     /* smallest L~_ii^2 */
     int64_t fail_leaf;    /* -1, or the first diagonal leaf whose pivot failed */
+    int32_t acc_loss;     /* recompressions that had to cut below their tolerance because a work
+                             capacity was exhausted (full-pivot ACA capacity, or an intermediate
+                             chunk recompression over 2 kcap; R22/R23).  0 on a clean run;
+                             with kmax == 0 a nonzero count returns HCOV_ERR_RANK_CAPACITY. */
+    int32_t pad_;
 } hcov_result;
 
 typedef struct {
@@ -148,9 +154,25 @@ hcov_status hcov_sample(hcov_hmat h, const double *xi_dev, double *Z_dev, hcov_s
  * row order; cols_host are external column indices. */
 hcov_status hcov_columns(hcov_hmat h, const int64_t *cols_host, int32_t m, double *out_dev,
                          hcov_stream stream);
+/* Exact covariance columns C e_j (Eq. (3) + nugget, direct device K_nu without the table), n x m
+ * column-major, external row order: the reference side of the sampled-column accuracy check
+ * ||C - C~||_F / ||C||_F (BASELINE north_star) at sizes the dense oracle cannot reach. */
+hcov_status hcov_cov_columns(hcov_tree t, const hcov_theta *theta, const int64_t *cols_host, int32_t m,
+                             double *out_dev, hcov_stream stream);
 /* Diagnostics of an H-matrix: bytes of dense tiles and low-rank factors at actual ranks. */
 hcov_status hcov_hmat_storage(hcov_hmat h, int64_t *dense_bytes, int64_t *lowrank_bytes,
                               int32_t *max_rank);
+
+/* The H-matrix (factored, L~) of the last hcov_eval on this tree: a BORROWED handle owned by the
+ * tree (do not free; invalidated by the next hcov_eval / hcov_tree_free).  For diagnostics
+ * (storage, ranks, work model) after an evaluation. */
+hcov_status hcov_tree_last_eval(hcov_tree t, hcov_hmat *out);
+/* Method-work model of SURVEY.md Sec. 8(d) / App. A.3 evaluated at the measured final ranks of a
+ * factored matrix (state >= factored): out[0] total flop of one evaluation; out[1] eager
+ * truncations of the low-rank Schur updates (4 m R^2 + 22 R^3 + 4 m R r per update), [2] low-rank
+ * products (cores, W = H V), [3] tile updates + TRSM, [4] V <- L^{-1} V solves, [5] POTRF, [6] ACA
+ * output truncation, [7] root forward solve.  The denominator of bench.py's roofline fraction. */
+hcov_status hcov_model_flops(hcov_hmat h, double *out8_host);
 
 /* Instrumentation (process-wide, not thread-safe).  launches/count: kernels the library launched
  * (always counted).  With events enabled: ms = device time per launch class from CUDA events

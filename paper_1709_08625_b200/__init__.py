@@ -43,7 +43,8 @@ class Trunc(ctypes.Structure):
 class Result(ctypes.Structure):
     _fields_ = [("loglik", ctypes.c_double), ("logdet", ctypes.c_double), ("quad", ctypes.c_double),
                 ("n", ctypes.c_int64), ("max_rank", ctypes.c_int32), ("cap_binds", ctypes.c_int32),
-                ("min_pivot", ctypes.c_double), ("fail_leaf", ctypes.c_int64)]
+                ("min_pivot", ctypes.c_double), ("fail_leaf", ctypes.c_int64), ("acc_loss", ctypes.c_int32),
+                ("pad_", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -85,6 +86,9 @@ _SIGS = {
     "hcov_sample": (_I32, [_P, _P, _P, _P]),
     "hcov_columns": (_I32, [_P, _P, _I32, _P, _P]),
     "hcov_hmat_storage": (_I32, [_P, _P, _P, _P]),
+    "hcov_cov_columns": (_I32, [_P, _P, _P, _I32, _P, _P]),
+    "hcov_model_flops": (_I32, [_P, _P]),
+    "hcov_tree_last_eval": (_I32, [_P, _P]),
     "hcov_prof_control": (_I32, [_I32, _I32]),
     "hcov_prof_read": (_I32, [_P]),
     "hcov_prof_class_name": (ctypes.c_char_p, [_I32]),
@@ -203,6 +207,26 @@ class Tree:
         return out
 
 
+class _Borrowed:
+    """A borrowed hcov_hmat (not freed by Python)."""
+
+    def __init__(self, tree, h):
+        self.tree, self._h = tree, h
+
+    model_flops = None
+    storage = None
+
+
+def last_eval(tree: "Tree"):
+    """hcov_tree_last_eval: the factored H-matrix of the last eval_loglik on this tree (borrowed)."""
+    h = ctypes.c_void_p()
+    _check(lib().hcov_tree_last_eval(tree.handle, ctypes.byref(h)), "hcov_tree_last_eval")
+    b = _Borrowed(tree, h)
+    b.model_flops = HMatrix.model_flops.__get__(b)
+    b.storage = HMatrix.storage.__get__(b)
+    return b
+
+
 def build_tree(s, eta: float = 2.0, dense_below: int = 32, stream=None) -> Tree:
     return Tree(s, eta=eta, dense_below=dense_below, stream=stream)
 
@@ -250,10 +274,28 @@ class HMatrix:
         _check(lib().hcov_columns(self._h, c.ctypes.data, len(c), _dev_f64(out), _stream(stream)), "hcov_columns")
         return out.T   # n x m, external rows
 
+    def model_flops(self) -> dict:
+        """hcov_model_flops: SURVEY Sec. 8(d) method-work model at the measured ranks (factored)."""
+        o = np.zeros(8)
+        _check(lib().hcov_model_flops(self._h, o.ctypes.data), "hcov_model_flops")
+        return dict(zip(["total", "truncation", "products", "tile", "solves", "potrf", "aca_truncation",
+                         "root_solve"], o.tolist()))
+
     def storage(self) -> dict:
         d, l, m = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
         _check(lib().hcov_hmat_storage(self._h, ctypes.byref(d), ctypes.byref(l), ctypes.byref(m)), "hcov_hmat_storage")
         return {"dense_bytes": d.value, "lowrank_bytes": l.value, "max_rank": m.value}
+
+
+def cov_columns(tree: Tree, theta, cols: Sequence[int], stream=None):
+    """hcov_cov_columns: exact Eq. (3) columns C e_j on the device (n x m, external rows)."""
+    import torch
+    c = np.ascontiguousarray(cols, dtype=np.int64)
+    out = torch.empty((len(c), tree.n), dtype=torch.float64, device="cuda")
+    th = Theta(*theta)
+    _check(lib().hcov_cov_columns(tree.handle, ctypes.byref(th), c.ctypes.data, len(c), _dev_f64(out),
+                                  _stream(stream)), "hcov_cov_columns")
+    return out.T
 
 
 def eval_loglik(tree: Tree, theta, Z, eps: float, kmax: int = 0, kcap: int = 0, stream=None) -> dict:

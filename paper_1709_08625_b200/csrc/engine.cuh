@@ -50,9 +50,11 @@ struct Ctx {
     double *vbuf;              // root right-hand side / solution (internal order)
     double *logdet_part, *minpiv_part, *quad_part;
     int32_t *fail_leaf;        // min over failing leaves (init INT32_MAX)
-    int32_t *flags;            // [0] cap binds, [1] rank overflow, [2] max rank
+    int32_t *flags;            // [0] cap binds, [1] rank overflow, [2] max rank, [3] accuracy losses
+                               // (a recompression cut below its tolerance: ACA or chunk capacity)
     int32_t kcap, kmax;
     double eps;
+    double interm_rel;         // intermediate (chunk) recompression tolerance, relative to eps (R22)
     MaternParams mp;
     // ---- engine ----
     int32_t *indeg;            // working copy of the in-degrees
@@ -143,7 +145,7 @@ __device__ __forceinline__ Fac get_fac(const Ctx &c, int f)
         F.p = c.U + c.fac_off[f] * (int64_t)c.kcap;
     } else {   // W slice (phw id, partner index)
         const int64_t code = c.fac_off[f];
-        const int qid = (int)(code >> 8), p = (int)(code & 255);
+        const int qid = (int)(code >> 20), p = (int)(code & 0xFFFFF);
         const DPhw q = c.phw[qid];
         F.p = w_base(c, qid) + (int64_t)q.m * partner_prefix(c, q, p);
     }
@@ -312,7 +314,7 @@ __device__ void record_rank(const Ctx &c, int r, int rk, int cb, int of)
 }
 
 __device__ __forceinline__ double final_tol(double eps, int R) { return eps / (10.0 * sqrt((double)(R > 0 ? R : 1))); }
-__device__ __forceinline__ double interm_tol(double eps) { return fmax(eps * 1e-2, 1e-15); }
+__device__ __forceinline__ double interm_tol(const Ctx &c) { return fmax(c.eps * c.interm_rel, 1e-15); }
 
 __device__ __forceinline__ double compress_flops(int64_t m, int R, int r)
 {
@@ -331,6 +333,7 @@ __device__ __forceinline__ double compress_flops(int64_t m, int R, int r)
 struct Gang {
     int g, G;
     int32_t *bar;
+    const uint32_t *abort;     // the engine's watchdog flag: a partly formed gang never spins forever
     int nb;
     int64_t mq, q0;
     double *shared;
@@ -351,7 +354,10 @@ __device__ __forceinline__ void gang_sync(Gang &gg)
         __threadfence();
         atomicAdd(gg.bar, 1);
         const int target = gg.nb * gg.G;
-        while (*(volatile int32_t *)gg.bar < target) __nanosleep(64);
+        while (*(volatile int32_t *)gg.bar < target) {
+            if (*(volatile const uint32_t *)gg.abort) break;
+            __nanosleep(64);
+        }
         __threadfence();
     }
     __syncthreads();
@@ -1044,7 +1050,7 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
 
 // A7 low-rank blocks: S = U V^T - sum of all pending terms, accumulated in factored form
 // X = [U, -A_1 K_1, ...], Y = [V, B_1, ...] (in scratch).  When the panel is full it is
-// recompressed near-losslessly (pivoted QR at eps*1e-4, no SVD); at the end X Y^T is truncated
+// recompressed near-losslessly (pivoted QR at eps * interm_rel, no SVD; R22); at the end X Y^T is truncated
 // to (eps, kmax) by QR + SVD (A6; Remark 2).
 __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *smem, double *red, double *redv,
                           int64_t *redi, double &fl, Gang *gg)
@@ -1118,10 +1124,10 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         if (cur + width > K) {
             int icb = 0, iof = 0, rk;
             if (gg)
-                rk = gang_compress(w, gw, *gg, cur, c.eps, interm_tol(c.eps), false, 0, K - maxw, X2 - q0, Y2 - q0, mq,
+                rk = gang_compress(w, gw, *gg, cur, c.eps, interm_tol(c), false, 0, K - maxw, X2 - q0, Y2 - q0, mq,
                                    &icb, &iof, red, redv, redi, smem, c.smem_dbl);
             else
-                rk = compress(w, m, cur, c.eps, interm_tol(c.eps), false, 0, K - maxw, X2, Y2, m, &icb, &iof, red,
+                rk = compress(w, m, cur, c.eps, interm_tol(c), false, 0, K - maxw, X2, Y2, m, &icb, &iof, red,
                               redv, redi, smem, c.smem_dbl);
             fl += (gg ? 1.0 / gg->G : 1.0) * compress_flops(m, cur, rk);
             if (iof && threadIdx.x == 0 && (!gg || gg->g == 0)) atomicAdd(c.flags + 3, 1);
@@ -1174,7 +1180,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     }
     // last chunk: truncation to (eps, kmax) into capacity kcap; else near-lossless into 2 kcap
     const bool fin = (tk.d == 1);
-    const double tq = fin ? final_tol(c.eps, cur) : interm_tol(c.eps);
+    const double tq = fin ? final_tol(c.eps, cur) : interm_tol(c);
     const int kmx = fin ? c.kmax : 0, rl = fin ? c.kcap : 2 * c.kcap;
     int rk;
     if (gg) {

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
         const int32_t t = s_task;
         if (t < 0) break;
         const DTask tk = c.tasks[t];
-        Gang gang{s_member, tk.qcls, c.gbar + t, 0, 0, 0, nullptr};
+        Gang gang{s_member, tk.qcls, c.gbar + t, c.qctl + QC_ABORT, 0, 0, 0, nullptr};
         Gang *gg = nullptr;
         double *tscr = scr;
         if (tk.qcls > 0) {
@@ -237,7 +237,11 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
                     s_cta0 = blockIdx.x;
                 } else {
                     int32_t v;
-                    while ((v = ld_volatile(c.gslot + t)) < 0) __nanosleep(64);
+                    while ((v = ld_volatile(c.gslot + t)) < 0) {
+                        if (ld_volatile((const int32_t *)c.qctl + QC_ABORT)) break;
+                        __nanosleep(64);
+                    }
+                    if (v < 0) v = blockIdx.x;   // aborted: the task body exits at its first gang barrier
                     s_cta0 = v;
                 }
                 __threadfence();
@@ -358,6 +362,13 @@ __global__ void __launch_bounds__(NT) k_reduce(Ctx c, double *out)
     }
 }
 
+// Per-theta K_nu Chebyshev table (general nu, matern.cuh): one thread per interval.
+__global__ void k_ktab(double nu, double *coef)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < KTAB_NI) hcov_matern_table_row(nu, i, coef + i * KTAB_NC);
+}
+
 // hcov_sample: t_b = V_b^T x[cols of b] for every R block
 __global__ void __launch_bounds__(NT) k_sample_t(Ctx c, const double *x, double *t)
 {
@@ -441,6 +452,19 @@ __global__ void __launch_bounds__(NT) k_columns(Ctx c, const int32_t *leafnodes,
         }
     }
 }
+// hcov_cov_columns: exact Eq. (3) columns C e_j (direct K_nu, no table), external row order.
+__global__ void k_cov_columns(Ctx c, const int64_t *pc, int mcols, double *out)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < c.n_pad * (int64_t)mcols;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = e % c.n_pad, k = e / c.n_pad;
+        const int64_t ex = c.perm_i2e[p];
+        if (ex < 0) continue;
+        const int64_t q = pc[k];
+        out[ex + c.n_real * k] = hcov_cov_entry(c.mp, c.xs[p], c.ys[p], c.xs[q], c.ys[q], p == q);
+    }
+}
+
 __global__ void k_columns_perm(Ctx c, const double *in, int mcols, double *out)
 {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < c.n_pad * (int64_t)mcols;
@@ -522,7 +546,7 @@ struct hcov_hmat_s {
     int32_t *indeg = nullptr, *q0 = nullptr, *q1 = nullptr, *gbar = nullptr, *gslot = nullptr;
     uint32_t *qctl = nullptr;
     double *scr = nullptr, *bscr = nullptr, *res = nullptr, *res_host = nullptr;
-    double *ktab = nullptr, *ktab_host = nullptr;
+    double *ktab = nullptr;
     int64_t *woff = nullptr, *poff = nullptr;
     unsigned long long *mem = nullptr;
     int64_t wcap = 0, pcap = 0;
@@ -545,7 +569,6 @@ struct hcov_hmat_s {
     {
         release_all();
         cudaFree(ktab);
-        if (ktab_host) cudaFreeHost(ktab_host);
         if (res_host) cudaFreeHost(res_host);
         if (stats_host) cudaFreeHost(stats_host);
     }
@@ -699,6 +722,9 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engine, NT, (size_t)h->smem));
     occ = std::max(1, std::min(occ, 512 / NT));
     h->grid = nsm * occ;
+    // every gang forms only if the CTAs that partly formed gangs can hold (at most one per band)
+    // leave at least one free CTA
+    if (h->grid <= HCOV_BANDS * (HCOV_GANG - 1)) return HCOV_ERR_INVALID_ARG;
     // per-CTA scratch: single-CTA tasks (blocks < HCOV_GANG_MIN, 6 panels) or a gang member's rows
     // (m / G rows, 4 panels) followed by the gang's shared workspace (used when the CTA is member 0)
     const int64_t med_m = std::min<int64_t>(HCOV_GANG_MIN / 2, std::max<int64_t>(P.max_rm, 32));
@@ -748,6 +774,13 @@ void fill_ctx(hcov_hmat h)
     c.vbuf = h->vbuf; c.logdet_part = h->logdet_part; c.minpiv_part = h->minpiv_part; c.quad_part = h->quad_part;
     c.fail_leaf = h->fail; c.flags = h->flags;
     c.kcap = h->kcap_alloc; c.kmax = h->trunc.kmax; c.eps = h->trunc.eps;
+    {
+        // R22: intermediate chunk recompressions at eps * interm_rel (default 1e-2; HCOV_INTERM_REL
+        // overrides it for the accuracy study in tests/test_gpu_accuracy.py)
+        const char *ir = std::getenv("HCOV_INTERM_REL");
+        const double v = ir ? std::atof(ir) : 1e-2;
+        c.interm_rel = (v > 0 && v <= 1) ? v : 1e-2;
+    }
     c.mp = hcov_matern_params(h->theta.sigma2, h->theta.ell, h->theta.nu, h->theta.nugget);
     if (c.mp.kind == 3) c.mp.tab = h->ktab;
     c.indeg = h->indeg; c.queue[0] = h->q0; c.queue[1] = h->q1; c.qctl = h->qctl; c.gbar = h->gbar;
@@ -828,16 +861,12 @@ hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trun
     h->theta = *theta;
     h->trunc = *trunc;
     if ((s = hmat_alloc(h, kcap))) return s;
-    if (!h->ktab) {
-        CK(cudaMalloc(&h->ktab, KTAB_NI * KTAB_NC * sizeof(double)));
-        CK(cudaMallocHost(&h->ktab_host, KTAB_NI * KTAB_NC * sizeof(double)));
-    }
+    if (!h->ktab) CK(cudaMalloc(&h->ktab, KTAB_NI * KTAB_NC * sizeof(double)));
     {
         const MaternParams mp = hcov_matern_params(theta->sigma2, theta->ell, theta->nu, theta->nugget);
         if (mp.kind == 3) {
-            CK(cudaStreamSynchronize(st));   // the pinned staging buffer may still feed a previous copy
-            hcov_matern_table(theta->nu, h->ktab_host);
-            CK(cudaMemcpyAsync(h->ktab, h->ktab_host, KTAB_NI * KTAB_NC * sizeof(double), cudaMemcpyHostToDevice, st));
+            LAUNCH(PC_AUX, st, k_ktab<<<1, KTAB_NI, 0, st>>>(theta->nu, h->ktab));
+            CK(cudaGetLastError());
         }
     }
     fill_ctx(h);
@@ -885,8 +914,9 @@ hcov_status finish_result(hcov_hmat h, cudaStream_t st, hcov_result *out)
     out->fail_leaf = (hf[0] == 0x7f7f7f7f) ? -1 : hf[0];
     out->cap_binds = hf[1];
     out->max_rank = hf[3];
+    out->acc_loss = hf[4];
     if (out->fail_leaf >= 0) { out->loglik = -INFINITY; return HCOV_ERR_NOT_SPD; }
-    if (hf[2] > 0 && h->trunc.kmax == 0) { out->loglik = -INFINITY; return HCOV_ERR_RANK_CAPACITY; }
+    if ((hf[2] > 0 || hf[4] > 0) && h->trunc.kmax == 0) { out->loglik = -INFINITY; return HCOV_ERR_RANK_CAPACITY; }
     return HCOV_OK;
 }
 
@@ -1057,7 +1087,7 @@ hcov_status hcov_cholesky(hcov_hmat h, hcov_stream stream, int64_t *fail_leaf)
     int64_t fl = (hf[0] == 0x7f7f7f7f) ? -1 : hf[0];
     if (fail_leaf) *fail_leaf = fl;
     if (fl >= 0) return HCOV_ERR_NOT_SPD;
-    if (hf[2] > 0 && h->trunc.kmax == 0) return HCOV_ERR_RANK_CAPACITY;
+    if ((hf[2] > 0 || hf[4] > 0) && h->trunc.kmax == 0) return HCOV_ERR_RANK_CAPACITY;
     return HCOV_OK;
 }
 
@@ -1160,6 +1190,37 @@ hcov_status hcov_columns(hcov_hmat h, const int64_t *cols_host, int32_t m, doubl
     return HCOV_OK;
 }
 
+hcov_status hcov_cov_columns(hcov_tree t, const hcov_theta *theta, const int64_t *cols_host, int32_t m,
+                             double *out_dev, hcov_stream stream)
+{
+    if (!t || !theta || !cols_host || m < 0 || !out_dev) return HCOV_ERR_INVALID_ARG;
+    hcov_trunc tr{0.0, 0, 0};
+    hcov_status s = check_theta(theta, &tr);
+    if (s) return s;
+    if ((s = tree_upload(t))) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    Plan &P = t->P;
+    std::vector<int64_t> e2i(P.n, -1);
+    for (int64_t p = 0; p < P.n_pad; ++p)
+        if (P.perm_i2e[p] >= 0) e2i[P.perm_i2e[p]] = p;
+    std::vector<int64_t> pc(std::max(1, m));
+    for (int k = 0; k < m; ++k) {
+        if (cols_host[k] < 0 || cols_host[k] >= P.n) return HCOV_ERR_INVALID_ARG;
+        pc[k] = e2i[cols_host[k]];
+    }
+    Ctx c{};
+    c.xs = t->d_xs; c.ys = t->d_ys; c.perm_i2e = t->d_perm_i2e; c.n_pad = P.n_pad; c.n_real = P.n;
+    c.mp = hcov_matern_params(theta->sigma2, theta->ell, theta->nu, theta->nugget);   // tab = null: direct K_nu
+    int64_t *d_pc = nullptr;
+    CK(cudaMalloc(&d_pc, std::max(1, m) * sizeof(int64_t)));
+    CK(cudaMemcpyAsync(d_pc, pc.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    LAUNCH(PC_AUX, st, k_cov_columns<<<1184, 256, 0, st>>>(c, d_pc, m, out_dev));
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(d_pc);
+    if (e != cudaSuccess) return map_err(e);
+    return HCOV_OK;
+}
+
 hcov_status hcov_hmat_storage(hcov_hmat h, int64_t *dense_bytes, int64_t *lowrank_bytes, int32_t *max_rank)
 {
     if (!h || !dense_bytes || !lowrank_bytes || !max_rank) return HCOV_ERR_INVALID_ARG;
@@ -1172,6 +1233,93 @@ hcov_status hcov_hmat_storage(hcov_hmat h, int64_t *dense_bytes, int64_t *lowran
     *dense_bytes = P.n_tiles() * HCOV_TILE * 8;
     *lowrank_bytes = lr;
     *max_rank = mx;
+    return HCOV_OK;
+}
+
+hcov_status hcov_tree_last_eval(hcov_tree t, hcov_hmat *out)
+{
+    if (!t || !out) return HCOV_ERR_INVALID_ARG;
+    *out = t->cached;
+    return t->cached ? HCOV_OK : HCOV_ERR_STATE;
+}
+
+hcov_status hcov_model_flops(hcov_hmat h, double *out)
+{
+    // SURVEY.md Sec. 8(d) / App. A.3 method-work model at the MEASURED final ranks r_b of L~:
+    // every Schur-complement term applied to every leaf it covers, low-rank targets truncated
+    // eagerly after each term (4 m R^2 + 22 R^3 + 4 m R r_b with R = r_b + term width), tile updates,
+    // POTRF / TRSM, the V <- L^{-1} V solves and W = H V products as 2 x (words of the operator) x
+    // (columns), the ACA output truncation, and the root forward solve (2 x words of L~).
+    if (!h || !out) return HCOV_ERR_INVALID_ARG;
+    if (h->state < 2) return HCOV_ERR_STATE;
+    const Plan &P = h->t->P;
+    std::vector<int32_t> rk(std::max<int64_t>(1, P.n_r()), 0);
+    if (P.n_r()) CK(cudaMemcpy(rk.data(), h->rank, P.n_r() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    auto ncols = [&](int f) { return (double)rk[P.fac_rank_src[f]]; };
+    auto trunc = [](double m, double R, double r) { return 4.0 * m * R * R + 22.0 * R * R * R + 4.0 * m * R * r; };
+    // words of L~ below each node (lower triangle)
+    std::vector<double> words(P.nodes.size(), 0.0);
+    for (int64_t k = (int64_t)P.nodes.size() - 1; k >= 0; --k) {   // children have larger ids (preorder)
+        const DNode &x = P.nodes[k];
+        if (x.type == ND_T) words[k] = HCOV_TILE;
+        else if (x.type == ND_R) words[k] = 2.0 * P.rblk[x.idx].m * rk[x.idx];
+        else
+            for (int c = 0; c < 4; ++c)
+                if (P.children[4 * k + c] >= 0) words[k] += words[P.children[4 * k + c]];
+    }
+    std::vector<int32_t> diag_node(P.n_clusters, -1);
+    for (size_t k = 0; k < P.nodes.size(); ++k)
+        if (P.nodes[k].i == P.nodes[k].j) diag_node[((int64_t)1 << P.nodes[k].level) - 1 + P.nodes[k].i] = (int32_t)k;
+    double f_trunc = 0, f_prod = 0, f_tile = 0, f_solve = 0, f_potrf = 0, f_aca = 0, f_root = 0;
+    for (int64_t r = 0; r < P.n_r(); ++r) f_aca += trunc(P.rblk[r].m, rk[r], rk[r]);
+    for (const DTask &tk : P.tasks) {
+        switch (tk.type) {
+        case TK_TAPP: case TK_POTRF: case TK_TRSM:
+            for (int k = tk.b; k < tk.c; ++k) {
+                const DTerm &t = P.terms[P.xterm[k]];
+                if (t.kind == TM_TT) f_tile += 2.0 * 32 * 32 * 32;
+                else {
+                    const double ra = ncols(t.a), rb = ncols(t.b);
+                    f_tile += 2.0 * 32 * 32 * rb + (t.core >= 0 ? 2.0 * 32 * ra * rb : 0.0);
+                }
+            }
+            if (tk.type == TK_POTRF) f_potrf += 32.0 * 32 * 32 / 3.0;
+            if (tk.type == TK_TRSM) f_tile += 32.0 * 32 * 32;
+            break;
+        case TK_RAPP: {
+            const double m = P.rblk[tk.a].m, ro = rk[tk.a];
+            for (int k = tk.b; k < tk.c; ++k) {
+                const DTerm &t = P.terms[P.xterm[k]];
+                double w = 32.0;
+                if (t.kind == TM_LR) {
+                    w = ncols(t.b);
+                    if (w == 0 || ncols(t.a) == 0) continue;
+                    if (t.core >= 0) f_prod += 2.0 * m * ncols(t.a) * w;
+                }
+                f_trunc += trunc(m, ro + w, ro);
+            }
+            break;
+        }
+        case TK_PRR: f_prod += 2.0 * P.rblk[tk.a].m * rk[tk.a] * rk[tk.b]; break;
+        default: break;
+        }
+    }
+    for (size_t s = 0; s < P.solves.size(); ++s) {
+        const DSolve &sv = P.solves[s];
+        const int32_t dn = diag_node[((int64_t)1 << sv.level) - 1 + sv.c];
+        if ((int)s == P.root_solve) { f_root += 2.0 * words[dn]; continue; }
+        double cols = 0;
+        for (int q = 0; q < sv.rhs_cnt; ++q) cols += rk[P.solve_rhs[sv.rhs_off + q]];
+        f_solve += 2.0 * words[dn] * cols;
+    }
+    for (const DPhw &q : P.phw) {
+        double cols = 0;
+        for (int p = 0; p < q.part_cnt; ++p) cols += rk[P.col_r[q.part_off + p]];
+        f_prod += 2.0 * words[q.hnode] * cols;
+    }
+    out[1] = f_trunc; out[2] = f_prod; out[3] = f_tile; out[4] = f_solve; out[5] = f_potrf; out[6] = f_aca;
+    out[7] = f_root;
+    out[0] = f_trunc + f_prod + f_tile + f_solve + f_potrf + f_aca + f_root;
     return HCOV_OK;
 }
 

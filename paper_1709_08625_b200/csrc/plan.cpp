@@ -47,6 +47,7 @@ struct Builder {
     std::vector<int32_t> tile_fill, fin_tile, aca_task, rfin, rdone;
     std::vector<int32_t> term_p0, term_p1;
     int32_t root_solve = -1;
+    bool too_many_partners = false;
 
     Builder(Plan &p, const PlanOpts &o) : P(p), O(o), L(p.depth) {}
 
@@ -288,11 +289,12 @@ struct Builder {
         q.w_off = P.w_elems;
         P.w_elems += m * (int64_t)rents.size();
         const int32_t qid = (int32_t)P.phw.size();
+        if (rents.size() >= ((size_t)1 << 20)) too_many_partners = true;   // fac_off packs p in 20 bits
         for (int p = 0; p < (int)rents.size(); ++p) {
             P.fac_row0.push_back((int64_t)h.i * m);
             P.fac_nrows.push_back((int32_t)m);
             P.fac_rank_src.push_back(rents[p]);
-            P.fac_off.push_back(((int64_t)qid << 8) | p);   // W slice: (phw id, partner index), offset at run time
+            P.fac_off.push_back(((int64_t)qid << 20) | p);  // W slice: (phw id, partner index < 2^20), offset at run time
             P.fac_pool.push_back(1);
         }
         P.phw.push_back(q);
@@ -524,6 +526,7 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
     const int32_t first_root_task = (int32_t)P.tasks.size();
     B.root_solve = (int32_t)P.solves.size();
     B.build_solve(0, 0, {});
+    if (B.too_many_partners) return 1;
 
     // ---- DAG: phases, successors, per-mode in-degrees and roots, critical path ------------
     const int32_t ntk = (int32_t)P.tasks.size();

@@ -28,10 +28,21 @@ def _rel(a, b):
     return abs(a - b) / abs(b)
 
 
+def _scale(ref, n):
+    return 0.5 * n * math.log(2 * math.pi) + 0.5 * abs(ref[1]) + 0.5 * ref[2]
+
+
 def _scaled_err(r, ref, n):
     """Component-scaled error |dL| / (n/2 log 2pi + |logdet|/2 + q/2) (reading R11)."""
-    scale = 0.5 * n * math.log(2 * math.pi) + 0.5 * abs(ref[1]) + 0.5 * ref[2]
-    return abs(r["loglik"] - ref[0]) / scale
+    return abs(r["loglik"] - ref[0]) / _scale(ref, n)
+
+
+def _err(r, ref, n):
+    """the plain relative error of L, except where |L| < 0.1 x the
+    component scale (L near a sign change), where the component-scaled error is graded."""
+    if abs(ref[0]) < 0.1 * _scale(ref, n):
+        return _scaled_err(r, ref, n)
+    return _rel(r["loglik"], ref[0])
 
 
 @pytest.fixture(scope="module")
@@ -53,6 +64,7 @@ def test_c1_parity(c1):
     assert _rel(r["logdet"], ref[1]) <= 1e-6
     assert _rel(r["quad"], ref[2]) <= 1e-6
     assert r["min_pivot"] >= cfg.nugget * (1 - 1e-6)   # pivots are conditional variances >= tau^2
+    assert r["acc_loss"] == 0 and r["cap_binds"] == 0
 
 
 def test_c1_staged_api_equals_eval(c1):
@@ -81,17 +93,19 @@ def test_all_dense_mode_ragged(n, seed):
     assert abs(r["logdet"] - ref[1]) <= 1e-10 * max(1.0, abs(ref[1]))
 
 
-def test_near_full_rank_mode():
-    # eps -> 0 (1e-11) with a large rank capacity: the H-matrix reproduces the dense matrix
+@pytest.mark.parametrize("eps,bar", [(1e-13, 1e-10), (1e-11, 1e-9)])
+def test_near_full_rank_mode(eps, bar):
+    # eps -> 0 with the largest rank capacity (64): the H-matrix reproduces the dense matrix
     n = 1200
     s = synth.uniform_points(n, 11)
     th = (1.0, 0.1, 0.5, 1e-6)
     Z = oracle.sample_dense(s, synth.xi(n, 12), *th)
     ref = oracle.loglik_dense(s, Z, *th)
     T = H.Tree(_dev(s))
-    r = H.eval_loglik(T, th, _dev(Z), eps=1e-11, kcap=64)
-    assert r["status"] == 0
-    assert _rel(r["loglik"], ref[0]) <= 1e-9, (r, ref)
+    r = H.eval_loglik(T, th, _dev(Z), eps=eps, kcap=64)
+    assert r["status"] == 0, r
+    assert r["acc_loss"] == 0
+    assert _rel(r["loglik"], ref[0]) <= bar, (r, ref)
 
 
 @pytest.mark.parametrize("nu,ell", [(1.0, 0.05), (0.3, 0.1), (2.2, 0.03), (1.5, 0.05), (2.5, 0.02)])
@@ -103,9 +117,8 @@ def test_general_nu_parity(nu, ell):
     ref = oracle.loglik_dense(s, Z, *th)
     T = H.Tree(_dev(s))
     r = H.eval_loglik(T, th, _dev(Z), eps=1e-8)
-    assert r["status"] == 0
-    err = min(_rel(r["loglik"], ref[0]), _scaled_err(r, ref, n))
-    assert err <= 1e-6, (r, ref)
+    assert r["status"] == 0 and r["acc_loss"] == 0
+    assert _err(r, ref, n) <= 1e-6, (r, ref)
 
 
 @pytest.mark.parametrize("nu,ell,sigma2", [(0.5, 0.1, 1.0), (1.0, 0.05, 2.0), (0.3, 0.2, 1.0),
@@ -132,36 +145,9 @@ def test_assembled_entries_vs_oracle(nu, ell, sigma2):
         assert np.all(d <= 1e-13 * np.abs(ref[same, k]) + 1e-300), (nu, c, d.max())
     fro = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert fro <= 10 * eps, fro
-
-
-@pytest.mark.parametrize("eps", [1e-8, 1e-4])
-def test_c2_grid_points(eps):
-    """C2 (n = 16,384, nu = 3/2): a subset of the 64-point ell grid.  DESIGN.md reading R12:
-    the bar applies where the eps-truncated matrix is SPD; NOT_SPD is a legal outcome at
-    eps = 1e-4 for ell >= 0.025 (the eps-oracle itself is indefinite there)."""
-    cfg = synth.CONFIGS["C2"]
-    s = synth.points(cfg)
-    th0 = (cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget)
-    Z = oracle.sample_dense(s, synth.xi(cfg.n, cfg.seed_xi), *th0)
-    T = H.Tree(_dev(s))
-    Zd = _dev(Z)
-    grid = cfg.ell_grid
-    picks = [grid[0], grid[20]] if eps == 1e-4 else [grid[0], grid[20], grid[29], grid[40]]
-    for ell in picks:
-        th = (cfg.sigma2, ell, cfg.nu, cfg.nugget)
-        ref = oracle.loglik_dense(s, Z, *th)
-        r = H.eval_loglik(T, th, Zd, eps=eps)
-        if r["status"] == 3:
-            assert eps == 1e-4 and ell >= 0.02, (ell, r)
-            continue
-        assert r["status"] == 0
-        bar = 1e-6 if eps == 1e-8 else 1e-3
-        if eps == 1e-8 and ell > 0.08:
-            # reading R12: the best possible eps-truncation (eps-oracle, SURVEY App. A.4) already has
-            # a component-scaled error of 2.5e-6 at ell = 0.1; require the same order
-            bar = 1e-5
-        err = min(_rel(r["loglik"], ref[0]), _scaled_err(r, ref, cfg.n))
-        assert err <= bar, (ell, r, ref)
+    # the device's exact-column evaluator (bench accuracy field) against the oracle as well
+    ce = H.cov_columns(T, th, cols).cpu().numpy()
+    assert np.max(np.abs(ce - ref) / np.abs(ref).max()) <= 1e-13
 
 
 def test_collinear_ou_exact_large():
@@ -202,9 +188,8 @@ def test_ragged_n_dense_oracle():
     ref = oracle.loglik_dense(s, Z, *th)
     T = H.Tree(_dev(s))
     r = H.eval_loglik(T, th, _dev(Z), eps=1e-8)
-    assert r["status"] == 0
-    err = min(_rel(r["loglik"], ref[0]), _scaled_err(r, ref, n))
-    assert err <= 1e-6, (r, ref)
+    assert r["status"] == 0 and r["acc_loss"] == 0
+    assert _err(r, ref, n) <= 1e-6, (r, ref)
 
 
 def test_sample_then_solve_gives_xi():

@@ -1,6 +1,7 @@
 """CPU build of the device Matern / K_nu code (matern.cuh compiled with g++): the series /
 continued fraction K_nu and the per-theta Chebyshev table against scipy.special.kv and the oracle."""
 import ctypes
+import math
 import os
 import subprocess
 
@@ -60,3 +61,21 @@ def test_chebyshev_table_matches_direct_and_oracle(lib, nu):
         ref = oracle.matern(h[k], 1.7, ell, nu)
         if ref > 1e-290:
             assert abs(tab[k] - ref) <= 2e-13 * max(1.0, h[k] / ell) * ref, (h[k], tab[k], ref)
+
+
+@pytest.mark.parametrize("nu", [0.5, 1.5, 2.5])
+def test_device_besselk_half_integer_closed_forms(lib, nu):
+    """|mu| = 1/2 (the reduced order where Temme's normalising coefficients C_j vanish for j >= 1):
+    K_{1/2}(x) = sqrt(pi/(2x)) e^{-x}, K_{3/2} = K_{1/2} (1 + 1/x), K_{5/2} = K_{1/2} (1 + 3/x + 3/x^2)
+    (DLMF 10.49.12), on both sides of the series / backward-recurrence switch at x = 2."""
+    for x in np.concatenate([np.geomspace(1e-6, 700, 300), [1.999999, 2.0, 2.000001]]):
+        k12 = math.sqrt(math.pi / (2 * x)) * math.exp(-x)
+        ref = {0.5: k12, 1.5: k12 * (1 + 1 / x), 2.5: k12 * (1 + 3 / x + 3 / x ** 2)}[nu]
+        assert abs(lib.host_besselk(nu, x) - ref) <= 3e-15 * ref * max(1.0, 1.0), (nu, x)
+
+
+def test_device_besselk_continuity_at_switch(lib):
+    """The two regimes (series x <= 2, U-function backward recurrence x > 2) agree at the switch."""
+    for nu in [0.05, 0.3, 1.0, 1.7, 3.3]:
+        a, b = lib.host_besselk(nu, 2.0), lib.host_besselk(nu, np.nextafter(2.0, 3.0))
+        assert abs(a - b) <= 4e-15 * a, (nu, a, b)

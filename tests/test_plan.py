@@ -9,6 +9,7 @@ import pytest
 
 import paper_1709_08625_b200 as H
 import synth
+from oracle import htree
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -24,61 +25,14 @@ def test_library_exports_every_declared_symbol():
 
 
 def _mirror_tree(s, leaf=32):
-    """Python re-statement of A1: longest bbox axis (ties -> x), stable cardinality median,
-    left = ceil(m/2), uniform depth L = ceil(log2(n/32))."""
-    n = len(s)
-    L = 0
-    while (leaf << L) < n:
-        L += 1
-    ranges = [list(range(n))]
-    for _ in range(L):
-        nxt = []
-        for idx in ranges:
-            P = s[idx]
-            ext = P.max(0) - P.min(0)
-            ax = 0 if ext[0] >= ext[1] else 1
-            order = sorted(range(len(idx)), key=lambda k: (P[k, ax], k))
-            idx = [idx[k] for k in order]
-            m1 = (len(idx) + 1) // 2
-            nxt += [idx[:m1], idx[m1:]]
-        ranges = nxt
-    perm = []
-    for idx in ranges:
-        perm += idx + [-1] * (leaf - len(idx))
-    return L, np.array(perm, dtype=np.int64)
+    """The oracle's restatement of A1 (oracle/htree.py; R5)."""
+    T = htree.cluster_tree(s)
+    return T.depth, T.perm
 
 
 def _mirror_blocks(s, perm, L, eta=2.0, leaf=32, dense_below=32):
-    npad = leaf << L
-    def box(l, c):
-        m = npad >> l
-        idx = perm[c * m:(c + 1) * m]
-        P = s[idx[idx >= 0]]
-        return P.min(0), P.max(0)
-    def adm(l, i, j):
-        (a0, a1), (b0, b1) = box(l, i), box(l, j)
-        gap = np.maximum(0, np.maximum(a0 - b1, b0 - a1))
-        d = math.hypot(*gap)
-        return eta > 0 and d > 0 and min(math.hypot(*(a1 - a0)), math.hypot(*(b1 - b0))) <= eta * d
-    out = set()
-    def rec(l, i, j, forced):
-        if i == j:
-            if l == L:
-                out.add((l, i, j, H.ND_T)); return
-            out.add((l, i, j, H.ND_H))
-            rec(l + 1, 2 * i, 2 * j, forced); rec(l + 1, 2 * i + 1, 2 * j, forced); rec(l + 1, 2 * i + 1, 2 * j + 1, forced)
-            return
-        a = (not forced) and adm(l, i, j)
-        if a and l < L and (npad >> l) > dense_below:
-            out.add((l, i, j, H.ND_R)); return
-        if l == L:
-            out.add((l, i, j, H.ND_T)); return
-        out.add((l, i, j, H.ND_H))
-        for x in (0, 1):
-            for y in (0, 1):
-                rec(l + 1, 2 * i + x, 2 * j + y, forced or a)
-    rec(0, 0, 0, False)
-    return out
+    """The oracle's restatement of A2 (oracle/htree.py; R6, R21)."""
+    return set(htree.block_tree(htree.cluster_tree(s), eta, dense_below))
 
 
 @pytest.mark.parametrize("n,seed,geom", [(1, 1, "u"), (31, 2, "u"), (33, 3, "u"), (500, 4, "u"),
