@@ -219,12 +219,23 @@ def run_hcov(args, cfg, rank: int, world: int):
     info = tree.info()
     # data: Z = L~_gen xi from a TIGHTER H-Cholesky factor than the one
     # evaluated (eps_gen = 1e-8, same rank cap), so v = L~^{-1} Z is not xi by construction
-    eps_gen = min(1e-8, eps)
+    # (row 15: 1e-8, "if memory forbids, 1e-7"; the first of these that fits the device is used)
     xi = torch.from_numpy(synth.xi(n, cfg.seed_xi)).to(dev)
-    hgen = H.HMatrix(tree, th0, eps_gen, kmax)
-    hgen.cholesky()
-    Z = hgen.sample(xi)
-    del hgen
+    Z, eps_gen = None, None
+    for eg in sorted({min(1e-8, eps), min(1e-7, eps), min(3e-7, eps)}):
+        try:
+            hgen = H.HMatrix(tree, th0, eg, kmax)
+            hgen.cholesky()
+            Z = hgen.sample(xi)
+            eps_gen = eg
+            del hgen
+            break
+        except H.HcovError as e:
+            hgen = None
+            if e.code != 4:      # only "out of device memory" moves to the next eps_gen
+                raise
+    if Z is None:
+        raise RuntimeError("could not generate Z")
     m_total = max(1, world)
     my_theta = th0 if m_total == 1 else (th0[0], th0[1] * 0.8 * (1.25 / 0.8) ** (rank / (m_total - 1)), th0[2], th0[3])
 

@@ -111,7 +111,8 @@ hcov_status hcov_tree_get_info(hcov_tree t, hcov_tree_info *info);
 hcov_status hcov_tree_blocks(hcov_tree t, int32_t *out4, int64_t cap, int64_t *count);
 /* Schedule introspection (diagnostics): 6 int32 per task of the DAG in generation order:
  * type (0 FILL, 1 ACA, 2 TAPP, 3 POTRF, 4 TRSM, 5 RAPP, 6 SEG, 7 PROJ, 8 PRR, 9 PHWP, 10 PHWR,
- * 11 NOP), phase (0 assembly, 1 H-Cholesky, 2 forward solve), and the task arguments a, b, c, d. */
+ * 11 NOP, 12 BSEG, 13 BPROJ), phase (0 assembly, 1 H-Cholesky, 2 forward solve, 3 back-solve), and
+ * the task arguments a, b, c, d. */
 hcov_status hcov_tree_tasks(hcov_tree t, int32_t *out6, int64_t cap, int64_t *count);
 /* DAG successors (diagnostics): off has n_tasks + 1 entries, succ has *count entries (CSR).
  * With off == NULL or succ == NULL only *count is set.  Setting the environment variable
@@ -146,6 +147,25 @@ hcov_status hcov_eval(hcov_tree t, const hcov_theta *theta, const hcov_trunc *tr
 hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *thetas_host, int32_t m,
                            const hcov_trunc *trunc, hcov_stream stream, double *loglik_host,
                            hcov_status *status_host);
+
+/* NEXT (f1): the paper's own quadratic-form path (listing PAPER.md:550-555: TCG on C~
+ * with the factor as preconditioner, 150 iterations, tolerance 1e-6) and its building blocks.
+ * All vectors are n fp64 device arrays in EXTERNAL order; P = the cluster-tree permutation.
+ *   hcov_forward_solve: v = P_i2e L~^{-1} P_e2i z   (the Eq. (2) forward solve; v^T v = q)
+ *   hcov_backsolve:     u = P_i2e L~^{-T} P_e2i v   (root back-solve, transposed leaf chain)
+ *   hcov_solve:         x = C~^{-1} b = P_i2e L~^{-T} L~^{-1} P_e2i b
+ *   hcov_matvec:        y = C~ x for an ASSEMBLED (not factored) H-matrix (Table 1),
+ *                       lower blocks and their mirror (Remark 1), deterministic order
+ *   hcov_pcg:           preconditioned CG for C~ x = b (A assembled, M factored, same tree):
+ *                       x0 = 0, preconditioner z = M^{-1} r via hcov_solve; stops after maxit
+ *                       iterations or when ||r||_2 <= tol ||b||_2; iters, relres = ||r|| / ||b||.
+ * Factored: state after hcov_cholesky (or hcov_eval's handle).  Synchronise the stream. */
+hcov_status hcov_forward_solve(hcov_hmat h, const double *z_dev, double *v_dev, hcov_stream stream);
+hcov_status hcov_backsolve(hcov_hmat h, const double *v_dev, double *u_dev, hcov_stream stream);
+hcov_status hcov_solve(hcov_hmat h, const double *b_dev, double *x_dev, hcov_stream stream);
+hcov_status hcov_matvec(hcov_hmat h, const double *x_dev, double *y_dev, hcov_stream stream);
+hcov_status hcov_pcg(hcov_hmat A, hcov_hmat M, const double *b_dev, double *x_dev, int32_t maxit, double tol,
+                     hcov_stream stream, int32_t *iters_host, double *relres_host);
 
 /* Support (not timed).  Z = P_i2e L~ xi for a factored matrix (Sec. 5.1);
  * xi_dev, Z_dev: n fp64 (xi in external order too: xi is permuted to internal first). */

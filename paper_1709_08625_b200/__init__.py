@@ -87,6 +87,11 @@ _SIGS = {
     "hcov_columns": (_I32, [_P, _P, _I32, _P, _P]),
     "hcov_hmat_storage": (_I32, [_P, _P, _P, _P]),
     "hcov_cov_columns": (_I32, [_P, _P, _P, _I32, _P, _P]),
+    "hcov_forward_solve": (_I32, [_P, _P, _P, _P]),
+    "hcov_backsolve": (_I32, [_P, _P, _P, _P]),
+    "hcov_solve": (_I32, [_P, _P, _P, _P]),
+    "hcov_matvec": (_I32, [_P, _P, _P, _P]),
+    "hcov_pcg": (_I32, [_P, _P, _P, _P, _I32, _D, _P, _P, _P]),
     "hcov_model_flops": (_I32, [_P, _P]),
     "hcov_tree_last_eval": (_I32, [_P, _P]),
     "hcov_prof_control": (_I32, [_I32, _I32]),
@@ -274,6 +279,28 @@ class HMatrix:
         _check(lib().hcov_columns(self._h, c.ctypes.data, len(c), _dev_f64(out), _stream(stream)), "hcov_columns")
         return out.T   # n x m, external rows
 
+    def _vec_op(self, fn, x, name, stream=None):
+        import torch
+        y = torch.empty_like(x)
+        _check(getattr(lib(), fn)(self._h, _dev_f64(x, self.tree.n, "x"), _dev_f64(y), _stream(stream)), fn)
+        return y
+
+    def forward_solve(self, z, stream=None):
+        """hcov_forward_solve: v = P L~^{-1} P^T z (external order)."""
+        return self._vec_op("hcov_forward_solve", z, "z", stream)
+
+    def backsolve(self, v, stream=None):
+        """hcov_backsolve: u = P L~^{-T} P^T v (external order)."""
+        return self._vec_op("hcov_backsolve", v, "v", stream)
+
+    def solve(self, b, stream=None):
+        """hcov_solve: x = C~^{-1} b through the factor."""
+        return self._vec_op("hcov_solve", b, "b", stream)
+
+    def matvec(self, x, stream=None):
+        """hcov_matvec: y = C~ x (assembled, not factored)."""
+        return self._vec_op("hcov_matvec", x, "x", stream)
+
     def model_flops(self) -> dict:
         """hcov_model_flops: SURVEY Sec. 8(d) method-work model at the measured ranks (factored)."""
         o = np.zeros(8)
@@ -310,6 +337,17 @@ def eval_loglik(tree: Tree, theta, Z, eps: float, kmax: int = 0, kcap: int = 0, 
     if code not in (HCOV_OK, 3, 6):
         raise HcovError(code, "hcov_eval")
     return d
+
+
+def pcg(A: "HMatrix", M: "HMatrix", b, maxit: int = 150, tol: float = 1e-6, stream=None):
+    """hcov_pcg: C~ x = b by CG preconditioned with the H-Cholesky factor M (listing PAPER.md:550-555).
+    Returns (x, iterations, relative residual)."""
+    import torch
+    x = torch.empty_like(b)
+    it, rr = ctypes.c_int32(), ctypes.c_double()
+    _check(lib().hcov_pcg(A._h, M._h, _dev_f64(b, A.tree.n, "b"), _dev_f64(x), maxit, tol, _stream(stream),
+                          ctypes.byref(it), ctypes.byref(rr)), "hcov_pcg")
+    return x, it.value, rr.value
 
 
 def mle_batch(tree: Tree, Z, thetas, eps: float, kmax: int = 0, kcap: int = 0, stream=None):

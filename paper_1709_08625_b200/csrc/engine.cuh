@@ -48,6 +48,7 @@ struct Ctx {
     unsigned long long *mem;   // [0] W bump, [1] P bump, [2] pool overflows
     int64_t wcap, pcap;        // pool capacities (doubles)
     double *vbuf;              // root right-hand side / solution (internal order)
+    double *tbuf;              // back-solve projections t_b = U_b^T u (n_r x kcap)
     double *logdet_part, *minpiv_part, *quad_part;
     int32_t *fail_leaf;        // min over failing leaves (init INT32_MAX)
     int32_t *flags;            // [0] cap binds, [1] rank overflow, [2] max rank, [3] accuracy losses
@@ -1595,6 +1596,85 @@ __device__ void task_phwr(const Ctx &c, const DTask &tk, double *smem, double &f
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Root back-solve u = L~^{-T} v in place in vbuf (NEXT (f1); the transpose of the root forward
+// solve).  Segment i: y = v_i - sum over the strictly-lower leaves over column i of
+//   tile (rho, i):      T^T u_rho                  (kind 0, aux = rho)
+//   low-rank b = U V^T: V_b[rows of i] t_b         (kind 1, t_b = U_b^T u[rows of b] from BPROJ)
+// then u_i = L_ii^{-T} y.  Each warp accumulates a fixed subset of the contributions; the partial
+// vectors are summed in warp order (deterministic).
+__device__ void task_bseg(const Ctx &c, const DTask &tk, double *smem, double &fl)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = tk.b;
+    double *part = smem;                          // NWARP x 32 partial sums
+    double *Ts = part + 32 * NWARP;               // NWARP padded 32 x 33 tiles
+    double *mine = Ts + (int64_t)warp * 32 * 33;
+    double acc = 0.0;                             // this warp's partial, entry `lane`
+    for (int z = tk.c + warp; z < tk.d; z += NWARP) {
+        const DCtr ct = c.ctr[z];
+        if (ct.kind == 0) {
+            const double *T = c.tiles + (int64_t)ct.id * HCOV_TILE;
+            const double *u = c.vbuf + (int64_t)ct.aux * HCOV_LEAF;
+            for (int cc = 0; cc < 32; ++cc) mine[lane + 33 * cc] = __ldcg(T + lane + 32 * cc);   // coalesced
+            const double ul = __ldcg(u + lane);
+            __syncwarp();
+            // (T^T u)[lane] = sum_rr T[rr, lane] u[rr]
+            double s = 0.0;
+#pragma unroll 8
+            for (int rr = 0; rr < 32; ++rr) s = fma(mine[rr + 33 * lane], __shfl_sync(0xffffffffu, ul, rr), s);
+            acc += s;
+            __syncwarp();
+            fl += 2.0 * 32 * 32;
+        } else {
+            const DRBlk b = c.rblk[ct.id];
+            const int rk = __ldcg(c.rank + ct.id);
+            const double *V = r_V(c, ct.id) + (i * HCOV_LEAF - b.col0) + lane;
+            const double *t = c.tbuf + (int64_t)ct.id * c.kcap;
+            double s = 0.0;
+            for (int l = 0; l < rk; ++l) s = fma(__ldcg(V + (int64_t)b.m * l), __ldcg(t + l), s);
+            acc += s;
+            fl += 2.0 * 32 * rk;
+        }
+    }
+    part[warp * 32 + lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+        double y = __ldcg(c.vbuf + i * HCOV_LEAF + lane);
+        for (int w = 0; w < NWARP; ++w) y -= part[w * 32 + lane];
+        // L_ii^T u = y: u_a = y_a / L_aa for a = 31..0, then y_b -= L_ab u_a for b < a
+        const double *L = c.tiles + (int64_t)c.diag_tile[i] * HCOV_TILE;
+        for (int cc = 0; cc < 32; ++cc) mine[lane + 33 * cc] = __ldcg(L + lane + 32 * cc);
+        __syncwarp();
+        for (int a = 31; a >= 0; --a) {
+            const double ua = __shfl_sync(0xffffffffu, y, a) / mine[a + 33 * a];
+            if (lane == a) y = ua;
+            else if (lane < a) y = fma(-mine[a + 33 * lane], ua, y);
+        }
+        __stcg(c.vbuf + i * HCOV_LEAF + lane, y);
+        fl += 32.0 * 32;
+    }
+}
+
+// t_b = U_b^T u[rows of b] (rank_b values into tbuf): one warp per column of U_b.
+__device__ void task_bproj(const Ctx &c, const DTask &tk, double &fl)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = tk.b;
+    const DRBlk b = c.rblk[r];
+    const int rk = __ldcg(c.rank + r);
+    const double *U = r_U(c, r);
+    const double *u = c.vbuf + b.row0;
+    for (int l = warp; l < rk; l += NWARP) {
+        const double *ul = U + (int64_t)b.m * l;
+        double s = 0.0;
+        for (int64_t q = lane; q < b.m; q += 32) s = fma(__ldcg(ul + q), __ldcg(u + q), s);
+        s = warp_sum(s);
+        if (lane == 0) __stcg(c.tbuf + (int64_t)r * c.kcap + l, s);
+    }
+    fl += 2.0 * b.m * rk;
 }
 
 // shared memory (doubles) of the engine's task bodies

@@ -47,8 +47,8 @@ cudaError_t upload(T **d, const std::vector<T> &h)
 // ------------------------------------------------------------------------------------------
 enum ProfCls { PC_ENGINE = 0, PC_RESET = 1, PC_PERM = 2, PC_REDUCE = 3, PC_AUX = 4, PC_N = 5 };
 const char *const PROF_NAMES[PC_N] = {"engine", "reset", "permute", "reduce", "aux"};
-const char *const TASK_NAMES[TK_NTYPES] = {"fill", "aca", "tapp", "potrf", "trsm", "rapp",
-                                           "seg", "proj", "prr", "phwp", "phwr", "nop"};
+const char *const TASK_NAMES[TK_NTYPES] = {"fill", "aca", "tapp", "potrf", "trsm", "rapp", "seg",
+                                           "proj", "prr", "phwp", "phwr", "nop", "bseg", "bproj"};
 struct ProfEv { int cls; cudaEvent_t a, b; };
 struct Prof {
     int64_t launches = 0;
@@ -272,6 +272,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
         case TK_PRR: task_prr(c, tk, fl[FC_PROD]); break;
         case TK_PHWP: task_phwp(c, tk, fl[FC_PROD]); break;
         case TK_PHWR: task_phwr(c, tk, smem, fl[FC_PROD]); break;
+        case TK_BSEG: task_bseg(c, tk, smem, fl[FC_SOLVE]); break;
+        case TK_BPROJ: task_bproj(c, tk, fl[FC_SOLVE]); break;
         default: break;
         }
         __threadfence();
@@ -475,6 +477,102 @@ __global__ void k_columns_perm(Ctx c, const double *in, int mcols, double *out)
     }
 }
 
+// ---- H-matvec y = C~ x of an assembled H-matrix (Table 1 row "C~ z"), internal order.
+// k_mv_t: per low-rank block, t1_b = V_b^T x[cols of b], t2_b = U_b^T x[rows of b].
+__global__ void __launch_bounds__(NT) k_mv_t(Ctx c, const double *x, double *t1, double *t2)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int r = blockIdx.x; r < c.n_r; r += gridDim.x) {
+        const DRBlk b = c.rblk[r];
+        const int rk = c.rank[r];
+        const double *U = r_U(c, r), *V = r_V(c, r);
+        for (int q = warp; q < 2 * rk; q += NWARP) {
+            const int l = q % rk;
+            const bool tv = q < rk;
+            const double *F = (tv ? V : U) + (int64_t)b.m * l;
+            const double *xx = x + (tv ? b.col0 : b.row0);
+            double s = 0.0;
+            for (int64_t i = lane; i < b.m; i += 32) s = fma(F[i], xx[i], s);
+            s = warp_sum(s);
+            if (lane == 0) (tv ? t1 : t2)[(int64_t)r * c.kcap + l] = s;
+        }
+    }
+}
+// k_mv_rows: one warp per leaf segment i, lane = row: y_i = sum over the leaves of row i (T x_j,
+// U_b[i] t1_b) + sum over the strictly-lower leaves of column i (T^T x_rho, V_b[i] t2_b), in the
+// fixed CSR order (deterministic).  The symmetric upper triangle is the mirror (Remark 1, R10).
+__global__ void __launch_bounds__(256) k_mv_rows(Ctx c, const int32_t *row_off, const int32_t *row_nodes,
+                                                 const int32_t *col_off, const int32_t *col_nodes, const double *x,
+                                                 const double *t1, const double *t2, double *y)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t seg = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); seg < c.n_leaves; seg += nw) {
+        double s = 0.0;
+        for (int k = row_off[seg]; k < row_off[seg + 1]; ++k) {
+            const DNode nd = c.nodes[row_nodes[k]];
+            if (nd.type == ND_T) {
+                const double *T = c.tiles + (int64_t)nd.idx * HCOV_TILE + lane;
+                const double *xx = x + (int64_t)nd.j * HCOV_LEAF;
+                for (int j = 0; j < 32; ++j) s = fma(T[32 * j], xx[j], s);
+            } else {
+                const DRBlk b = c.rblk[nd.idx];
+                const int rk = c.rank[nd.idx];
+                const double *U = r_U(c, nd.idx) + (seg * HCOV_LEAF - b.row0 + lane);
+                const double *t = t1 + (int64_t)nd.idx * c.kcap;
+                for (int l = 0; l < rk; ++l) s = fma(U[(int64_t)b.m * l], t[l], s);
+            }
+        }
+        for (int k = col_off[seg]; k < col_off[seg + 1]; ++k) {
+            const DNode nd = c.nodes[col_nodes[k]];
+            if (nd.type == ND_T) {
+                const double *T = c.tiles + (int64_t)nd.idx * HCOV_TILE + 32 * lane;
+                const double *xx = x + (int64_t)nd.i * HCOV_LEAF;
+                for (int j = 0; j < 32; ++j) s = fma(T[j], xx[j], s);
+            } else {
+                const DRBlk b = c.rblk[nd.idx];
+                const int rk = c.rank[nd.idx];
+                const double *V = r_V(c, nd.idx) + (seg * HCOV_LEAF - b.col0 + lane);
+                const double *t = t2 + (int64_t)nd.idx * c.kcap;
+                for (int l = 0; l < rk; ++l) s = fma(V[(int64_t)b.m * l], t[l], s);
+            }
+        }
+        y[seg * HCOV_LEAF + lane] = s;
+    }
+}
+
+// ---- vector kernels of the PCG (external order).  Dot products in a fixed order: 148 x 256 partials
+// (grid-stride, fixed assignment), then one CTA sums them in index order.
+#define DOT_BLOCKS 148
+__global__ void __launch_bounds__(256) k_dot_part(const double *a, const double *b, int64_t n, double *part)
+{
+    __shared__ double red[8];
+    double s = 0.0;
+    for (int64_t k = blockIdx.x * 256 + threadIdx.x; k < n; k += (int64_t)DOT_BLOCKS * 256) s = fma(a[k], b[k], s);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+__global__ void k_dot_sum(const double *part, double *out)
+{
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < DOT_BLOCKS; ++k) t += part[k];
+        *out = t;
+    }
+}
+// y = a x + b y
+__global__ void k_axpby(int64_t n, double a, const double *x, double b, double *y)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        y[k] = fma(a, x[k], b * y[k]);
+}
+
 // Unit-test kernel for the truncation (A6): one CTA truncates X Y^T (m x m, R columns).
 __global__ void __launch_bounds__(NT) k_test_truncate(double *scr, int64_t m, int R, int K, double eps, int kmax,
                                                       int rlim, int path, double *U, double *V, int *rank,
@@ -517,9 +615,10 @@ struct hcov_tree_s {
     DTask *d_tasks = nullptr;
     int8_t *d_phase = nullptr;
     int32_t *d_succ_off = nullptr, *d_succ = nullptr;
-    int32_t *d_indeg[4] = {nullptr, nullptr, nullptr, nullptr};
-    int32_t *d_roots[4][2] = {};
-    int32_t *d_q0init[4] = {}, *d_q0tail[4] = {};
+    int32_t *d_indeg[HCOV_MODES] = {};
+    int32_t *d_roots[HCOV_MODES][2] = {};
+    int32_t *d_q0init[HCOV_MODES] = {}, *d_q0tail[HCOV_MODES] = {};
+    int32_t *d_col_off = nullptr, *d_col_nodes = nullptr;
     int32_t *d_band_off = nullptr;
     int32_t *d_diag_tile = nullptr;
     double *d_xs = nullptr, *d_ys = nullptr;
@@ -541,7 +640,7 @@ struct hcov_hmat_s {
     int grid = 0;
     int64_t smem = 0;
     double *tiles = nullptr, *U = nullptr, *V = nullptr, *cores = nullptr, *W = nullptr, *P = nullptr;
-    double *vbuf = nullptr, *logdet_part = nullptr, *minpiv_part = nullptr, *quad_part = nullptr;
+    double *vbuf = nullptr, *tbuf = nullptr, *logdet_part = nullptr, *minpiv_part = nullptr, *quad_part = nullptr;
     int32_t *rank = nullptr, *fail = nullptr, *flags = nullptr;
     int32_t *indeg = nullptr, *q0 = nullptr, *q1 = nullptr, *gbar = nullptr, *gslot = nullptr;
     uint32_t *qctl = nullptr;
@@ -553,10 +652,11 @@ struct hcov_hmat_s {
     EngineStats *stats = nullptr, *stats_host = nullptr;
     void release_all()
     {
-        void *ps[] = {tiles, U, V, cores, W, P, vbuf, logdet_part, minpiv_part, quad_part, rank, fail, flags,
+        void *ps[] = {tiles, U, V, cores, W, P, vbuf, tbuf, logdet_part, minpiv_part, quad_part, rank, fail, flags,
                       indeg, q0, q1, gbar, gslot, qctl, scr, bscr, res, stats, woff, poff, mem};
         for (void *p : ps) cudaFree(p);
-        tiles = U = V = cores = W = P = vbuf = logdet_part = minpiv_part = quad_part = nullptr;
+        tiles = U = V = cores = W = P = vbuf = tbuf = logdet_part = minpiv_part = quad_part = nullptr;
+        wcap = pcap = 0;
         rank = fail = flags = indeg = q0 = q1 = gbar = gslot = nullptr;
         qctl = nullptr;
         scr = bscr = res = nullptr;
@@ -579,9 +679,10 @@ hcov_tree_s::~hcov_tree_s()
     if (cached) delete cached;
     void *ps[] = {d_nodes, d_tile_node, d_rblk, d_terms, d_xterm, d_fac_row0, d_fac_nrows, d_fac_rank_src,
                   d_fac_off, d_fac_pool, d_solves, d_solve_rhs, d_slots, d_ctr, d_phw, d_col_r, d_tasks, d_phase,
-                  d_succ_off, d_succ, d_diag_tile, d_xs, d_ys, d_perm_i2e, d_leafnodes, d_row_off, d_row_nodes};
+                  d_succ_off, d_succ, d_diag_tile, d_xs, d_ys, d_perm_i2e, d_leafnodes, d_row_off, d_row_nodes,
+                  d_col_off, d_col_nodes};
     for (void *p : ps) cudaFree(p);
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < HCOV_MODES; ++m) {
         cudaFree(d_indeg[m]);
         cudaFree(d_roots[m][0]);
         cudaFree(d_roots[m][1]);
@@ -619,7 +720,9 @@ hcov_status tree_upload(hcov_tree t)
     CK(upload(&t->d_phase, P.phase));
     CK(upload(&t->d_succ_off, P.succ_off));
     CK(upload(&t->d_succ, P.succ));
-    for (int m = 0; m < 4; ++m) {
+    CK(upload(&t->d_col_off, P.col_off));
+    CK(upload(&t->d_col_nodes, P.col_nodes));
+    for (int m = 0; m < HCOV_MODES; ++m) {
         CK(upload(&t->d_indeg[m], P.indeg[m]));
         CK(upload(&t->d_roots[m][0], P.roots[m][0]));
         CK(upload(&t->d_roots[m][1], P.roots[m][1]));
@@ -675,7 +778,7 @@ int eff_kcap(const hcov_trunc *tr)
 int64_t qcap(const Plan &P, int cls)
 {
     int64_t q = 1;
-    for (int m = 0; m < 4; ++m) q = std::max<int64_t>(q, P.n_q[m][cls]);
+    for (int m = 0; m < HCOV_MODES; ++m) q = std::max<int64_t>(q, P.n_q[m][cls]);
     return q;
 }
 
@@ -697,6 +800,7 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     CK(cudaMalloc(&h->poff, std::max<size_t>(1, P.slots.size()) * sizeof(int64_t)));
     CK(cudaMalloc(&h->mem, 4 * sizeof(unsigned long long)));
     CK(cudaMalloc(&h->vbuf, P.n_pad * sizeof(double)));
+    CK(cudaMalloc(&h->tbuf, std::max<int64_t>(1, P.n_r() * kc) * sizeof(double)));
     CK(cudaMalloc(&h->logdet_part, P.n_leaves * sizeof(double)));
     CK(cudaMalloc(&h->minpiv_part, P.n_leaves * sizeof(double)));
     CK(cudaMalloc(&h->quad_part, P.n_leaves * sizeof(double)));
@@ -737,22 +841,32 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     h->ctx.scr_stride = scr_stride;
     h->ctx.bscr_stride = 0;
     h->ctx.gshared_off = gshared_off;
-    {
-        // W and product slots are allocated at run time with actual ranks (bump pools); the pools get
-        // the capacity-based sizes when they fit, else the free device memory (minus 3 GB headroom)
-        // split 70 / 30.  An overflow is detected and reported as HCOV_ERR_OUT_OF_MEMORY.
-        size_t fr = 0, tot = 0;
-        CK(cudaMemGetInfo(&fr, &tot));
-        const int64_t avail = std::max<int64_t>(0, (int64_t)fr / 8 - ((int64_t)3 << 27));
-        if (wfull + pfull <= avail) { h->wcap = wfull; h->pcap = pfull; }
-        else {
-            h->wcap = std::min<int64_t>(wfull, (int64_t)(0.7 * avail));
-            h->pcap = std::min<int64_t>(pfull, avail - h->wcap);
-        }
-        CK(cudaMalloc(&h->W, std::max<int64_t>(1, h->wcap) * sizeof(double)));
-        CK(cudaMalloc(&h->P, std::max<int64_t>(1, h->pcap) * sizeof(double)));
-    }
     h->kcap_alloc = kcap;
+    return HCOV_OK;
+}
+
+// The W and product-slot pools (H-Cholesky and solves only; an assembly-only H-matrix never holds
+// them).  W and the slots are bump-allocated at run time with the actual ranks; the pools get the
+// capacity-based sizes when they fit, else the free device memory (minus 3 GB headroom) split
+// 70 / 30.  An overflow is detected and reported as HCOV_ERR_OUT_OF_MEMORY.
+hcov_status pools_alloc(hcov_hmat h)
+{
+    if (h->W) return HCOV_OK;
+    const Plan &P = h->t->P;
+    const int64_t kc = h->kcap_alloc;
+    const int64_t wfull = P.w_elems * kc + (int64_t)P.phw.size() + 64;
+    const int64_t pfull = P.slot_a * kc * kc + P.slot_b * kc + (int64_t)P.slots.size() + 64;
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const int64_t avail = std::max<int64_t>(0, (int64_t)fr / 8 - ((int64_t)3 << 27));
+    if (wfull + pfull <= avail) { h->wcap = wfull; h->pcap = pfull; }
+    else {
+        h->wcap = std::min<int64_t>(wfull, (int64_t)(0.7 * avail));
+        h->pcap = std::min<int64_t>(pfull, avail - h->wcap);
+    }
+    CK(cudaMalloc(&h->W, std::max<int64_t>(1, h->wcap) * sizeof(double)));
+    CK(cudaMalloc(&h->P, std::max<int64_t>(1, h->pcap) * sizeof(double)));
+    h->ctx.W = h->W; h->ctx.P = h->P; h->ctx.wcap = h->wcap; h->ctx.pcap = h->pcap;
     return HCOV_OK;
 }
 
@@ -771,7 +885,7 @@ void fill_ctx(hcov_hmat h)
     c.n_pad = P.n_pad; c.n_leaves = P.n_leaves; c.n_real = P.n; c.n_tiles = P.n_tiles();
     c.tiles = h->tiles; c.U = h->U; c.V = h->V; c.rank = h->rank; c.cores = h->cores; c.W = h->W; c.P = h->P;
     c.woff = h->woff; c.poff = h->poff; c.mem = h->mem; c.wcap = h->wcap; c.pcap = h->pcap;
-    c.vbuf = h->vbuf; c.logdet_part = h->logdet_part; c.minpiv_part = h->minpiv_part; c.quad_part = h->quad_part;
+    c.vbuf = h->vbuf; c.tbuf = h->tbuf; c.logdet_part = h->logdet_part; c.minpiv_part = h->minpiv_part; c.quad_part = h->quad_part;
     c.fail_leaf = h->fail; c.flags = h->flags;
     c.kcap = h->kcap_alloc; c.kmax = h->trunc.kmax; c.eps = h->trunc.eps;
     {
@@ -796,13 +910,17 @@ void fill_ctx(hcov_hmat h)
     c.timeout_ns = (unsigned long long)(wds * 1e9);
 }
 
-// Run the engine in mode md (0 all, 1 assembly, 2 Cholesky, 3 solve) on stream st.
+// Run the engine in mode md (0 eval, 1 assembly, 2 Cholesky, 3 forward solve, 4 back-solve) on st.
 hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
 {
     hcov_tree t = h->t;
     Plan &P = t->P;
-    static const int mask[4] = {7, 1, 2, 4};
+    static const int mask[HCOV_MODES] = {7, 1, 2, 4, 8};
     const int64_t ntk = (int64_t)P.tasks.size();
+    if (md == 0 || md == 2 || md == 3) {
+        hcov_status ps = pools_alloc(h);
+        if (ps) return ps;
+    }
     Ctx c = h->ctx;
     c.nq[0] = P.n_q[md][0];
     c.nq[1] = P.n_q[md][1];
@@ -1136,6 +1254,151 @@ hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *t
             loglik_host[k] = -INFINITY;
         else return s;
     }
+    return HCOV_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// in (external) -> vbuf -> [forward] -> [back] -> out (external); factored H-matrix.
+hcov_status solve_ext(hcov_hmat h, const double *in, double *out, bool fwd, bool back, cudaStream_t st)
+{
+    LAUNCH(PC_AUX, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, in, h->vbuf));
+    hcov_status s;
+    if (fwd && (s = engine_run(h, 3, st))) return s;
+    if (back && (s = engine_run(h, 4, st))) return s;
+    LAUNCH(PC_AUX, st, k_permute_out<<<256, 256, 0, st>>>(h->ctx, h->vbuf, out));
+    int32_t hf[5];
+    return check_abort(h, st, hf);
+}
+
+hcov_status matvec_ext(hcov_hmat h, const double *x, double *y, double *xi, double *yi, double *t12, cudaStream_t st)
+{
+    hcov_tree t = h->t;
+    const Plan &P = t->P;
+    LAUNCH(PC_AUX, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, x, xi));
+    double *t1 = t12, *t2 = t12 + std::max<int64_t>(1, P.n_r()) * h->ctx.kcap;
+    if (P.n_r() > 0) LAUNCH(PC_AUX, st, k_mv_t<<<(int)std::min<int64_t>(P.n_r(), 65535), NT, 0, st>>>(h->ctx, xi, t1, t2));
+    LAUNCH(PC_AUX, st, k_mv_rows<<<(int)std::min<int64_t>((P.n_leaves + 7) / 8, 65535), 256, 0, st>>>(
+                           h->ctx, t->d_row_off, t->d_row_nodes, t->d_col_off, t->d_col_nodes, xi, t1, t2, yi));
+    LAUNCH(PC_AUX, st, k_permute_out<<<256, 256, 0, st>>>(h->ctx, yi, y));
+    CK(cudaGetLastError());
+    return HCOV_OK;
+}
+
+struct DevBuf {
+    std::vector<void *> ps;
+    ~DevBuf() { for (void *p : ps) cudaFree(p); }
+    template <class T> cudaError_t get(T **p, int64_t n)
+    {
+        cudaError_t e = cudaMalloc((void **)p, std::max<int64_t>(1, n) * sizeof(T));
+        if (e == cudaSuccess) ps.push_back(*p);
+        return e;
+    }
+};
+
+double dot_dev(const double *a, const double *b, int64_t n, double *part, double *res, double *res_host, cudaStream_t st)
+{
+    k_dot_part<<<DOT_BLOCKS, 256, 0, st>>>(a, b, n, part);
+    k_dot_sum<<<1, 32, 0, st>>>(part, res);
+    g_prof.launches += 2;
+    cudaMemcpyAsync(res_host, res, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return *res_host;
+}
+}  // namespace
+
+extern "C" {
+
+hcov_status hcov_forward_solve(hcov_hmat h, const double *z_dev, double *v_dev, hcov_stream stream)
+{
+    if (!h || !z_dev || !v_dev) return HCOV_ERR_INVALID_ARG;
+    if (h->state < 2) return HCOV_ERR_STATE;
+    return solve_ext(h, z_dev, v_dev, true, false, (cudaStream_t)stream);
+}
+
+hcov_status hcov_backsolve(hcov_hmat h, const double *v_dev, double *u_dev, hcov_stream stream)
+{
+    if (!h || !v_dev || !u_dev) return HCOV_ERR_INVALID_ARG;
+    if (h->state < 2) return HCOV_ERR_STATE;
+    return solve_ext(h, v_dev, u_dev, false, true, (cudaStream_t)stream);
+}
+
+hcov_status hcov_solve(hcov_hmat h, const double *b_dev, double *x_dev, hcov_stream stream)
+{
+    if (!h || !b_dev || !x_dev) return HCOV_ERR_INVALID_ARG;
+    if (h->state < 2) return HCOV_ERR_STATE;
+    return solve_ext(h, b_dev, x_dev, true, true, (cudaStream_t)stream);
+}
+
+hcov_status hcov_matvec(hcov_hmat h, const double *x_dev, double *y_dev, hcov_stream stream)
+{
+    if (!h || !x_dev || !y_dev) return HCOV_ERR_INVALID_ARG;
+    if (h->state != 1) return HCOV_ERR_STATE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Plan &P = h->t->P;
+    DevBuf B;
+    double *xi, *yi, *t12;
+    CK(B.get(&xi, P.n_pad));
+    CK(B.get(&yi, P.n_pad));
+    CK(B.get(&t12, 2 * std::max<int64_t>(1, P.n_r()) * h->ctx.kcap));
+    hcov_status s = matvec_ext(h, x_dev, y_dev, xi, yi, t12, st);
+    if (s) return s;
+    CK(cudaStreamSynchronize(st));
+    return HCOV_OK;
+}
+
+hcov_status hcov_pcg(hcov_hmat A, hcov_hmat M, const double *b_dev, double *x_dev, int32_t maxit, double tol,
+                     hcov_stream stream, int32_t *iters, double *relres)
+{
+    if (!A || !M || !b_dev || !x_dev || maxit < 0 || !(tol >= 0) || !iters || !relres) return HCOV_ERR_INVALID_ARG;
+    if (A->state != 1 || M->state < 2) return HCOV_ERR_STATE;
+    if (A->t != M->t) return HCOV_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Plan &P = A->t->P;
+    const int64_t n = P.n;
+    DevBuf B;
+    double *r, *z, *p, *q, *xi, *yi, *t12, *part, *res, *resh;
+    CK(B.get(&r, n)); CK(B.get(&z, n)); CK(B.get(&p, n)); CK(B.get(&q, n));
+    CK(B.get(&xi, P.n_pad)); CK(B.get(&yi, P.n_pad));
+    CK(B.get(&t12, 2 * std::max<int64_t>(1, P.n_r()) * A->ctx.kcap));
+    CK(B.get(&part, DOT_BLOCKS)); CK(B.get(&res, 1));
+    CK(cudaMallocHost(&resh, sizeof(double)));
+    std::unique_ptr<double, cudaError_t (*)(void *)> resh_guard(resh, cudaFreeHost);
+    const int gb = 592;
+    // x0 = 0, r0 = b, z0 = M^{-1} r0, p0 = z0  (TCG with preconditioner A_inv, listing PAPER.md:550-555)
+    CK(cudaMemsetAsync(x_dev, 0, n * sizeof(double), st));
+    CK(cudaMemcpyAsync(r, b_dev, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    hcov_status s;
+    if ((s = solve_ext(M, r, z, true, true, st))) return s;
+    CK(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    const double bb = std::sqrt(dot_dev(b_dev, b_dev, n, part, res, resh, st));
+    double rz = dot_dev(r, z, n, part, res, resh, st);
+    int it = 0;
+    double rr = bb;
+    *relres = bb > 0 ? 1.0 : 0.0;
+    while (it < maxit && bb > 0) {
+        if ((s = matvec_ext(A, p, q, xi, yi, t12, st))) return s;
+        const double pq = dot_dev(p, q, n, part, res, resh, st);
+        if (!(pq > 0)) break;   // A~ not positive definite along p
+        const double alpha = rz / pq;
+        k_axpby<<<gb, 256, 0, st>>>(n, alpha, p, 1.0, x_dev);
+        k_axpby<<<gb, 256, 0, st>>>(n, -alpha, q, 1.0, r);
+        g_prof.launches += 2;
+        ++it;
+        rr = std::sqrt(dot_dev(r, r, n, part, res, resh, st));
+        *relres = rr / bb;
+        if (rr <= tol * bb) break;
+        if ((s = solve_ext(M, r, z, true, true, st))) return s;
+        const double rz1 = dot_dev(r, z, n, part, res, resh, st);
+        const double beta = rz1 / rz;
+        rz = rz1;
+        k_axpby<<<gb, 256, 0, st>>>(n, 1.0, z, beta, p);
+        g_prof.launches += 1;
+    }
+    *iters = it;
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
     return HCOV_OK;
 }
 

@@ -47,8 +47,11 @@ enum TaskType : int32_t {
     TK_PHWP = 9,   // a = phw id, b = R id (leaf of the H block), c = q slot: Q = V_x^T V_partners[cols of x]
     TK_PHWR = 10,  // a = phw id, b = leaf row segment, [c, d) = ctr[]: W rows = H(rows, :) V_partners
     TK_NOP = 11,   // join (completed inline by the engine, never occupies a CTA)
-    TK_NTYPES = 12
+    TK_BSEG = 12,  // b = leaf segment, [c, d) = ctr[]: back-solve rows u_i = L_ii^{-T} (v_i - sum L_ri^T u_r)
+    TK_BPROJ = 13, // b = R id: t_b = U_b^T u[rows of b] (back-solve projection into tbuf)
+    TK_NTYPES = 14
 };
+#define HCOV_MODES 5   // engine modes (plan.h)
 struct DTask {
     int32_t type;
     int32_t a, b, c, d;

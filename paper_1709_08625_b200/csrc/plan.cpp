@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <limits>
 #include <numeric>
 #include <unordered_map>
@@ -275,6 +276,51 @@ struct Builder {
         return join(S, l, c);
     }
 
+    // Root back-solve u = L~^{-T} v (transpose of the root forward solve; NEXT (f1), listing
+    // PAPER.md:550-555): leaf segments from the last to the first; segment i subtracts, for every
+    // strictly-lower leaf (rho, sigma) whose column range holds i, its transpose applied to the final
+    // u of its rows: tiles T^T u_rho (kind 0, aux = row segment), low-rank blocks V_b[rows of i] t_b
+    // with t_b = U_b^T u[rows of b] from a BPROJ task (kind 1), which waits for all of b's row segments.
+    void build_backsolve(const std::vector<std::vector<int32_t>> &colsv)
+    {
+        const int64_t nl = P.n_leaves;
+        std::vector<int32_t> bseg(nl, -1);
+        std::unordered_map<int64_t, int32_t> bj, bproj;
+        std::function<int32_t(int, int64_t)> bjoin = [&](int lv, int64_t c) -> int32_t {
+            if (lv == L) return bseg[c];
+            const int64_t h = heap_id(lv, c);
+            auto it = bj.find(h);
+            if (it != bj.end()) return it->second;
+            const int32_t t = task(TK_NOP, 0, 0, 0, 0, 0, {bjoin(lv + 1, 2 * c), bjoin(lv + 1, 2 * c + 1)});
+            bj[h] = t;
+            return t;
+        };
+        for (int64_t i = nl - 1; i >= 0; --i) {
+            std::vector<int32_t> dp;
+            const int32_t cb = (int32_t)P.ctr.size();
+            for (int32_t nd : colsv[i]) {
+                const DNode &x = P.nodes[nd];
+                if (x.type == ND_T) {
+                    P.ctr.push_back(DCtr{0, x.idx, x.i, 0});
+                    dp.push_back(bseg[x.i]);
+                } else {
+                    const int32_t r = x.idx;
+                    auto it = bproj.find(r);
+                    int32_t pt;
+                    if (it != bproj.end()) pt = it->second;
+                    else {
+                        pt = task(TK_BPROJ, 0, r, 0, 0, 0, {bjoin(x.level, x.i)});
+                        bproj[r] = pt;
+                    }
+                    P.ctr.push_back(DCtr{1, r, 0, 0});
+                    dp.push_back(pt);
+                }
+            }
+            const int32_t ce = (int32_t)P.ctr.size();
+            bseg[i] = task(TK_BSEG, 0, (int32_t)i, cb, ce, 0, dp);
+        }
+    }
+
     // W = H_e * [V of partners]: PHWP per low-rank leaf of H_e, PHWR per leaf row of H_e.
     int32_t build_phw(int32_t e, const std::vector<int32_t> &rents, int32_t col_off, int32_t solve_done)
     {
@@ -527,6 +573,29 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
     B.root_solve = (int32_t)P.solves.size();
     B.build_solve(0, 0, {});
     if (B.too_many_partners) return 1;
+    // columns (transpose of rows[]): strictly-lower leaves over each leaf column, rows ascending
+    std::vector<std::vector<int32_t>> colsv(P.n_leaves);
+    for (size_t k = 0; k < P.nodes.size(); ++k) {
+        const DNode &x = P.nodes[k];
+        if (x.type == ND_H || x.i == x.j) continue;
+        const int64_t span = (int64_t)1 << (L - x.level);
+        for (int64_t seg = (int64_t)x.j * span; seg < (int64_t)(x.j + 1) * span; ++seg) colsv[seg].push_back((int32_t)k);
+    }
+    for (auto &cv : colsv)
+        std::sort(cv.begin(), cv.end(), [&](int32_t a, int32_t b) {
+            const int64_t ra = (int64_t)P.nodes[a].i * P.cluster_size(P.nodes[a].level);
+            const int64_t rb = (int64_t)P.nodes[b].i * P.cluster_size(P.nodes[b].level);
+            return ra < rb;
+        });
+    P.col_off.assign(P.n_leaves + 1, 0);
+    P.col_nodes.clear();
+    for (int64_t seg = 0; seg < P.n_leaves; ++seg) {
+        P.col_off[seg] = (int32_t)P.col_nodes.size();
+        P.col_nodes.insert(P.col_nodes.end(), colsv[seg].begin(), colsv[seg].end());
+    }
+    P.col_off[P.n_leaves] = (int32_t)P.col_nodes.size();
+    const int32_t first_back_task = (int32_t)P.tasks.size();
+    B.build_backsolve(colsv);
 
     // ---- DAG: phases, successors, per-mode in-degrees and roots, critical path ------------
     const int32_t ntk = (int32_t)P.tasks.size();
@@ -535,6 +604,7 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
     for (int32_t t = 0; t < ntk; ++t) {
         const int ty = P.tasks[t].type;
         if (ty == TK_FILL || ty == TK_ACA) P.phase[t] = 0;
+        else if (t >= first_back_task) P.phase[t] = 3;
         else if (t >= first_root_task) P.phase[t] = 2;
     }
     P.succ_off.assign(ntk + 1, 0);
@@ -555,7 +625,7 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
         int32_t lmax = 0;
         for (int32_t d : B.deps[t]) lmax = std::max(lmax, len[d]);
         len[t] = lmax + (k.type == TK_NOP ? 0 : 1);
-        P.crit_len = std::max(P.crit_len, len[t]);
+        if (P.phase[t] <= 2) P.crit_len = std::max(P.crit_len, len[t]);   // the evaluation's chain
         if (k.type == TK_FILL) {
             int64_t cmin = INT64_MAX;
             for (int32_t q = k.a; q < k.a + k.b; ++q) cmin = std::min<int64_t>(cmin, P.nodes[P.tile_node[q]].j);
@@ -576,7 +646,7 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
             else if (k.type == TK_RAPP || k.type == TK_ACA) {
                 const double m = (double)P.rblk[k.a].m;
                 w[t] = (m <= HCOV_DENSE_MAX) ? 40.0 : 40.0 + m / (64.0 * std::max(1, k.qcls));
-            } else if (k.type == TK_SEG || k.type == TK_PHWR) w[t] = 3.0;
+            } else if (k.type == TK_SEG || k.type == TK_PHWR || k.type == TK_BSEG) w[t] = 3.0;
         }
         double bmax = 0.0;
         for (int32_t t = ntk - 1; t >= 0; --t) {
@@ -595,8 +665,8 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
         P.band_off.assign(HCOV_BANDS + 1, 0);
         for (int b = 0; b < HCOV_BANDS; ++b) P.band_off[b + 1] = P.band_off[b] + std::max(1, cnt[b]);
     }
-    static const int mask[4] = {7, 1, 2, 4};
-    for (int md = 0; md < 4; ++md) {
+    static const int mask[HCOV_MODES] = {7, 1, 2, 4, 8};
+    for (int md = 0; md < HCOV_MODES; ++md) {
         P.indeg[md].assign(ntk, 0);
         std::vector<std::pair<int64_t, int32_t>> rk[2];
         for (int32_t t = 0; t < ntk; ++t) {

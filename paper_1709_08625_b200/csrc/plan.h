@@ -55,21 +55,23 @@ struct Plan {
     std::vector<DCtr> ctr;           // SEG / PHWR contribution lists
 
     // ---- DAG ---------------------------------------------------------------------------
-    // Engine modes: 0 = all phases (hcov_eval), 1 = assembly (A3-A6), 2 = H-Cholesky (A7),
-    // 3 = forward solve (A8-A9).  Phase of a task: 0 assembly, 1 Cholesky, 2 root solve.
+    // Engine modes: 0 = phases 0-2 (hcov_eval), 1 = assembly (A3-A6), 2 = H-Cholesky (A7),
+    // 3 = forward solve (A8-A9), 4 = back-solve u = L~^{-T} v (NEXT (f1)).  Phase of a task:
+    // 0 assembly, 1 Cholesky, 2 root forward solve, 3 root back-solve.
     std::vector<DTask> tasks;
     std::vector<int8_t> phase;
     std::vector<int32_t> succ_off, succ;
-    std::vector<int32_t> indeg[4];       // dependencies inside the mode, per task
-    std::vector<int32_t> roots[4][2];    // initial ready tasks per mode and queue class
-    std::vector<int32_t> band_off;       // queue 0: HCOV_BANDS + 1 offsets of the bands' rings
-    std::vector<int32_t> q0init[4];      // queue 0 initial content per mode (-1 = empty slot)
-    std::vector<int32_t> q0tail[4];      // per mode: initial tail of each band
-    int32_t n_q[4][2] = {};              // non-NOP tasks per mode and queue class
+    std::vector<int32_t> indeg[HCOV_MODES];       // dependencies inside the mode, per task
+    std::vector<int32_t> roots[HCOV_MODES][2];    // initial ready tasks per mode and queue class
+    std::vector<int32_t> band_off;                // queue 0: HCOV_BANDS + 1 offsets of the bands' rings
+    std::vector<int32_t> q0init[HCOV_MODES];      // queue 0 initial content per mode (-1 = empty slot)
+    std::vector<int32_t> q0tail[HCOV_MODES];      // per mode: initial tail of each band
+    int32_t n_q[HCOV_MODES][2] = {};              // non-NOP tasks per mode and queue class
     int32_t crit_len = 0;                // longest dependency chain (tasks, NOPs excluded)
     int64_t max_rm = 0;                  // largest low-rank block
     int64_t max_mq = 0;                  // largest rows-per-member of a gang task
     int32_t root_solve = -1;
+    std::vector<int32_t> col_off, col_nodes;   // per leaf column segment: strictly-lower T/R leaves over it
 
     int64_t n_tiles() const { return (int64_t)tile_node.size(); }
     int64_t n_r() const { return (int64_t)rblk.size(); }

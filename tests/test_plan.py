@@ -113,9 +113,33 @@ def test_task_dag_is_consistent():
         info = T.info()
         t = T.tasks()
         assert t.shape[0] == info["n_tasks"]
-        assert set(np.unique(t[:, 0])) <= set(range(12))
-        assert set(np.unique(t[:, 1])) == {0, 1, 2}
-        # phases are ordered: assembly tasks first, the root forward solve last
+        assert set(np.unique(t[:, 0])) <= set(range(14))
+        assert set(np.unique(t[:, 1])) == {0, 1, 2, 3}
+        # phases are ordered: assembly tasks first, then the root forward solve, the back-solve last
         ph = t[:, 1]
         assert np.all(np.diff(ph[ph > 0]) >= 0)
         assert info["n_waves"] <= 12 * info["n_leaves"] + 64
+
+
+def test_backsolve_dag_is_the_transposed_solve():
+    """Phase 3 (root back-solve, NEXT (f1)): one BSEG per leaf segment, in reverse order, each
+    depending only on later segments / BPROJ tasks; one BPROJ per low-rank block."""
+    n = 4096
+    T = H.Tree(synth.uniform_points(n, 5))
+    info = T.info()
+    t = T.tasks()
+    off, sc = T.succ()
+    ph3 = np.nonzero(t[:, 1] == 3)[0]
+    bseg = ph3[t[ph3, 0] == 12]
+    bproj = ph3[t[ph3, 0] == 13]
+    assert len(bseg) == info["n_leaves"] and len(bproj) == info["n_lowrank"]
+    assert np.array_equal(t[bseg, 3], np.arange(info["n_leaves"])[::-1])
+    seg_of = {int(k): int(t[k, 3]) for k in bseg}
+    # edges into a BSEG come from BSEGs of larger segments, BPROJs or joins of phase 3 only
+    for k in range(len(t)):
+        for z in range(off[k], off[k + 1]):
+            d = sc[z]
+            if t[d, 1] == 3:
+                assert t[k, 1] == 3
+            if d in seg_of and k in seg_of:
+                assert seg_of[k] > seg_of[d]
