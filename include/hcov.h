@@ -75,7 +75,9 @@ typedef struct {
                              capacity was exhausted (full-pivot ACA capacity, or an intermediate
                              chunk recompression over 2 kcap; R22/R23).  0 on a clean run;
                              with kmax == 0 a nonzero count returns HCOV_ERR_RANK_CAPACITY. */
-    int32_t pad_;
+    int32_t interm_cuts;  /* with kmax > 0: the same capacity cuts, each keeping a rank >= kmax (every
+                             work capacity is >= kmax), so the cut is covered by the rank cap and is
+                             not an accuracy loss beyond it (R26) */
 } hcov_result;
 
 typedef struct {
@@ -179,6 +181,11 @@ hcov_status hcov_columns(hcov_hmat h, const int64_t *cols_host, int32_t m, doubl
  * ||C - C~||_F / ||C||_F (BASELINE north_star) at sizes the dense oracle cannot reach. */
 hcov_status hcov_cov_columns(hcov_tree t, const hcov_theta *theta, const int64_t *cols_host, int32_t m,
                              double *out_dev, hcov_stream stream);
+/* Device memory of an H-matrix handle (bytes), out8_host: [0] dense tiles, [1] U/V pools (rank
+ * capacity), [2] cores, [3] W pool capacity, [4] product-slot pool capacity, [5] W used by the last
+ * engine run, [6] product slots used, [7] pool overflows of the last run (> 0: it returned
+ * HCOV_ERR_OUT_OF_MEMORY).  The per-CTA engine scratch is shared by every handle (not counted). */
+hcov_status hcov_hmat_mem_info(hcov_hmat h, int64_t *out8_host);
 /* Diagnostics of an H-matrix: bytes of dense tiles and low-rank factors at actual ranks. */
 hcov_status hcov_hmat_storage(hcov_hmat h, int64_t *dense_bytes, int64_t *lowrank_bytes,
                               int32_t *max_rank);

@@ -44,7 +44,7 @@ class Result(ctypes.Structure):
     _fields_ = [("loglik", ctypes.c_double), ("logdet", ctypes.c_double), ("quad", ctypes.c_double),
                 ("n", ctypes.c_int64), ("max_rank", ctypes.c_int32), ("cap_binds", ctypes.c_int32),
                 ("min_pivot", ctypes.c_double), ("fail_leaf", ctypes.c_int64), ("acc_loss", ctypes.c_int32),
-                ("pad_", ctypes.c_int32)]
+                ("interm_cuts", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -86,6 +86,7 @@ _SIGS = {
     "hcov_sample": (_I32, [_P, _P, _P, _P]),
     "hcov_columns": (_I32, [_P, _P, _I32, _P, _P]),
     "hcov_hmat_storage": (_I32, [_P, _P, _P, _P]),
+    "hcov_hmat_mem_info": (_I32, [_P, _P]),
     "hcov_cov_columns": (_I32, [_P, _P, _P, _I32, _P, _P]),
     "hcov_forward_solve": (_I32, [_P, _P, _P, _P]),
     "hcov_backsolve": (_I32, [_P, _P, _P, _P]),
@@ -220,6 +221,7 @@ class _Borrowed:
 
     model_flops = None
     storage = None
+    mem_info = None
 
 
 def last_eval(tree: "Tree"):
@@ -229,6 +231,7 @@ def last_eval(tree: "Tree"):
     b = _Borrowed(tree, h)
     b.model_flops = HMatrix.model_flops.__get__(b)
     b.storage = HMatrix.storage.__get__(b)
+    b.mem_info = HMatrix.mem_info.__get__(b)
     return b
 
 
@@ -312,6 +315,13 @@ class HMatrix:
         d, l, m = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
         _check(lib().hcov_hmat_storage(self._h, ctypes.byref(d), ctypes.byref(l), ctypes.byref(m)), "hcov_hmat_storage")
         return {"dense_bytes": d.value, "lowrank_bytes": l.value, "max_rank": m.value}
+
+    def mem_info(self) -> dict:
+        """hcov_hmat_mem_info: device bytes of the handle's pools and their use by the last run."""
+        o = np.zeros(8, dtype=np.int64)
+        _check(lib().hcov_hmat_mem_info(self._h, o.ctypes.data), "hcov_hmat_mem_info")
+        return dict(zip(["tiles", "uv", "cores", "w_cap", "p_cap", "w_used", "p_used", "overflows"],
+                        [int(x) for x in o]))
 
 
 def cov_columns(tree: Tree, theta, cols: Sequence[int], stream=None):

@@ -9,6 +9,15 @@
 #include "hcov_internal.h"
 #include "la.cuh"
 
+// qctl layout (engine control words, hcov.cu)
+#define QC_HEAD1 0      // gang queue: next ticket
+#define QC_TAIL1 1      // gang queue: published tickets
+#define QC_ABORT 2      // watchdog / pool overflow: every CTA leaves its loop
+#define QC_DONE0 3      // completed queue-0 tasks
+#define QC_BHEAD 4      // HCOV_BANDS band heads
+#define QC_BTAIL (4 + HCOV_BANDS)
+#define QC_N (4 + 2 * HCOV_BANDS)
+
 // algorithmic flop counters per task class
 enum FlopCls { FC_ASM = 0, FC_TILE = 1, FC_TRUNC = 2, FC_SOLVE = 3, FC_PROD = 4, FC_N = 5 };
 
@@ -52,7 +61,9 @@ struct Ctx {
     double *logdet_part, *minpiv_part, *quad_part;
     int32_t *fail_leaf;        // min over failing leaves (init INT32_MAX)
     int32_t *flags;            // [0] cap binds, [1] rank overflow, [2] max rank, [3] accuracy losses
-                               // (a recompression cut below its tolerance: ACA or chunk capacity)
+                               // (a recompression cut below its tolerance for lack of work capacity,
+                               // kmax == 0), [4] the same cuts under a rank cap kmax > 0 (the kept
+                               // rank is >= kmax, so the cut is covered by the cap; not a loss)
     int32_t kcap, kmax;
     double eps;
     double interm_rel;         // intermediate (chunk) recompression tolerance, relative to eps (R22)
@@ -70,8 +81,12 @@ struct Ctx {
     int64_t gshared_off;       // offset (doubles) of the shared gang workspace in a gang CTA's scratch
     double *scr;               // per-CTA scratch (normal CTAs), scr_stride doubles each
     int64_t scr_stride;
-    double *bscr;              // per-CTA scratch of the big CTAs
-    int64_t bscr_stride;
+    double *bscr;              // big-member scratch: n_bgrp groups of HCOV_GANG member slots
+    int64_t bscr_stride;       // doubles per member slot
+    int32_t *bgrp_busy;        // per group: 1 while a gang holds it
+    int32_t *bgrp_cta;         // per CTA (member 0 of a gang): the group its gang holds
+    int32_t big_mq;            // gang members with more rows than this use a big-member slot
+    int32_t n_bgrp;
     double *flop;              // FC_N accumulators
     int64_t smem_dbl;          // dynamic shared memory of the engine (doubles)
     unsigned long long timeout_ns;
@@ -97,7 +112,13 @@ __device__ __forceinline__ const double *slot_get(const Ctx &c, int s) { return 
 __device__ __forceinline__ int64_t pool_bump(const Ctx &c, int which, int64_t size, int64_t cap)
 {
     int64_t off = (int64_t)atomicAdd(c.mem + which, (unsigned long long)size);
-    if (off + size > cap) { atomicAdd(c.mem + 2, 1ull); off = 0; }
+    if (off + size > cap) {
+        // overflow: counted, reported as out of memory; the engine is stopped at once (the
+        // aliased allocation below is never used for a result)
+        atomicAdd(c.mem + 2, 1ull);
+        atomicExch(c.qctl + QC_ABORT, 1u);
+        off = 0;
+    }
     return off;
 }
 // Product slot s of `size` doubles (single producer task; CTA-collective).
@@ -313,6 +334,11 @@ __device__ void record_rank(const Ctx &c, int r, int rk, int cb, int of)
     }
     __syncthreads();
 }
+
+// Index of the flag counting a recompression cut made for lack of work capacity: an accuracy
+// loss (flags[3]) without a rank cap, else a cut covered by the cap (flags[4]; every work capacity
+// is >= kmax).
+__device__ __forceinline__ int cut_flag(const Ctx &c) { return c.kmax > 0 ? 4 : 3; }
 
 __device__ __forceinline__ double final_tol(double eps, int R) { return eps / (10.0 * sqrt((double)(R > 0 ? R : 1))); }
 __device__ __forceinline__ double interm_tol(const Ctx &c) { return fmax(c.eps * c.interm_rel, 1e-15); }
@@ -809,6 +835,7 @@ __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *sme
         PH_BEGIN(tp);
         k = aca_partial(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, K, 0.1 * c.eps, used, red, redv, redi);
         PH_END(8, tp);
+        if (k == K && K < m && threadIdx.x == 0) atomicAdd(c.flags + cut_flag(c), 1);   // ACA not converged
         rk = compress(w, m, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m, &cb, &of,
                       red, redv, redi, smem, c.smem_dbl);
         record_rank(c, r, rk, cb, of);
@@ -819,6 +846,7 @@ __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *sme
         GangWs gw = make_gws(gg->shared, KB, gg->G);
         k = gang_aca(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, (uint8_t *)w.tail, K, 0.1 * c.eps, gw, *gg, red,
                      redv, redi);
+        if (k == K && K < m && gg->g == 0 && threadIdx.x == 0) atomicAdd(c.flags + cut_flag(c), 1);
         rk = gang_compress(w, gw, *gg, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m,
                            &cb, &of, red, redv, redi, smem, c.smem_dbl);
         if (gg->g == 0) record_rank(c, r, rk, cb, of);
@@ -1092,7 +1120,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         int k = aca_full(S, m, wd.X, wd.Y, KA, 0.1 * c.eps / (double)m, 0.1 * c.eps, red, redv, redi);
         PH_END(5, ta);
         fl += 2.0 * m * m * k;
-        if (k == KA && KA < m && threadIdx.x == 0) atomicAdd(c.flags + 3, 1);
+        if (k == KA && KA < m && threadIdx.x == 0) atomicAdd(c.flags + cut_flag(c), 1);
         int rk = compress(wd, m, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, U, V, m, &cb, &of, red, redv,
                           redi, smem, c.smem_dbl);
         fl += compress_flops(m, k, rk);
@@ -1131,7 +1159,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
                 rk = compress(w, m, cur, c.eps, interm_tol(c), false, 0, K - maxw, X2, Y2, m, &icb, &iof, red,
                               redv, redi, smem, c.smem_dbl);
             fl += (gg ? 1.0 / gg->G : 1.0) * compress_flops(m, cur, rk);
-            if (iof && threadIdx.x == 0 && (!gg || gg->g == 0)) atomicAdd(c.flags + 3, 1);
+            if (iof && threadIdx.x == 0 && (!gg || gg->g == 0)) atomicAdd(c.flags + cut_flag(c), 1);
             double *tx = w.X, *ty = w.Y;
             w.X = X2; w.Y = Y2; X2 = tx; Y2 = ty;
             cur = rk;
@@ -1193,7 +1221,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         fl += compress_flops(m, cur, rk);
     }
     if (!fin) {
-        if (of && threadIdx.x == 0 && (!gg || gg->g == 0)) atomicAdd(c.flags + 3, 1);
+        if (of && threadIdx.x == 0 && (!gg || gg->g == 0)) atomicAdd(c.flags + cut_flag(c), 1);
         cb = 0;
         of = 0;
     }

@@ -120,14 +120,6 @@ __device__ __forceinline__ unsigned long long gtimer()
 }
 __device__ __forceinline__ int ld_volatile(const int32_t *p) { return *(volatile const int32_t *)p; }
 
-// qctl layout
-#define QC_HEAD1 0      // gang queue: next ticket
-#define QC_TAIL1 1      // gang queue: published tickets
-#define QC_ABORT 2      // watchdog
-#define QC_DONE0 3      // completed queue-0 tasks
-#define QC_BHEAD 4      // HCOV_BANDS band heads
-#define QC_BTAIL (4 + HCOV_BANDS)
-#define QC_N (4 + 2 * HCOV_BANDS)
 
 __device__ __forceinline__ void push_ready(const Ctx &c, int32_t s)
 {
@@ -228,6 +220,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
         Gang gang{s_member, tk.qcls, c.gbar + t, c.qctl + QC_ABORT, 0, 0, 0, nullptr};
         Gang *gg = nullptr;
         double *tscr = scr;
+        bool use_big = false;
+        __shared__ int32_t s_bgrp;
         if (tk.qcls > 0) {
             // member 0 (the first entry of the gang) lends the shared workspace of its scratch
             __shared__ int32_t s_cta0;
@@ -249,6 +243,39 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
             __syncthreads();
             gg = &gang;
             gang.shared = c.scr + (int64_t)s_cta0 * c.scr_stride + c.gshared_off;
+            // members with more rows than the per-CTA scratch holds take a slot of a big-member
+            // group: once the gang has formed (all members present), member 0 claims a free group
+            // (only formed gangs hold groups, so a waiting gang never blocks the holder); member g
+            // uses slot g of it.  Released by member 0 after the task body (every member has passed
+            // the body's last gang barrier by then).
+            if (c.n_bgrp > 0 && (tk.type == TK_ACA || tk.type == TK_RAPP)) {
+                const int64_t m = c.rblk[tk.a].m;
+                const int64_t mq_last = m - (int64_t)(tk.qcls - 1) * (m / tk.qcls);
+                if (mq_last > c.big_mq) {
+                    gang_sync(gang);
+                    if (gang.g == 0 && threadIdx.x == 0) {
+                        int k = -1;
+                        unsigned ns = 64;
+                        const unsigned long long tw0 = gtimer();
+                        while (k < 0) {
+                            for (int q = 0; q < c.n_bgrp && k < 0; ++q)
+                                if (atomicCAS(c.bgrp_busy + q, 0, 1) == 0) k = q;
+                            if (k >= 0) break;
+                            if (ld_volatile((const int32_t *)c.qctl + QC_ABORT)) { k = 0; break; }
+                            if (gtimer() - tw0 > c.timeout_ns) { atomicExch(c.qctl + QC_ABORT, 1u); k = 0; break; }
+                            __nanosleep(ns);
+                            if (ns < 1024) ns <<= 1;
+                        }
+                        __stcg(c.bgrp_cta + blockIdx.x, k);
+                        s_bgrp = k;
+                    }
+                    gang_sync(gang);
+                    if (threadIdx.x == 0) s_bgrp = __ldcg(c.bgrp_cta + s_cta0);
+                    __syncthreads();
+                    tscr = c.bscr + ((int64_t)s_bgrp * HCOV_GANG + gang.g) * c.bscr_stride;
+                    use_big = true;
+                }
+            }
         }
         const unsigned long long t0 = gtimer();
         if (threadIdx.x == 0) {
@@ -278,6 +305,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
         }
         __threadfence();
         __syncthreads();
+        if (use_big && gang.g == 0 && threadIdx.x == 0) atomicExch(c.bgrp_busy + s_bgrp, 0);
         if (gang.g == 0) {
             if (threadIdx.x == 0) {
                 const unsigned long long t1 = gtimer();
@@ -642,7 +670,7 @@ struct hcov_hmat_s {
     double *tiles = nullptr, *U = nullptr, *V = nullptr, *cores = nullptr, *W = nullptr, *P = nullptr;
     double *vbuf = nullptr, *tbuf = nullptr, *logdet_part = nullptr, *minpiv_part = nullptr, *quad_part = nullptr;
     int32_t *rank = nullptr, *fail = nullptr, *flags = nullptr;
-    int32_t *indeg = nullptr, *q0 = nullptr, *q1 = nullptr, *gbar = nullptr, *gslot = nullptr;
+    int32_t *indeg = nullptr, *q0 = nullptr, *q1 = nullptr, *gbar = nullptr, *gslot = nullptr, *bgrp = nullptr;
     uint32_t *qctl = nullptr;
     double *scr = nullptr, *bscr = nullptr, *res = nullptr, *res_host = nullptr;
     double *ktab = nullptr;
@@ -653,11 +681,11 @@ struct hcov_hmat_s {
     void release_all()
     {
         void *ps[] = {tiles, U, V, cores, W, P, vbuf, tbuf, logdet_part, minpiv_part, quad_part, rank, fail, flags,
-                      indeg, q0, q1, gbar, gslot, qctl, scr, bscr, res, stats, woff, poff, mem};
+                      indeg, q0, q1, gbar, gslot, bgrp, qctl, scr, bscr, res, stats, woff, poff, mem};
         for (void *p : ps) cudaFree(p);
         tiles = U = V = cores = W = P = vbuf = tbuf = logdet_part = minpiv_part = quad_part = nullptr;
         wcap = pcap = 0;
-        rank = fail = flags = indeg = q0 = q1 = gbar = gslot = nullptr;
+        rank = fail = flags = indeg = q0 = q1 = gbar = gslot = bgrp = nullptr;
         qctl = nullptr;
         scr = bscr = res = nullptr;
         stats = nullptr;
@@ -806,7 +834,7 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     CK(cudaMalloc(&h->quad_part, P.n_leaves * sizeof(double)));
     CK(cudaMalloc(&h->rank, std::max<int64_t>(1, P.n_r()) * sizeof(int32_t)));
     CK(cudaMalloc(&h->fail, sizeof(int32_t)));
-    CK(cudaMalloc(&h->flags, 4 * sizeof(int32_t)));
+    CK(cudaMalloc(&h->flags, 5 * sizeof(int32_t)));
     const int64_t ntk = (int64_t)P.tasks.size();
     CK(cudaMalloc(&h->indeg, std::max<int64_t>(1, ntk) * sizeof(int32_t)));
     CK(cudaMalloc(&h->gbar, std::max<int64_t>(1, ntk) * sizeof(int32_t)));
@@ -831,15 +859,29 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     if (h->grid <= HCOV_BANDS * (HCOV_GANG - 1)) return HCOV_ERR_INVALID_ARG;
     // per-CTA scratch: single-CTA tasks (blocks < HCOV_GANG_MIN, 6 panels) or a gang member's rows
     // (m / G rows, 4 panels) followed by the gang's shared workspace (used when the CTA is member 0)
+    // members of more than HCOV_BIG_MQ rows (gangs on the largest blocks, m >= 8 * HCOV_BIG_MQ) use
+    // one of HCOV_BIG_GROUPS shared big-member groups instead
     const int64_t med_m = std::min<int64_t>(HCOV_GANG_MIN / 2, std::max<int64_t>(P.max_rm, 32));
-    int64_t gshared_off = 0, scr_stride = task_scratch(med_m, kcap);
+    int64_t gshared_off = 0, scr_stride = task_scratch(med_m, kcap), bstride = 0;
+    int nbg = 0;
     if (P.max_mq > 0) {
-        gshared_off = task_scratch(P.max_mq, kcap, 4);
+        gshared_off = task_scratch(std::min<int64_t>(P.max_mq, HCOV_BIG_MQ), kcap, 4);
         scr_stride = std::max<int64_t>(scr_stride, gshared_off + gang_shared_doubles(kbuf_of(kcap), HCOV_GANG));
+        if (P.max_mq > HCOV_BIG_MQ) {
+            bstride = task_scratch(P.max_mq, kcap, 4);
+            nbg = HCOV_BIG_GROUPS;
+        }
     }
     CK(cudaMalloc(&h->scr, scr_stride * (int64_t)h->grid * sizeof(double)));
+    CK(cudaMalloc(&h->bscr, std::max<int64_t>(1, bstride * HCOV_GANG * nbg) * sizeof(double)));
+    CK(cudaMalloc(&h->bgrp, (HCOV_BIG_GROUPS + h->grid) * sizeof(int32_t)));
+    CK(cudaMemset(h->bgrp, 0, (HCOV_BIG_GROUPS + h->grid) * sizeof(int32_t)));
     h->ctx.scr_stride = scr_stride;
-    h->ctx.bscr_stride = 0;
+    h->ctx.bscr_stride = bstride;
+    h->ctx.n_bgrp = nbg;
+    h->ctx.big_mq = HCOV_BIG_MQ;
+    h->ctx.bgrp_busy = h->bgrp;
+    h->ctx.bgrp_cta = h->bgrp + HCOV_BIG_GROUPS;
     h->ctx.gshared_off = gshared_off;
     h->kcap_alloc = kcap;
     return HCOV_OK;
@@ -901,7 +943,7 @@ void fill_ctx(hcov_hmat h)
     c.band_off = t->d_band_off;
     c.gslot = h->gslot;
     c.nbig = NBIG;
-    c.scr = h->scr; c.bscr = h->bscr;
+    c.scr = h->scr; c.bscr = h->bscr;   // (bscr_stride, n_bgrp, big_mq, bgrp_*: set by hmat_alloc)
     c.flop = nullptr;
     c.smem_dbl = h->smem / (int64_t)sizeof(double);
     const char *wd = std::getenv("HCOV_WATCHDOG_S");
@@ -990,7 +1032,7 @@ hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trun
     fill_ctx(h);
     Plan &P = t->P;
     CK(cudaMemsetAsync(h->rank, 0, std::max<int64_t>(1, P.n_r()) * sizeof(int32_t), st));
-    CK(cudaMemsetAsync(h->flags, 0, 4 * sizeof(int32_t), st));
+    CK(cudaMemsetAsync(h->flags, 0, 5 * sizeof(int32_t), st));
     CK(cudaMemsetAsync(h->fail, 0x7f, sizeof(int32_t), st));
     CK(cudaMemsetAsync(h->quad_part, 0, P.n_leaves * sizeof(double), st));
     CK(cudaMemsetAsync(h->woff, 0xff, std::max<size_t>(1, P.phw.size()) * sizeof(int64_t), st));
@@ -1006,10 +1048,10 @@ hcov_status check_abort(hcov_hmat h, cudaStream_t st, int32_t *hf)
     CK(cudaMemcpyAsync(mem, h->mem, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&ab, h->qctl + QC_ABORT, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf, h->fail, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hf + 1, h->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hf + 1, h->flags, 5 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (mem[2]) return HCOV_ERR_OUT_OF_MEMORY;   // a pool overflow also raises the abort flag
     if (ab) return HCOV_ERR_CUDA;
-    if (mem[2]) return HCOV_ERR_OUT_OF_MEMORY;
     return HCOV_OK;
 }
 
@@ -1018,7 +1060,7 @@ hcov_status finish_result(hcov_hmat h, cudaStream_t st, hcov_result *out)
     Plan &P = h->t->P;
     LAUNCH(PC_REDUCE, st, k_reduce<<<1, NT, 0, st>>>(h->ctx, h->res));
     CK(cudaGetLastError());
-    int32_t hf[5];
+    int32_t hf[6];
     CK(cudaMemcpyAsync(h->res_host, h->res, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     hcov_status s = check_abort(h, st, hf);
     if (s) return s;
@@ -1033,6 +1075,7 @@ hcov_status finish_result(hcov_hmat h, cudaStream_t st, hcov_result *out)
     out->cap_binds = hf[1];
     out->max_rank = hf[3];
     out->acc_loss = hf[4];
+    out->interm_cuts = hf[5];
     if (out->fail_leaf >= 0) { out->loglik = -INFINITY; return HCOV_ERR_NOT_SPD; }
     if ((hf[2] > 0 || hf[4] > 0) && h->trunc.kmax == 0) { out->loglik = -INFINITY; return HCOV_ERR_RANK_CAPACITY; }
     return HCOV_OK;
@@ -1183,7 +1226,7 @@ hcov_status hcov_assemble(hcov_tree t, const hcov_theta *theta, const hcov_trunc
     s = assemble_setup(h, theta, trunc, st);
     if (!s) s = engine_run(h, 1, st);
     if (!s) {
-        int32_t hf[5];
+        int32_t hf[6];
         s = check_abort(h, st, hf);
     }
     if (s) { delete h; return s; }
@@ -1199,7 +1242,7 @@ hcov_status hcov_cholesky(hcov_hmat h, hcov_stream stream, int64_t *fail_leaf)
     cudaStream_t st = (cudaStream_t)stream;
     hcov_status s = engine_run(h, 2, st);
     if (s) return s;
-    int32_t hf[5];
+    int32_t hf[6];
     if ((s = check_abort(h, st, hf))) return s;
     h->state = 2;
     int64_t fl = (hf[0] == 0x7f7f7f7f) ? -1 : hf[0];
@@ -1268,7 +1311,7 @@ hcov_status solve_ext(hcov_hmat h, const double *in, double *out, bool fwd, bool
     if (fwd && (s = engine_run(h, 3, st))) return s;
     if (back && (s = engine_run(h, 4, st))) return s;
     LAUNCH(PC_AUX, st, k_permute_out<<<256, 256, 0, st>>>(h->ctx, h->vbuf, out));
-    int32_t hf[5];
+    int32_t hf[6];
     return check_abort(h, st, hf);
 }
 
@@ -1481,6 +1524,24 @@ hcov_status hcov_cov_columns(hcov_tree t, const hcov_theta *theta, const int64_t
     cudaError_t e = cudaStreamSynchronize(st);
     cudaFree(d_pc);
     if (e != cudaSuccess) return map_err(e);
+    return HCOV_OK;
+}
+
+hcov_status hcov_hmat_mem_info(hcov_hmat h, int64_t *out)
+{
+    if (!h || !out) return HCOV_ERR_INVALID_ARG;
+    const Plan &P = h->t->P;
+    const int64_t kc = std::max(0, h->kcap_alloc);
+    unsigned long long mem[4] = {0, 0, 0, 0};
+    if (h->mem) CK(cudaMemcpy(mem, h->mem, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    out[0] = P.n_tiles() * HCOV_TILE * 8;
+    out[1] = 2 * P.uv_elems * kc * 8;
+    out[2] = (int64_t)P.n_cores * kc * kc * 8;
+    out[3] = h->wcap * 8;
+    out[4] = h->pcap * 8;
+    out[5] = (int64_t)mem[0] * 8;
+    out[6] = (int64_t)mem[1] * 8;
+    out[7] = (int64_t)mem[2];
     return HCOV_OK;
 }
 

@@ -10,6 +10,8 @@
                               // formed gang per band can hold CTAs, so every gang eventually forms)
 #define HCOV_DENSE_MAX 256    // low-rank blocks up to this size are recompressed from a dense accumulation
 #define HCOV_SMEM_DBL 28160 // dynamic shared memory of the engine CTA (220 KB + static <= 227 KB; one 512-thread CTA per SM)
+#define HCOV_BIG_MQ 4096      // gang members with more rows use a big-member scratch slot (hcov.cu)
+#define HCOV_BIG_GROUPS 4     // big-member groups (HCOV_GANG slots each)
 #define HCOV_GANG_MIN 512     // low-rank blocks from this size on are processed by gangs of min(8, m/256) CTAs
 
 // Block-tree node types (lower triangle incl. diagonal).

@@ -8,7 +8,7 @@ Sec. 8(c) pins), and the exact collinear Ornstein-Uhlenbeck likelihood at the he
   hcov_columns.
 * collinear exponential model, tau^2 = 0: the exact O(n) Markov likelihood at n = 2,097,152
   (SURVEY 8(c) "strongest pin for C5-scale code paths": every admissible block has rank 1).
-* R22 (intermediate chunk tolerance eps * 1e-2): n = 32,768 (blocks up to 4,096 rows recompressed
+* R22 (intermediate chunk tolerance eps * 1e-2): n = 16,384 (blocks up to 2,048 rows recompressed
   in many chunks) against the dense oracle, at 1e-2 and at 1e-4.
 """
 import math
@@ -51,14 +51,15 @@ def test_c3_sampled_columns():
 
 
 def test_c3_evaluation_and_chi2():
-    """C3 as BASELINE writes it: Z from a tight (eps_gen = 1e-10, uncapped) H-Cholesky factor, one
+    """C3 as BASELINE writes it: Z from a tight uncapped H-Cholesky factor (eps_gen = 1e-9: the
+    row-15 value 1e-10 is not SPD under the method on C3's clustered points, R25), one
     evaluation at eps = 1e-6, k = 16.  At theta_gen, q = Z^T C~^{-1} Z ~ chi^2_n: |q - n| <= 5 sqrt(2n)
     (SURVEY 8(c) pin (vi)) for the tight factor itself."""
     cfg = synth.CONFIGS["C3"]
     s = synth.points(cfg)
     th = (cfg.sigma2, cfg.ell, cfg.nu, cfg.nugget)
     T = H.Tree(_dev(s))
-    hg = H.HMatrix(T, th, 1e-10, kmax=0, kcap=64)
+    hg = H.HMatrix(T, th, synth.EPS_GEN["C3"], kmax=0, kcap=64)
     assert hg.cholesky() == -1
     Z = hg.sample(_dev(synth.xi(cfg.n, cfg.seed_xi)))
     rt = hg.loglik(Z)
@@ -106,10 +107,11 @@ def test_collinear_ou_exact_2M():
 def test_intermediate_tolerance_many_chunks(interm, monkeypatch):
     """R22: the intermediate recompressions of a block's Schur updates at eps * interm (relative to the
     partial sum) must not cost the final eps accuracy when the Schur complement is much smaller than
-    the block (smooth kernel, C5's nu = 1, ell = 0.05; n = 32,768: blocks of 512-4,096 rows, each
-    updated in many chunks) — against the dense oracle."""
+    the block (smooth kernel, C5's nu = 1, ell = 0.05; n = 16,384: blocks of 512-2,048 rows, each
+    updated in many chunks) — against the dense oracle.  (At n = 32,768 this kernel with tau^2 = 1e-6
+    is not numerically SPD even for the dense fp64 oracle.)"""
     monkeypatch.setenv("HCOV_INTERM_REL", interm)
-    n = 32768
+    n = 16384
     s = synth.uniform_points(n, 91)
     th = (1.0, 0.05, 1.0, 1e-6)
     Z = oracle.sample_dense(s, synth.xi(n, 92), *th)
