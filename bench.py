@@ -52,6 +52,9 @@ def _args():
     p.add_argument("--kmax", type=int, default=-1, help="override the rank cap (-1 = the workload's)")
     p.add_argument("--acc-cols", type=int, default=64, help="sampled columns for ||C - C~||_F / ||C||_F")
     p.add_argument("--out", default="", help="also write the JSON line to this file")
+    p.add_argument("--cands-per-rank", type=int, default=1,
+                   help="theta candidates per rank and step (> 1: hcov_mle_batch runs them in shared engine "
+                        "launches); the batch is the config's theta with ell log-spaced in ell*[0.8, 1.25]")
     return p.parse_args()
 
 
@@ -244,8 +247,14 @@ def run_hcov(args, cfg, rank: int, world: int):
     if Z is None:
         raise RuntimeError(f"could not generate Z: {gen_mem}")
     eps_gen = gen
-    m_total = max(1, world)
-    my_theta = th0 if m_total == 1 else (th0[0], th0[1] * 0.8 * (1.25 / 0.8) ** (rank / (m_total - 1)), th0[2], th0[3])
+    # theta candidates of one step: m_total = world x cands-per-rank, candidate j on rank j mod world
+    # (SURVEY 8(e)); a single candidate is the config's theta
+    cpr = max(1, args.cands_per_rank)
+    m_total = world * cpr
+    all_thetas = [_theta_for(type("T", (), {"sigma2": th0[0], "ell": th0[1], "nu": th0[2], "nugget": th0[3]}), j, m_total)
+                  for j in range(m_total)]
+    my_thetas = all_thetas[rank::world]
+    my_theta = my_thetas[0]
 
     # accuracy of the evaluated C~ (north_star: ||C - C~||_F / ||C||_F <= 10 eps on sampled columns),
     # both sides on the device: C~ e_j from the assembled H-matrix, C e_j by direct Eq. (3) evaluation
@@ -263,10 +272,18 @@ def run_hcov(args, cfg, rank: int, world: int):
                "C_tilde_max_rank": st_c["max_rank"]}
 
     def step():
-        return H.eval_loglik(tree, my_theta, Z, eps, kmax)
+        if cpr == 1:
+            r = H.eval_loglik(tree, my_theta, Z, eps, kmax)
+            return r, [r["loglik"]]
+        ll, st = H.mle_batch(tree, Z, my_thetas, eps, kmax)
+        if any(int(x) != 0 for x in st):
+            raise RuntimeError(f"candidate rejected: {list(st)}")
+        return None, list(ll)
 
     for _ in range(max(3, args.warmup)):
-        r = step()
+        r, lls = step()
+    if cpr > 1:   # the first candidate once more on its own: result fields and the work model below
+        r = H.eval_loglik(tree, my_theta, Z, eps, kmax)
     if r["status"] != 0:
         raise RuntimeError(f"evaluation failed: {r}")
     # ---- timed region -----------------------------------------------------------------------
@@ -278,10 +295,10 @@ def run_hcov(args, cfg, rank: int, world: int):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        r = step()
-        if dist:
-            t = torch.tensor([r["loglik"]], dtype=torch.float64, device=dev)
-            g = torch.empty(world, dtype=torch.float64, device=dev)
+        _, lls = step()
+        if dist:   # every rank receives all m_total values (the MLE update input)
+            t = torch.tensor(lls, dtype=torch.float64, device=dev)
+            g = torch.empty(world * cpr, dtype=torch.float64, device=dev)
             dist.all_gather_into_tensor(g, t)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -296,7 +313,9 @@ def run_hcov(args, cfg, rank: int, world: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * args.steps / (ms * 1e-3)
+    value = m_total * args.steps / (ms * 1e-3)
+    if cpr > 1:
+        H.eval_loglik(tree, my_theta, Z, eps, kmax)   # (outside the clock) the handle of the work model
     last = H.last_eval(tree)
     model = last.model_flops()
     st_l = last.storage()
@@ -307,20 +326,34 @@ def run_hcov(args, cfg, rank: int, world: int):
     k_e = max(1, min(args.steps, 2))
     if dist:
         dist.barrier()
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(k_e):
-        Zd.copy_(Zh, non_blocking=True)
-        r2 = H.eval_loglik(tree, my_theta, Zd, eps, kmax)    # returns host scalars (D2H inside)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms_e2e = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
-    e2e = {"value": world * k_e / (ms_e2e * 1e-3), "unit": "evals/s", "h2d_bytes_per_step": 8 * n,
-           "d2h_bytes_per_step": 3 * 8}
+    if cpr == 1:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(k_e):
+            Zd.copy_(Zh, non_blocking=True)
+            H.eval_loglik(tree, my_theta, Zd, eps, kmax)    # returns host scalars (D2H inside)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+    else:   # e2e of the batch: host Z copied in, the m values read back
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(k_e):
+            Zd.copy_(Zh, non_blocking=True)
+            H.mle_batch(tree, Zd, my_thetas, eps, kmax)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+    e2e = {"value": m_total * k_e / (ms_e2e * 1e-3), "unit": "evals/s", "h2d_bytes_per_step": 8 * n,
+           "d2h_bytes_per_step": 3 * 8 if cpr == 1 else 12 * cpr}
 
     # ---- roofline of the dominant kernel (k_engine, one launch per step) ---------------------
     # achieved = SURVEY Sec. 8(d)'s method-work model at the measured ranks (hcov_model_flops) per
@@ -354,6 +387,7 @@ def run_hcov(args, cfg, rank: int, world: int):
                       "theta_note": note, "config_as_written": {"name": cfg.name, "nu": cfg.nu, "ell": cfg.ell,
                                                                 "eps": cfg.eps[0], "kmax": cfg.kmax},
                       "leaf": 32, "eta": 2.0, "parallelism": f"theta-batch dp{world}",
+                      "candidates_per_step": m_total, "candidates_per_rank": cpr,
                       "l2": "inputs larger than L2 (H-matrix >> 126 MB)",
                       "tree": {k: info[k] for k in ("depth", "n_dense_tiles", "n_lowrank", "n_tasks", "n_waves")}},
            "loglik": r["loglik"], "logdet": r["logdet"], "quad": r["quad"], "max_rank": r["max_rank"],

@@ -44,7 +44,7 @@ struct Ctx {
     const int32_t *diag_tile;
     const double *xs, *ys;
     const int64_t *perm_i2e;
-    int32_t depth, n_r, root_solve, pad0;
+    int32_t depth, n_r, root_solve, ntasks;
     int64_t n_pad, n_leaves, n_real, n_tiles;
     // ---- numeric (per H-matrix) ----
     double *tiles;
@@ -70,11 +70,11 @@ struct Ctx {
     MaternParams mp;
     // ---- engine ----
     int32_t *indeg;            // working copy of the in-degrees
-    int32_t *queue[2];         // [0]: HCOV_BANDS priority rings (band_off), [1]: gang tickets
+    int32_t *queue[2];         // [0]: HCOV_BANDS priority rings (band_off x ninst), [1]: unused
     const int32_t *band_off;   // HCOV_BANDS + 1
     uint32_t *qctl;            // see QC_* in hcov.cu
     int32_t nq[2];
-    int32_t nbig;              // CTAs serving queue 1 (HCOV_GANG * HCOV_GANG_SLOTS)
+    int32_t ninst;             // instances (H-matrices of one tree) run by this engine launch
     int32_t pad1;
     int32_t *gbar;             // per-task gang barrier counters
     int32_t *gslot;            // per-task: CTA index of the gang's member 0 (-1 until it joined)

@@ -121,17 +121,24 @@ __device__ __forceinline__ unsigned long long gtimer()
 __device__ __forceinline__ int ld_volatile(const int32_t *p) { return *(volatile const int32_t *)p; }
 
 
-__device__ __forceinline__ void push_ready(const Ctx &c, int32_t s)
+// Queue entries: (global task id << QE_SHIFT) | gang member, global task id = instance * ntasks +
+// task (an engine launch runs the DAGs of c.ninst H-matrices of the same tree: a theta batch).  A
+// gang task of G CTAs occupies G consecutive entries.  Band b of the ring holds ninst x its
+// per-instance capacity.
+#define QE_SHIFT 3
+__device__ __forceinline__ void push_ready(const Ctx &c, int32_t inst, int32_t s)
 {
-    // entries are task * 32 + member; a gang task of G CTAs occupies G consecutive entries
     const int b = c.tasks[s].band;
     const int G = max(1, c.tasks[s].qcls);
     const uint32_t pos = atomicAdd(c.qctl + QC_BTAIL + b, (uint32_t)G);
-    for (int g = 0; g < G; ++g) atomicExch(c.queue[0] + c.band_off[b] + pos + g, s * 32 + g);
+    int32_t *q = c.queue[0] + (int64_t)c.band_off[b] * c.ninst + pos;
+    const int32_t e0 = (inst * c.ntasks + s) << QE_SHIFT;
+    for (int g = 0; g < G; ++g) atomicExch(q + g, e0 + g);
 }
 
-// Release the successors of task t (all threads of the CTA; NOP joins complete inline).
-__device__ void release(const Ctx &c, int32_t t, int mask, const int8_t *phase)
+// Release the successors of task t of instance inst (all threads of the CTA; NOP joins complete
+// inline).  c: the instance's context (its in-degrees).
+__device__ void release(const Ctx &c, int32_t inst, int32_t t, int mask, const int8_t *phase)
 {
     const int b = c.succ_off[t], e = c.succ_off[t + 1];
     for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
@@ -143,81 +150,80 @@ __device__ void release(const Ctx &c, int32_t t, int mask, const int8_t *phase)
         stack[sp++] = s;
         while (sp > 0) {
             int32_t u = stack[--sp];
-            if (c.tasks[u].type != TK_NOP) { push_ready(c, u); continue; }
+            if (c.tasks[u].type != TK_NOP) { push_ready(c, inst, u); continue; }
             __threadfence();
             for (int z = c.succ_off[u]; z < c.succ_off[u + 1]; ++z) {
                 int32_t v = c.succ[z];
                 if (!(mask & (1 << phase[v]))) continue;
                 if (atomicSub(c.indeg + v, 1) == 1) {
                     if (sp < 24) stack[sp++] = v;
-                    else push_ready(c, v);
+                    else push_ready(c, inst, v);
                 }
             }
         }
     }
 }
 
-__global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const int8_t *phase, EngineStats *stats,
-                                               unsigned long long *tl)
+// The persistent engine: every CTA claims the head entry of the most urgent non-empty band, runs
+// the task with its instance's context (copied to shared memory), releases the successors.
+// c: engine-level fields (queue, control words, scratch; identical in every instance context);
+// ictx[i]: the full context of instance i.
+__global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, const Ctx *__restrict__ ictx, int mask,
+                                                         const int8_t *phase, EngineStats *stats,
+                                                         unsigned long long *tl)
 {
     extern __shared__ double smem[];
     __shared__ double red[NWARP], redv[NWARP];
     __shared__ int64_t redi[NWARP];
-    __shared__ int32_t s_task, s_member;
-    const int q = (blockIdx.x < c.nbig) ? 1 : 0;
-    double *scr = c.scr + (int64_t)(blockIdx.x - c.nbig) * c.scr_stride;
+    __shared__ int32_t s_entry;
+    __shared__ Ctx s_ctx;
+    double *scr = c.scr + (int64_t)blockIdx.x * c.scr_stride;
     double fl[FC_N] = {0, 0, 0, 0, 0};
     unsigned long long busy[TK_NTYPES] = {}, cnt[TK_NTYPES] = {};
+    const int ninst = c.ninst;
     while (true) {
         if (threadIdx.x == 0) {
-            int32_t t = -1;
-            uint32_t pos = 0;
+            int32_t v = -1;
             const unsigned long long t0 = gtimer();
             unsigned ns = 32;
-            if (q == 1) {
-                // gang queue: claim the next ticket, wait until it is published
-                pos = atomicAdd(c.qctl + QC_HEAD1, 1u);
-                if (pos < (uint32_t)c.nq[1]) {
-                    while ((t = ld_volatile(c.queue[1] + pos)) < 0) {
-                        if (ld_volatile((const int32_t *)c.qctl + QC_ABORT)) { t = -1; break; }
-                        __nanosleep(ns);
-                        if (ns < 256) ns <<= 1;
-                        if (gtimer() - t0 > c.timeout_ns) { atomicExch(c.qctl + QC_ABORT, 1u); t = -1; break; }
+            // take the head of the most urgent non-empty band (try-claim by CAS)
+            while (true) {
+                if (ld_volatile((const int32_t *)c.qctl + QC_DONE0) >= c.nq[0]) break;
+                if (ld_volatile((const int32_t *)c.qctl + QC_ABORT)) break;
+                bool got = false;
+                for (int b = HCOV_BANDS - 1; b >= 0 && !got; --b) {
+                    const int64_t base = (int64_t)c.band_off[b] * ninst;
+                    const uint32_t cap = (uint32_t)((c.band_off[b + 1] - c.band_off[b]) * ninst);
+                    while (true) {
+                        const uint32_t h = (uint32_t)ld_volatile((const int32_t *)c.qctl + QC_BHEAD + b);
+                        if (h >= cap) break;
+                        const int32_t e = ld_volatile(c.queue[0] + base + h);
+                        if (e < 0) break;
+                        if (atomicCAS(c.qctl + QC_BHEAD + b, h, h + 1) == h) { v = e; got = true; break; }
                     }
                 }
-            } else {
-                // queue 0: take the head of the most urgent non-empty band (try-claim by CAS)
-                while (true) {
-                    if (ld_volatile((const int32_t *)c.qctl + QC_DONE0) >= c.nq[0]) break;
-                    if (ld_volatile((const int32_t *)c.qctl + QC_ABORT)) break;
-                    bool got = false;
-                    for (int b = HCOV_BANDS - 1; b >= 0 && !got; --b) {
-                        const int32_t base = c.band_off[b], cap = c.band_off[b + 1] - base;
-                        while (true) {
-                            const uint32_t h = (uint32_t)ld_volatile((const int32_t *)c.qctl + QC_BHEAD + b);
-                            if (h >= (uint32_t)cap) break;
-                            const int32_t v = ld_volatile(c.queue[0] + base + h);
-                            if (v < 0) break;
-                            if (atomicCAS(c.qctl + QC_BHEAD + b, h, h + 1) == h) { t = v; got = true; break; }
-                        }
-                    }
-                    if (got) break;
-                    __nanosleep(ns);
-                    if (ns < 256) ns <<= 1;
-                    if (gtimer() - t0 > c.timeout_ns) { atomicExch(c.qctl + QC_ABORT, 1u); break; }
-                }
+                if (got) break;
+                __nanosleep(ns);
+                if (ns < 256) ns <<= 1;
+                if (gtimer() - t0 > c.timeout_ns) { atomicExch(c.qctl + QC_ABORT, 1u); break; }
             }
             __threadfence();
-            s_member = 0;
-            if (t >= 0) { s_member = t & 31; t >>= 5; }
-            s_task = t;
-            (void)pos;
+            s_entry = v;
         }
         __syncthreads();
-        const int32_t t = s_task;
-        if (t < 0) break;
+        const int32_t v = s_entry;
+        if (v < 0) break;
+        const int32_t gt = v >> QE_SHIFT, member = v & ((1 << QE_SHIFT) - 1);
+        const int32_t inst = gt / c.ntasks, t = gt - inst * c.ntasks;
+        {
+            const unsigned long long *src = (const unsigned long long *)(ictx + inst);
+            unsigned long long *dst = (unsigned long long *)&s_ctx;
+            for (int k = threadIdx.x; k < (int)(sizeof(Ctx) / 8); k += NT) dst[k] = __ldg(src + k);
+        }
+        __syncthreads();
+        const Ctx &ci = s_ctx;
         const DTask tk = c.tasks[t];
-        Gang gang{s_member, tk.qcls, c.gbar + t, c.qctl + QC_ABORT, 0, 0, 0, nullptr};
+        Gang gang{member, tk.qcls, ci.gbar + t, c.qctl + QC_ABORT, 0, 0, 0, nullptr};
         Gang *gg = nullptr;
         double *tscr = scr;
         bool use_big = false;
@@ -227,16 +233,16 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
             __shared__ int32_t s_cta0;
             if (threadIdx.x == 0) {
                 if (gang.g == 0) {
-                    atomicExch(c.gslot + t, (int32_t)blockIdx.x);
+                    atomicExch(ci.gslot + t, (int32_t)blockIdx.x);
                     s_cta0 = blockIdx.x;
                 } else {
-                    int32_t v;
-                    while ((v = ld_volatile(c.gslot + t)) < 0) {
+                    int32_t w;
+                    while ((w = ld_volatile(ci.gslot + t)) < 0) {
                         if (ld_volatile((const int32_t *)c.qctl + QC_ABORT)) break;
                         __nanosleep(64);
                     }
-                    if (v < 0) v = blockIdx.x;   // aborted: the task body exits at its first gang barrier
-                    s_cta0 = v;
+                    if (w < 0) w = blockIdx.x;   // aborted: the task body exits at its first gang barrier
+                    s_cta0 = w;
                 }
                 __threadfence();
             }
@@ -288,19 +294,19 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
         }
         __syncthreads();
         switch (tk.type) {
-        case TK_FILL: task_fill(c, tk, fl[FC_ASM]); break;
-        case TK_ACA: task_aca(c, tk, tscr, smem, red, redv, redi, fl[FC_ASM], fl[FC_TRUNC], gg); break;
+        case TK_FILL: task_fill(ci, tk, fl[FC_ASM]); break;
+        case TK_ACA: task_aca(ci, tk, tscr, smem, red, redv, redi, fl[FC_ASM], fl[FC_TRUNC], gg); break;
         case TK_TAPP:
         case TK_POTRF:
-        case TK_TRSM: task_tile(c, tk, smem, fl[FC_TILE]); break;
-        case TK_RAPP: task_rapp(c, tk, tscr, smem, red, redv, redi, fl[FC_TRUNC], gg); break;
-        case TK_SEG: task_seg(c, tk, smem, fl[FC_SOLVE]); break;
-        case TK_PROJ: task_proj(c, tk, smem, fl[FC_SOLVE]); break;
-        case TK_PRR: task_prr(c, tk, fl[FC_PROD]); break;
-        case TK_PHWP: task_phwp(c, tk, fl[FC_PROD]); break;
-        case TK_PHWR: task_phwr(c, tk, smem, fl[FC_PROD]); break;
-        case TK_BSEG: task_bseg(c, tk, smem, fl[FC_SOLVE]); break;
-        case TK_BPROJ: task_bproj(c, tk, fl[FC_SOLVE]); break;
+        case TK_TRSM: task_tile(ci, tk, smem, fl[FC_TILE]); break;
+        case TK_RAPP: task_rapp(ci, tk, tscr, smem, red, redv, redi, fl[FC_TRUNC], gg); break;
+        case TK_SEG: task_seg(ci, tk, smem, fl[FC_SOLVE]); break;
+        case TK_PROJ: task_proj(ci, tk, smem, fl[FC_SOLVE]); break;
+        case TK_PRR: task_prr(ci, tk, fl[FC_PROD]); break;
+        case TK_PHWP: task_phwp(ci, tk, fl[FC_PROD]); break;
+        case TK_PHWR: task_phwr(ci, tk, smem, fl[FC_PROD]); break;
+        case TK_BSEG: task_bseg(ci, tk, smem, fl[FC_SOLVE]); break;
+        case TK_BPROJ: task_bproj(ci, tk, fl[FC_SOLVE]); break;
         default: break;
         }
         __threadfence();
@@ -311,13 +317,11 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
                 const unsigned long long t1 = gtimer();
                 busy[tk.type] += t1 - t0;
                 cnt[tk.type] += 1;
-                if (tl) { tl[3 * (int64_t)t] = t0; tl[3 * (int64_t)t + 1] = t1; tl[3 * (int64_t)t + 2] = blockIdx.x; }
+                if (tl && ninst == 1) { tl[3 * (int64_t)t] = t0; tl[3 * (int64_t)t + 1] = t1; tl[3 * (int64_t)t + 2] = blockIdx.x; }
             }
-            release(c, t, mask, phase);
-            if (q == 0) {
-                __syncthreads();
-                if (threadIdx.x == 0) { __threadfence(); atomicAdd(c.qctl + QC_DONE0, 1u); }
-            }
+            release(ci, inst, t, mask, phase);
+            __syncthreads();
+            if (threadIdx.x == 0) { __threadfence(); atomicAdd(c.qctl + QC_DONE0, 1u); }
         }
         __syncthreads();
     }
@@ -333,22 +337,41 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, int mask, const 
     }
 }
 
-__global__ void k_reset(Ctx c, const int32_t *indeg_mode, int64_t ntasks, const int32_t *q0init, int64_t q0len,
-                        const int32_t *q0tail, const int32_t *roots1, int32_t nr1, int64_t qcap1)
+// Per instance: working in-degrees of the mode, gang barriers and member-0 slots.
+__global__ void k_reset_inst(Ctx c, const int32_t *indeg_mode, int64_t ntasks)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    for (int64_t k = tid; k < ntasks; k += stride) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntasks; k += stride) {
         c.indeg[k] = indeg_mode[k];
         c.gbar[k] = 0;
         c.gslot[k] = -1;
     }
-    for (int64_t k = tid; k < q0len; k += stride) c.queue[0][k] = q0init[k];
-    for (int64_t k = tid; k < qcap1; k += stride) c.queue[1][k] = (k < nr1) ? roots1[k] : -1;
+}
+
+// The batch's ready queue: band b holds, for instance 0, 1, ..., the mode's initially ready entries
+// of the band (q0init, plan order), then -1; control words reset (band tails = ninst x initial).
+__global__ void k_qinit(Ctx c, const int32_t *q0init, const int32_t *q0tail)
+{
+    const int ninst = c.ninst;
+    const int64_t total = (int64_t)c.band_off[HCOV_BANDS] * ninst;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int64_t p = tid; p < total; p += stride) {
+        int b = 0;
+        while (b + 1 < HCOV_BANDS && (int64_t)c.band_off[b + 1] * ninst <= p) ++b;
+        const int64_t local = p - (int64_t)c.band_off[b] * ninst;
+        const int64_t qt = q0tail[b];
+        int32_t e = -1;
+        if (local < qt * ninst) {
+            const int64_t inst = local / qt, k = local - inst * qt;
+            const int32_t v = q0init[c.band_off[b] + k];   // plan entries: task * 32 + member
+            e = (int32_t)(((inst * c.ntasks + (v >> 5)) << QE_SHIFT) | (v & 31));
+        }
+        c.queue[0][p] = e;
+    }
     if (tid < QC_N) {
         uint32_t v = 0;
-        if (tid == QC_TAIL1) v = (uint32_t)nr1;
-        if (tid >= QC_BTAIL && tid < QC_BTAIL + HCOV_BANDS) v = (uint32_t)q0tail[tid - QC_BTAIL];
+        if (tid >= QC_BTAIL && tid < QC_BTAIL + HCOV_BANDS) v = (uint32_t)(q0tail[tid - QC_BTAIL] * ninst);
         c.qctl[tid] = v;
     }
 }
@@ -622,6 +645,32 @@ __global__ void __launch_bounds__(NT) k_test_truncate(double *scr, int64_t m, in
 // ------------------------------------------------------------------------------------------
 // handles
 // ------------------------------------------------------------------------------------------
+// Engine resources shared by every H-matrix of a tree (one persistent launch at a time per tree):
+// per-CTA scratch, big-member groups, the ready queue and control words, the per-instance
+// context array of a batched launch, statistics.
+struct Engine {
+    int kcap = -1, grid = 0, ninst_cap = 0, nbg = 0;
+    int64_t smem = 0, scr_stride = 0, bstride = 0, gshared_off = 0;
+    double *scr = nullptr, *bscr = nullptr;
+    int32_t *bgrp = nullptr, *q0 = nullptr, *q1 = nullptr;
+    uint32_t *qctl = nullptr;
+    Ctx *d_ctx = nullptr;
+    EngineStats *stats = nullptr, *stats_host = nullptr;
+    void release()
+    {
+        void *ps[] = {scr, bscr, bgrp, q0, q1, qctl, d_ctx, stats};
+        for (void *p : ps) cudaFree(p);
+        if (stats_host) cudaFreeHost(stats_host);
+        scr = bscr = nullptr;
+        bgrp = q0 = q1 = nullptr;
+        qctl = nullptr;
+        d_ctx = nullptr;
+        stats = stats_host = nullptr;
+        kcap = -1;
+        ninst_cap = 0;
+    }
+};
+
 struct hcov_tree_s {
     Plan P;
     bool uploaded = false;
@@ -654,7 +703,13 @@ struct hcov_tree_s {
     int32_t *d_leafnodes = nullptr;
     int32_t n_leafnodes = 0;
     int32_t *d_row_off = nullptr, *d_row_nodes = nullptr;
-    hcov_hmat cached = nullptr;
+    Engine eng;
+    hcov_hmat cached = nullptr;              // instance 0 of hcov_eval / hcov_mle_batch
+    std::vector<hcov_hmat> extra;            // instances 1.. of the last theta batch
+    // W / product-slot words used by the most demanding run so far at capacity est_kcap (per-instance
+    // pool sizing of theta batches)
+    int est_kcap = -1;
+    int64_t est_w = 0, est_p = 0;
     ~hcov_tree_s();
 };
 
@@ -665,30 +720,34 @@ struct hcov_hmat_s {
     hcov_trunc trunc{};
     int state = 0;   // 1 assembled, 2 factored, 3 solved
     int kcap_alloc = -1;
-    int grid = 0;
-    int64_t smem = 0;
     double *tiles = nullptr, *U = nullptr, *V = nullptr, *cores = nullptr, *W = nullptr, *P = nullptr;
     double *vbuf = nullptr, *tbuf = nullptr, *logdet_part = nullptr, *minpiv_part = nullptr, *quad_part = nullptr;
     int32_t *rank = nullptr, *fail = nullptr, *flags = nullptr;
-    int32_t *indeg = nullptr, *q0 = nullptr, *q1 = nullptr, *gbar = nullptr, *gslot = nullptr, *bgrp = nullptr;
-    uint32_t *qctl = nullptr;
-    double *scr = nullptr, *bscr = nullptr, *res = nullptr, *res_host = nullptr;
+    int32_t *indeg = nullptr, *gbar = nullptr, *gslot = nullptr;
+    double *res = nullptr, *res_host = nullptr;
     double *ktab = nullptr;
     int64_t *woff = nullptr, *poff = nullptr;
     unsigned long long *mem = nullptr;
     int64_t wcap = 0, pcap = 0;
-    EngineStats *stats = nullptr, *stats_host = nullptr;
+    int64_t w_budget = 0, p_budget = 0;   // > 0: pool sizes (words) fixed by a theta batch
+    void release_pools()
+    {
+        cudaFree(W);
+        cudaFree(P);
+        W = P = nullptr;
+        wcap = pcap = 0;
+        ctx.W = ctx.P = nullptr;
+        ctx.wcap = ctx.pcap = 0;
+    }
     void release_all()
     {
-        void *ps[] = {tiles, U, V, cores, W, P, vbuf, tbuf, logdet_part, minpiv_part, quad_part, rank, fail, flags,
-                      indeg, q0, q1, gbar, gslot, bgrp, qctl, scr, bscr, res, stats, woff, poff, mem};
+        release_pools();
+        void *ps[] = {tiles, U, V, cores, vbuf, tbuf, logdet_part, minpiv_part, quad_part, rank, fail, flags,
+                      indeg, gbar, gslot, res, woff, poff, mem};
         for (void *p : ps) cudaFree(p);
-        tiles = U = V = cores = W = P = vbuf = tbuf = logdet_part = minpiv_part = quad_part = nullptr;
-        wcap = pcap = 0;
-        rank = fail = flags = indeg = q0 = q1 = gbar = gslot = bgrp = nullptr;
-        qctl = nullptr;
-        scr = bscr = res = nullptr;
-        stats = nullptr;
+        tiles = U = V = cores = vbuf = tbuf = logdet_part = minpiv_part = quad_part = nullptr;
+        rank = fail = flags = indeg = gbar = gslot = nullptr;
+        res = nullptr;
         woff = poff = nullptr;
         mem = nullptr;
         kcap_alloc = -1;
@@ -698,13 +757,14 @@ struct hcov_hmat_s {
         release_all();
         cudaFree(ktab);
         if (res_host) cudaFreeHost(res_host);
-        if (stats_host) cudaFreeHost(stats_host);
     }
 };
 
 hcov_tree_s::~hcov_tree_s()
 {
     if (cached) delete cached;
+    for (hcov_hmat h : extra) delete h;
+    eng.release();
     void *ps[] = {d_nodes, d_tile_node, d_rblk, d_terms, d_xterm, d_fac_row0, d_fac_nrows, d_fac_rank_src,
                   d_fac_off, d_fac_pool, d_solves, d_solve_rhs, d_slots, d_ctr, d_phw, d_col_r, d_tasks, d_phase,
                   d_succ_off, d_succ, d_diag_tile, d_xs, d_ys, d_perm_i2e, d_leafnodes, d_row_off, d_row_nodes,
@@ -722,7 +782,6 @@ hcov_tree_s::~hcov_tree_s()
 
 namespace {
 
-const int NBIG = 0;   // (no dedicated gang CTAs: gangs are formed from the priority queue)
 
 hcov_status tree_upload(hcov_tree t)
 {
@@ -803,11 +862,15 @@ int eff_kcap(const hcov_trunc *tr)
     return 64;
 }
 
-int64_t qcap(const Plan &P, int cls)
+
+// Device bytes of one H-matrix instance outside its W / product-slot pools (memory planning of
+// theta batches; must follow hmat_alloc).
+int64_t inst_fixed_bytes(const Plan &P, int64_t kc)
 {
-    int64_t q = 1;
-    for (int m = 0; m < HCOV_MODES; ++m) q = std::max<int64_t>(q, P.n_q[m][cls]);
-    return q;
+    const int64_t ntk = (int64_t)P.tasks.size();
+    return 8 * (P.n_tiles() * HCOV_TILE + 2 * P.uv_elems * kc + (int64_t)P.n_cores * kc * kc + P.n_pad +
+                P.n_r() * kc + 3 * P.n_leaves + (int64_t)P.phw.size() + (int64_t)P.slots.size()) +
+           4 * (P.n_r() + 3 * ntk) + (int64_t)KTAB_NI * KTAB_NC * 8 + (1 << 20);
 }
 
 // (Re)allocate the numeric buffers of h for the tree's plan and capacity kcap.
@@ -822,11 +885,10 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     CK(cudaMalloc(&h->U, std::max<int64_t>(1, P.uv_elems * kc) * sizeof(double)));
     CK(cudaMalloc(&h->V, std::max<int64_t>(1, P.uv_elems * kc) * sizeof(double)));
     CK(cudaMalloc(&h->cores, std::max<int64_t>(1, (int64_t)P.n_cores * kc * kc) * sizeof(double)));
-    const int64_t wfull = P.w_elems * kc + (int64_t)P.phw.size() + 64;
-    const int64_t pfull = P.slot_a * kc * kc + P.slot_b * kc + (int64_t)P.slots.size() + 64;
     CK(cudaMalloc(&h->woff, std::max<size_t>(1, P.phw.size()) * sizeof(int64_t)));
     CK(cudaMalloc(&h->poff, std::max<size_t>(1, P.slots.size()) * sizeof(int64_t)));
     CK(cudaMalloc(&h->mem, 4 * sizeof(unsigned long long)));
+    CK(cudaMemset(h->mem, 0, 4 * sizeof(unsigned long long)));
     CK(cudaMalloc(&h->vbuf, P.n_pad * sizeof(double)));
     CK(cudaMalloc(&h->tbuf, std::max<int64_t>(1, P.n_r() * kc) * sizeof(double)));
     CK(cudaMalloc(&h->logdet_part, P.n_leaves * sizeof(double)));
@@ -839,58 +901,76 @@ hcov_status hmat_alloc(hcov_hmat h, int kcap)
     CK(cudaMalloc(&h->indeg, std::max<int64_t>(1, ntk) * sizeof(int32_t)));
     CK(cudaMalloc(&h->gbar, std::max<int64_t>(1, ntk) * sizeof(int32_t)));
     CK(cudaMalloc(&h->gslot, std::max<int64_t>(1, ntk) * sizeof(int32_t)));
-    CK(cudaMalloc(&h->q0, std::max<int64_t>(1, P.band_off[HCOV_BANDS]) * sizeof(int32_t)));
-    CK(cudaMalloc(&h->q1, qcap(P, 1) * sizeof(int32_t)));
-    CK(cudaMalloc(&h->qctl, QC_N * sizeof(uint32_t)));
     CK(cudaMalloc(&h->res, 8 * sizeof(double)));
-    CK(cudaMalloc(&h->stats, sizeof(EngineStats)));
     if (!h->res_host) CK(cudaMallocHost(&h->res_host, 8 * sizeof(double)));
-    if (!h->stats_host) CK(cudaMallocHost(&h->stats_host, sizeof(EngineStats)));
-    h->smem = engine_smem_doubles(kcap) * (int64_t)sizeof(double);
-    CK(cudaFuncSetAttribute(k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
-    int dev = 0, nsm = 0, occ = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engine, NT, (size_t)h->smem));
-    occ = std::max(1, std::min(occ, 512 / NT));
-    h->grid = nsm * occ;
-    // every gang forms only if the CTAs that partly formed gangs can hold (at most one per band)
-    // leave at least one free CTA
-    if (h->grid <= HCOV_BANDS * (HCOV_GANG - 1)) return HCOV_ERR_INVALID_ARG;
-    // per-CTA scratch: single-CTA tasks (blocks < HCOV_GANG_MIN, 6 panels) or a gang member's rows
-    // (m / G rows, 4 panels) followed by the gang's shared workspace (used when the CTA is member 0)
-    // members of more than HCOV_BIG_MQ rows (gangs on the largest blocks, m >= 8 * HCOV_BIG_MQ) use
-    // one of HCOV_BIG_GROUPS shared big-member groups instead
-    const int64_t med_m = std::min<int64_t>(HCOV_GANG_MIN / 2, std::max<int64_t>(P.max_rm, 32));
-    int64_t gshared_off = 0, scr_stride = task_scratch(med_m, kcap), bstride = 0;
-    int nbg = 0;
-    if (P.max_mq > 0) {
-        gshared_off = task_scratch(std::min<int64_t>(P.max_mq, HCOV_BIG_MQ), kcap, 4);
-        scr_stride = std::max<int64_t>(scr_stride, gshared_off + gang_shared_doubles(kbuf_of(kcap), HCOV_GANG));
-        if (P.max_mq > HCOV_BIG_MQ) {
-            bstride = task_scratch(P.max_mq, kcap, 4);
-            nbg = HCOV_BIG_GROUPS;
-        }
-    }
-    CK(cudaMalloc(&h->scr, scr_stride * (int64_t)h->grid * sizeof(double)));
-    CK(cudaMalloc(&h->bscr, std::max<int64_t>(1, bstride * HCOV_GANG * nbg) * sizeof(double)));
-    CK(cudaMalloc(&h->bgrp, (HCOV_BIG_GROUPS + h->grid) * sizeof(int32_t)));
-    CK(cudaMemset(h->bgrp, 0, (HCOV_BIG_GROUPS + h->grid) * sizeof(int32_t)));
-    h->ctx.scr_stride = scr_stride;
-    h->ctx.bscr_stride = bstride;
-    h->ctx.n_bgrp = nbg;
-    h->ctx.big_mq = HCOV_BIG_MQ;
-    h->ctx.bgrp_busy = h->bgrp;
-    h->ctx.bgrp_cta = h->bgrp + HCOV_BIG_GROUPS;
-    h->ctx.gshared_off = gshared_off;
     h->kcap_alloc = kcap;
     return HCOV_OK;
 }
 
+// The tree's engine resources for rank capacity kcap and ninst instances per launch.
+hcov_status engine_alloc(hcov_tree t, int kcap, int ninst)
+{
+    Engine &E = t->eng;
+    const Plan &P = t->P;
+    if (E.kcap != kcap) {
+        E.release();
+        E.smem = engine_smem_doubles(kcap) * (int64_t)sizeof(double);
+        CK(cudaFuncSetAttribute(k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E.smem));
+        int dev = 0, nsm = 0, occ = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engine, NT, (size_t)E.smem));
+        occ = std::max(1, std::min(occ, 512 / NT));
+        E.grid = nsm * occ;
+        // every gang forms only if the CTAs that partly formed gangs can hold (at most one per band)
+        // leave at least one free CTA
+        if (E.grid <= HCOV_BANDS * (HCOV_GANG - 1)) return HCOV_ERR_INVALID_ARG;
+        // per-CTA scratch: single-CTA tasks (blocks < HCOV_GANG_MIN, 6 panels) or a gang member's rows
+        // (m / G rows, 4 panels) followed by the gang's shared workspace (used when the CTA is member
+        // 0); members of more than HCOV_BIG_MQ rows (gangs on the largest blocks) use one of
+        // HCOV_BIG_GROUPS shared big-member groups instead
+        const int64_t med_m = std::min<int64_t>(HCOV_GANG_MIN / 2, std::max<int64_t>(P.max_rm, 32));
+        E.gshared_off = 0;
+        E.scr_stride = task_scratch(med_m, kcap);
+        E.bstride = 0;
+        E.nbg = 0;
+        if (P.max_mq > 0) {
+            E.gshared_off = task_scratch(std::min<int64_t>(P.max_mq, HCOV_BIG_MQ), kcap, 4);
+            E.scr_stride = std::max<int64_t>(E.scr_stride, E.gshared_off + gang_shared_doubles(kbuf_of(kcap), HCOV_GANG));
+            if (P.max_mq > HCOV_BIG_MQ) {
+                E.bstride = task_scratch(P.max_mq, kcap, 4);
+                E.nbg = HCOV_BIG_GROUPS;
+            }
+        }
+        CK(cudaMalloc(&E.scr, E.scr_stride * (int64_t)E.grid * sizeof(double)));
+        CK(cudaMalloc(&E.bscr, std::max<int64_t>(1, E.bstride * HCOV_GANG * E.nbg) * sizeof(double)));
+        CK(cudaMalloc(&E.bgrp, (HCOV_BIG_GROUPS + E.grid) * sizeof(int32_t)));
+        CK(cudaMemset(E.bgrp, 0, (HCOV_BIG_GROUPS + E.grid) * sizeof(int32_t)));
+        CK(cudaMalloc(&E.q1, sizeof(int32_t)));
+        CK(cudaMalloc(&E.qctl, QC_N * sizeof(uint32_t)));
+        CK(cudaMemset(E.qctl, 0, QC_N * sizeof(uint32_t)));
+        CK(cudaMalloc(&E.stats, sizeof(EngineStats)));
+        CK(cudaMallocHost(&E.stats_host, sizeof(EngineStats)));
+        E.kcap = kcap;
+    }
+    if (ninst > E.ninst_cap) {
+        cudaFree(E.q0);
+        cudaFree(E.d_ctx);
+        E.q0 = nullptr;
+        E.d_ctx = nullptr;
+        E.ninst_cap = 0;
+        CK(cudaMalloc(&E.q0, std::max<int64_t>(1, (int64_t)P.band_off[HCOV_BANDS] * ninst) * sizeof(int32_t)));
+        CK(cudaMalloc(&E.d_ctx, ninst * sizeof(Ctx)));
+        E.ninst_cap = ninst;
+    }
+    return HCOV_OK;
+}
+
 // The W and product-slot pools (H-Cholesky and solves only; an assembly-only H-matrix never holds
-// them).  W and the slots are bump-allocated at run time with the actual ranks; the pools get the
-// capacity-based sizes when they fit, else the free device memory (minus 3 GB headroom) split
-// 70 / 30.  An overflow is detected and reported as HCOV_ERR_OUT_OF_MEMORY.
+// them).  W and the slots are bump-allocated at run time with the actual ranks.  Sizes: the
+// instance's budget when a theta batch fixed one; else the capacity-based sizes when they fit,
+// else the free device memory (minus 3 GB headroom) split 70 / 30.  An overflow stops the engine
+// and is reported as HCOV_ERR_OUT_OF_MEMORY.
 hcov_status pools_alloc(hcov_hmat h)
 {
     if (h->W) return HCOV_OK;
@@ -898,13 +978,18 @@ hcov_status pools_alloc(hcov_hmat h)
     const int64_t kc = h->kcap_alloc;
     const int64_t wfull = P.w_elems * kc + (int64_t)P.phw.size() + 64;
     const int64_t pfull = P.slot_a * kc * kc + P.slot_b * kc + (int64_t)P.slots.size() + 64;
-    size_t fr = 0, tot = 0;
-    CK(cudaMemGetInfo(&fr, &tot));
-    const int64_t avail = std::max<int64_t>(0, (int64_t)fr / 8 - ((int64_t)3 << 27));
-    if (wfull + pfull <= avail) { h->wcap = wfull; h->pcap = pfull; }
-    else {
-        h->wcap = std::min<int64_t>(wfull, (int64_t)(0.7 * avail));
-        h->pcap = std::min<int64_t>(pfull, avail - h->wcap);
+    if (h->w_budget > 0) {
+        h->wcap = std::min(wfull, h->w_budget);
+        h->pcap = std::min(pfull, h->p_budget);
+    } else {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        const int64_t avail = std::max<int64_t>(0, (int64_t)fr / 8 - ((int64_t)3 << 27));
+        if (wfull + pfull <= avail) { h->wcap = wfull; h->pcap = pfull; }
+        else {
+            h->wcap = std::min<int64_t>(wfull, (int64_t)(0.7 * avail));
+            h->pcap = std::min<int64_t>(pfull, avail - h->wcap);
+        }
     }
     CK(cudaMalloc(&h->W, std::max<int64_t>(1, h->wcap) * sizeof(double)));
     CK(cudaMalloc(&h->P, std::max<int64_t>(1, h->pcap) * sizeof(double)));
@@ -923,7 +1008,7 @@ void fill_ctx(hcov_hmat h)
     c.solves = t->d_solves; c.solve_rhs = t->d_solve_rhs; c.slots = t->d_slots; c.ctr = t->d_ctr;
     c.phw = t->d_phw; c.col_r = t->d_col_r; c.tasks = t->d_tasks; c.succ_off = t->d_succ_off; c.succ = t->d_succ;
     c.diag_tile = t->d_diag_tile; c.xs = t->d_xs; c.ys = t->d_ys; c.perm_i2e = t->d_perm_i2e;
-    c.depth = P.depth; c.n_r = (int32_t)P.n_r(); c.root_solve = P.root_solve;
+    c.depth = P.depth; c.n_r = (int32_t)P.n_r(); c.root_solve = P.root_solve; c.ntasks = (int32_t)P.tasks.size();
     c.n_pad = P.n_pad; c.n_leaves = P.n_leaves; c.n_real = P.n; c.n_tiles = P.n_tiles();
     c.tiles = h->tiles; c.U = h->U; c.V = h->V; c.rank = h->rank; c.cores = h->cores; c.W = h->W; c.P = h->P;
     c.woff = h->woff; c.poff = h->poff; c.mem = h->mem; c.wcap = h->wcap; c.pcap = h->pcap;
@@ -939,39 +1024,60 @@ void fill_ctx(hcov_hmat h)
     }
     c.mp = hcov_matern_params(h->theta.sigma2, h->theta.ell, h->theta.nu, h->theta.nugget);
     if (c.mp.kind == 3) c.mp.tab = h->ktab;
-    c.indeg = h->indeg; c.queue[0] = h->q0; c.queue[1] = h->q1; c.qctl = h->qctl; c.gbar = h->gbar;
+    c.indeg = h->indeg; c.gbar = h->gbar; c.gslot = h->gslot;
     c.band_off = t->d_band_off;
-    c.gslot = h->gslot;
-    c.nbig = NBIG;
-    c.scr = h->scr; c.bscr = h->bscr;   // (bscr_stride, n_bgrp, big_mq, bgrp_*: set by hmat_alloc)
     c.flop = nullptr;
-    c.smem_dbl = h->smem / (int64_t)sizeof(double);
     const char *wd = std::getenv("HCOV_WATCHDOG_S");
     double wds = wd ? std::atof(wd) : 300.0;
     if (!(wds > 0)) wds = 300.0;
     c.timeout_ns = (unsigned long long)(wds * 1e9);
 }
 
-// Run the engine in mode md (0 eval, 1 assembly, 2 Cholesky, 3 forward solve, 4 back-solve) on st.
-hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
+// Engine-level fields of a context (identical in every instance of a launch).
+void engine_fields(Ctx &c, const Engine &E, int ninst)
 {
-    hcov_tree t = h->t;
+    c.queue[0] = E.q0; c.queue[1] = E.q1; c.qctl = E.qctl;
+    c.ninst = ninst;
+    c.scr = E.scr; c.scr_stride = E.scr_stride; c.gshared_off = E.gshared_off;
+    c.bscr = E.bscr; c.bscr_stride = E.bstride; c.n_bgrp = E.nbg; c.big_mq = HCOV_BIG_MQ;
+    c.bgrp_busy = E.bgrp; c.bgrp_cta = E.bgrp + HCOV_BIG_GROUPS;
+    c.smem_dbl = E.smem / (int64_t)sizeof(double);
+}
+
+// Run the engine in mode md (0 eval, 1 assembly, 2 Cholesky, 3 forward solve, 4 back-solve) on st
+// for nb H-matrices of the same tree and rank capacity in ONE persistent launch (their DAGs share
+// the priority queue; a theta batch).
+hcov_status engine_run_batch(hcov_hmat *hs, int nb, int md, cudaStream_t st)
+{
+    hcov_tree t = hs[0]->t;
     Plan &P = t->P;
     static const int mask[HCOV_MODES] = {7, 1, 2, 4, 8};
     const int64_t ntk = (int64_t)P.tasks.size();
-    if (md == 0 || md == 2 || md == 3) {
-        hcov_status ps = pools_alloc(h);
-        if (ps) return ps;
+    if (((int64_t)nb * ntk) >= ((int64_t)1 << (31 - QE_SHIFT))) return HCOV_ERR_INVALID_ARG;
+    for (int i = 0; i < nb; ++i) {
+        if (hs[i]->t != t || hs[i]->kcap_alloc != hs[0]->kcap_alloc) return HCOV_ERR_INVALID_ARG;
+        if (md == 0 || md == 2 || md == 3) {
+            hcov_status ps = pools_alloc(hs[i]);
+            if (ps) return ps;
+        }
     }
-    Ctx c = h->ctx;
-    c.nq[0] = P.n_q[md][0];
-    c.nq[1] = P.n_q[md][1];
-    if (c.nq[0] + c.nq[1] == 0) return HCOV_OK;
-    LAUNCH(PC_RESET, st, k_reset<<<296, 256, 0, st>>>(c, t->d_indeg[md], ntk, t->d_q0init[md],
-                                                     (int64_t)P.band_off[HCOV_BANDS], t->d_q0tail[md],
-                                                     t->d_roots[md][1], (int32_t)P.roots[md][1].size(), qcap(P, 1)));
-    EngineStats *stats = g_prof.events ? h->stats : nullptr;
-    if (stats) CK(cudaMemsetAsync(h->stats, 0, sizeof(EngineStats), st));
+    hcov_status es = engine_alloc(t, hs[0]->kcap_alloc, nb);
+    if (es) return es;
+    Engine &E = t->eng;
+    std::vector<Ctx> cx(nb);
+    for (int i = 0; i < nb; ++i) {
+        engine_fields(hs[i]->ctx, E, nb);
+        cx[i] = hs[i]->ctx;
+        cx[i].nq[0] = nb * P.n_q[md][0];
+        cx[i].nq[1] = 0;
+    }
+    if (cx[0].nq[0] == 0) return HCOV_OK;
+    CK(cudaMemcpyAsync(E.d_ctx, cx.data(), nb * sizeof(Ctx), cudaMemcpyHostToDevice, st));
+    for (int i = 0; i < nb; ++i)
+        LAUNCH(PC_RESET, st, k_reset_inst<<<296, 256, 0, st>>>(cx[i], t->d_indeg[md], ntk));
+    LAUNCH(PC_RESET, st, k_qinit<<<296, 256, 0, st>>>(cx[0], t->d_q0init[md], t->d_q0tail[md]));
+    EngineStats *stats = g_prof.events ? E.stats : nullptr;
+    if (stats) CK(cudaMemsetAsync(E.stats, 0, sizeof(EngineStats), st));
     {
         static const unsigned long long zeros[64] = {};
         const int on = stats ? 1 : 0;
@@ -980,12 +1086,14 @@ hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
     }
     const char *tlpath = std::getenv("HCOV_TIMELINE");
     unsigned long long *tl = nullptr;
-    if (tlpath) {
+    if (tlpath && nb == 1) {
         CK(cudaMalloc(&tl, 3 * std::max<int64_t>(1, ntk) * sizeof(unsigned long long)));
         CK(cudaMemsetAsync(tl, 0, 3 * std::max<int64_t>(1, ntk) * sizeof(unsigned long long), st));
     }
-    LAUNCH(PC_ENGINE, st, k_engine<<<h->grid, NT, h->smem, st>>>(c, mask[md], t->d_phase, stats, tl));
+    LAUNCH(PC_ENGINE, st, k_engine<<<E.grid, NT, E.smem, st>>>(cx[0], E.d_ctx, mask[md], t->d_phase, stats, tl));
     CK(cudaGetLastError());
+    // the context array's host copy (cx) must outlive the asynchronous upload
+    CK(cudaStreamSynchronize(st));
     if (tl) {
         std::vector<unsigned long long> hv(3 * ntk);
         CK(cudaMemcpyAsync(hv.data(), tl, hv.size() * 8, cudaMemcpyDeviceToHost, st));
@@ -998,19 +1106,21 @@ hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st)
         }
     }
     if (stats) {
-        CK(cudaMemcpyAsync(h->stats_host, h->stats, sizeof(EngineStats), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(E.stats_host, E.stats, sizeof(EngineStats), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         for (int k = 0; k < TK_NTYPES; ++k) {
-            g_prof.busy_ns[k] += (double)h->stats_host->busy_ns[k];
-            g_prof.tasks[k] += (double)h->stats_host->tasks[k];
+            g_prof.busy_ns[k] += (double)E.stats_host->busy_ns[k];
+            g_prof.tasks[k] += (double)E.stats_host->tasks[k];
         }
-        for (int k = 0; k < FC_N; ++k) g_prof.flop[k] += h->stats_host->flop[k];
+        for (int k = 0; k < FC_N; ++k) g_prof.flop[k] += E.stats_host->flop[k];
         unsigned long long ph[64];
         CK(cudaMemcpyFromSymbol(ph, g_phase_ns, sizeof(ph)));
         for (int k = 0; k < 64; ++k) g_prof.phase_ns[k] += (double)ph[k];
     }
     return HCOV_OK;
 }
+
+hcov_status engine_run(hcov_hmat h, int md, cudaStream_t st) { return engine_run_batch(&h, 1, md, st); }
 
 hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trunc *trunc, cudaStream_t st)
 {
@@ -1046,11 +1156,18 @@ hcov_status check_abort(hcov_hmat h, cudaStream_t st, int32_t *hf)
     uint32_t ab = 0;
     unsigned long long mem[4] = {0, 0, 0, 0};
     CK(cudaMemcpyAsync(mem, h->mem, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&ab, h->qctl + QC_ABORT, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    if (h->t->eng.qctl) CK(cudaMemcpyAsync(&ab, h->t->eng.qctl + QC_ABORT, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf, h->fail, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf + 1, h->flags, 5 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (mem[2]) return HCOV_ERR_OUT_OF_MEMORY;   // a pool overflow also raises the abort flag
+    {
+        // pool words this run used: sizing of later theta batches on this tree
+        hcov_tree t = h->t;
+        if (t->est_kcap != h->kcap_alloc) { t->est_kcap = h->kcap_alloc; t->est_w = 0; t->est_p = 0; }
+        t->est_w = std::max<int64_t>(t->est_w, (int64_t)mem[0]);
+        t->est_p = std::max<int64_t>(t->est_p, (int64_t)mem[1]);
+    }
     if (ab) return HCOV_ERR_CUDA;
     return HCOV_OK;
 }
@@ -1078,6 +1195,39 @@ hcov_status finish_result(hcov_hmat h, cudaStream_t st, hcov_result *out)
     out->interm_cuts = hf[5];
     if (out->fail_leaf >= 0) { out->loglik = -INFINITY; return HCOV_ERR_NOT_SPD; }
     if ((hf[2] > 0 || hf[4] > 0) && h->trunc.kmax == 0) { out->loglik = -INFINITY; return HCOV_ERR_RANK_CAPACITY; }
+    return HCOV_OK;
+}
+
+
+// Release the extra instances of the last theta batch.
+void free_extra(hcov_tree t)
+{
+    for (hcov_hmat h : t->extra) delete h;
+    t->extra.clear();
+}
+
+// Evaluate L~ for nb thetas on nb instances of one tree in ONE engine launch (A3-A10 each);
+// out[i] / sts[i] per instance (sts == nullptr: nb == 1, the status is returned).
+hcov_status eval_instances(hcov_hmat *hs, int nb, const hcov_theta *const *th, const hcov_trunc *trunc,
+                           const double *Z_dev, cudaStream_t st, hcov_result *out, hcov_status *sts)
+{
+    hcov_status s;
+    for (int i = 0; i < nb; ++i) {
+        if ((s = assemble_setup(hs[i], th[i], trunc, st))) return s;
+        LAUNCH(PC_PERM, st, k_permute_in<<<256, 256, 0, st>>>(hs[i]->ctx, Z_dev, hs[i]->vbuf));
+    }
+    s = engine_run_batch(hs, nb, 0, st);
+    if (s) {
+        if (!sts) return s;
+        for (int i = 0; i < nb; ++i) { sts[i] = s; out[i] = hcov_result{}; out[i].loglik = -INFINITY; }
+        return (s == HCOV_ERR_OUT_OF_MEMORY) ? HCOV_OK : s;
+    }
+    for (int i = 0; i < nb; ++i) {
+        hs[i]->state = 3;
+        const hcov_status r = finish_result(hs[i], st, out + i);
+        if (!sts) return r;
+        sts[i] = r;
+    }
     return HCOV_OK;
 }
 
@@ -1277,25 +1427,97 @@ hcov_status hcov_eval(hcov_tree t, const hcov_theta *theta, const hcov_trunc *tr
     }
     hcov_hmat h = t->cached;
     cudaStream_t st = (cudaStream_t)stream;
-    if ((s = assemble_setup(h, theta, trunc, st))) return s;
-    LAUNCH(PC_PERM, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, Z_dev, h->vbuf));
-    if ((s = engine_run(h, 0, st))) return s;
-    h->state = 3;
-    return finish_result(h, st, out);
+    s = eval_instances(&h, 1, &theta, trunc, Z_dev, st, out, nullptr);
+    if (s == HCOV_ERR_OUT_OF_MEMORY && (h->w_budget > 0 || !t->extra.empty())) {
+        // pools sized for a theta batch were too small for this theta: all free memory, once more
+        free_extra(t);
+        h->release_pools();
+        h->w_budget = h->p_budget = 0;
+        s = eval_instances(&h, 1, &theta, trunc, Z_dev, st, out, nullptr);
+    }
+    return s;
 }
 
 hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *thetas, int32_t m,
                            const hcov_trunc *trunc, hcov_stream stream, double *loglik_host, hcov_status *status_host)
 {
     if (!t || !Z_dev || !thetas || m < 0 || !trunc || !loglik_host || !status_host) return HCOV_ERR_INVALID_ARG;
-    for (int32_t k = 0; k < m; ++k) {
-        hcov_result r;
-        hcov_status s = hcov_eval(t, thetas + k, trunc, Z_dev, stream, &r);
+    cudaStream_t st = (cudaStream_t)stream;
+    auto record = [&](int k, hcov_status s, const hcov_result &r) -> hcov_status {
         status_host[k] = s;
-        if (s == HCOV_OK) loglik_host[k] = r.loglik;
-        else if (s == HCOV_ERR_NOT_SPD || s == HCOV_ERR_RANK_CAPACITY || s == HCOV_ERR_INVALID_ARG)
-            loglik_host[k] = -INFINITY;
-        else return s;
+        if (s == HCOV_OK) { loglik_host[k] = r.loglik; return HCOV_OK; }
+        loglik_host[k] = -INFINITY;
+        if (s == HCOV_ERR_NOT_SPD || s == HCOV_ERR_RANK_CAPACITY || s == HCOV_ERR_INVALID_ARG) return HCOV_OK;
+        return s;   // out of memory / CUDA: abort the batch
+    };
+    std::vector<int> todo;
+    for (int32_t k = 0; k < m; ++k) {
+        if (check_theta(thetas + k, trunc)) { status_host[k] = HCOV_ERR_INVALID_ARG; loglik_host[k] = -INFINITY; }
+        else todo.push_back(k);
+    }
+    if (todo.empty()) return HCOV_OK;
+    hcov_status s = tree_upload(t);
+    if (s) return s;
+    const int kcap = eff_kcap(trunc);
+    size_t next = 0;
+    // pool sizes of the batch instances come from the words an earlier run on this tree used; without
+    // that, the first candidate runs alone (all free memory) and provides it
+    if (t->est_kcap != kcap || t->est_w + t->est_p == 0) {
+        hcov_result r{};
+        const int k = todo[next++];
+        if ((s = record(k, hcov_eval(t, thetas + k, trunc, Z_dev, stream, &r), r))) return s;
+    }
+    if (next == todo.size()) return HCOV_OK;
+    // batch size B: instance 0 (t->cached) plus B - 1 extra instances, every instance with pools of
+    // 1.3 x the estimate, 2 GB headroom (HCOV_MAX_BATCH at most; env HCOV_BATCH overrides downwards)
+    free_extra(t);
+    t->cached->release_pools();
+    const Plan &P = t->P;
+    const int64_t wb = (int64_t)(1.3 * (double)t->est_w) + ((int64_t)1 << 20);
+    const int64_t pb = (int64_t)(1.3 * (double)t->est_p) + ((int64_t)1 << 20);
+    const int64_t fixed = inst_fixed_bytes(P, kcap), pools = 8 * (wb + pb);
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const int64_t avail = (int64_t)fr - ((int64_t)2 << 30);
+    int B = 1;
+    if (avail > pools) B = 1 + (int)std::min<int64_t>(HCOV_MAX_BATCH - 1, (avail - pools) / (fixed + pools));
+    if (const char *eb = std::getenv("HCOV_BATCH")) B = std::max(1, std::min(B, std::atoi(eb)));
+    B = std::min<int>(B, (int)(todo.size() - next));
+    std::vector<hcov_hmat> inst(1, t->cached);
+    for (int i = 1; i < B; ++i) {
+        hcov_hmat h = new (std::nothrow) hcov_hmat_s();
+        if (!h) break;
+        h->t = t;
+        t->extra.push_back(h);
+        if (hmat_alloc(h, kcap)) { free_extra(t); inst.resize(1); break; }   // (fixed memory only: B shrinks)
+        inst.push_back(h);
+    }
+    B = (int)inst.size();
+    for (hcov_hmat h : inst) { h->w_budget = B > 1 ? wb : 0; h->p_budget = B > 1 ? pb : 0; }
+    std::vector<int> retry;
+    while (next < todo.size()) {
+        const int nb = (int)std::min<size_t>(B, todo.size() - next);
+        std::vector<const hcov_theta *> th(nb);
+        std::vector<hcov_result> res(nb);
+        std::vector<hcov_status> sts(nb);
+        for (int i = 0; i < nb; ++i) th[i] = thetas + todo[next + i];
+        s = eval_instances(inst.data(), nb, th.data(), trunc, Z_dev, st, res.data(), sts.data());
+        if (s) return s;
+        for (int i = 0; i < nb; ++i) {
+            const int k = todo[next + i];
+            // a pool overflow stops the whole launch: every candidate of it that did not finish is
+            // evaluated again on its own
+            if (sts[i] == HCOV_ERR_OUT_OF_MEMORY || sts[i] == HCOV_ERR_CUDA) retry.push_back(k);
+            else if ((s = record(k, sts[i], res[i]))) return s;
+        }
+        next += nb;
+    }
+    free_extra(t);
+    t->cached->release_pools();
+    t->cached->w_budget = t->cached->p_budget = 0;
+    for (int k : retry) {
+        hcov_result r{};
+        if ((s = record(k, hcov_eval(t, thetas + k, trunc, Z_dev, stream, &r), r))) return s;
     }
     return HCOV_OK;
 }

@@ -12,6 +12,7 @@
 #define HCOV_SMEM_DBL 28160 // dynamic shared memory of the engine CTA (220 KB + static <= 227 KB; one 512-thread CTA per SM)
 #define HCOV_BIG_MQ 4096      // gang members with more rows use a big-member scratch slot (hcov.cu)
 #define HCOV_BIG_GROUPS 4     // big-member groups (HCOV_GANG slots each)
+#define HCOV_MAX_BATCH 8      // H-matrices (theta candidates) per engine launch in hcov_mle_batch
 #define HCOV_GANG_MIN 512     // low-rank blocks from this size on are processed by gangs of min(8, m/256) CTAs
 
 // Block-tree node types (lower triangle incl. diagonal).

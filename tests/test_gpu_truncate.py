@@ -52,3 +52,12 @@ def _check(path, kind, m, R, eps):
     assert err <= 10 * eps * s[0], (err / s[0], r)
     r_ref = int(np.sum(s > eps * s[0]))
     assert abs(r - r_ref) <= 2, (r, r_ref)
+
+
+# large work capacities (K = 3 kcap + 32 up to 224 columns at kcap = 64): the core arrays leave
+# shared memory (R > 96) and the panel QRs use the global paths; tight eps down to 1e-13
+@pytest.mark.parametrize("path", [0, 1, 2])
+@pytest.mark.parametrize("kind", ["decay", "dependent", "scaled"])
+@pytest.mark.parametrize("m,R,eps", [(512, 150, 1e-10), (256, 200, 1e-12), (1024, 120, 1e-9), (300, 224, 1e-13)])
+def test_truncation_large_capacity(path, kind, m, R, eps):
+    _check(path, kind, m, R, eps)
