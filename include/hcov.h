@@ -169,6 +169,22 @@ hcov_status hcov_matvec(hcov_hmat h, const double *x_dev, double *y_dev, hcov_st
 hcov_status hcov_pcg(hcov_hmat A, hcov_hmat M, const double *b_dev, double *x_dev, int32_t maxit, double tol,
                      hcov_stream stream, int32_t *iters_host, double *relres_host);
 
+/* NEXT (f3): accuracy diagnostics of Sec. 4 (Tables 2-3; Table 4's last
+ * column).  Deterministic power iterations from a hashed start vector (seed).
+ *   hcov_norm2_diff:  ||A~ - B~||_2 of two ASSEMBLED matrices on the same n points (e.g. B = the exact C
+ *                     as an eta = 0 all-dense tree), power iteration on the symmetric difference.
+ *   hcov_inv_error:   ||I - M^{-1} A~||_2, A assembled, M factored (M = L~ L~^T), by power iteration on
+ *                     E^T E, E = I - M^{-1} A (= ||A M^{-1} - I||_2, the Table 2-3 column with A = C).
+ *   hcov_trace_inv:   tr(M^{-1} A) by n solves with the columns of A (the KLD's trace term,
+ *                     KLD = (tr(M^{-1} C) - n + log det M - log det C) / 2; feasible for small n).
+ * Outputs: one host double.  Iterations: the largest ||E x_k|| (||x_k|| = 1) seen, a lower bound that
+ * converges to the norm.  Synchronise the stream. */
+hcov_status hcov_norm2_diff(hcov_hmat A, hcov_hmat B, int32_t iters, uint64_t seed, hcov_stream stream,
+                            double *out_host);
+hcov_status hcov_inv_error(hcov_hmat A, hcov_hmat M, int32_t iters, uint64_t seed, hcov_stream stream,
+                           double *out_host);
+hcov_status hcov_trace_inv(hcov_hmat M, hcov_hmat A, hcov_stream stream, double *out_host);
+
 /* Support (not timed).  Z = P_i2e L~ xi for a factored matrix (Sec. 5.1);
  * xi_dev, Z_dev: n fp64 (xi in external order too: xi is permuted to internal first). */
 hcov_status hcov_sample(hcov_hmat h, const double *xi_dev, double *Z_dev, hcov_stream stream);

@@ -93,6 +93,9 @@ _SIGS = {
     "hcov_solve": (_I32, [_P, _P, _P, _P]),
     "hcov_matvec": (_I32, [_P, _P, _P, _P]),
     "hcov_pcg": (_I32, [_P, _P, _P, _P, _I32, _D, _P, _P, _P]),
+    "hcov_norm2_diff": (_I32, [_P, _P, _I32, ctypes.c_uint64, _P, _P]),
+    "hcov_inv_error": (_I32, [_P, _P, _I32, ctypes.c_uint64, _P, _P]),
+    "hcov_trace_inv": (_I32, [_P, _P, _P, _P]),
     "hcov_model_flops": (_I32, [_P, _P]),
     "hcov_tree_last_eval": (_I32, [_P, _P]),
     "hcov_prof_control": (_I32, [_I32, _I32]),
@@ -358,6 +361,47 @@ def pcg(A: "HMatrix", M: "HMatrix", b, maxit: int = 150, tol: float = 1e-6, stre
     _check(lib().hcov_pcg(A._h, M._h, _dev_f64(b, A.tree.n, "b"), _dev_f64(x), maxit, tol, _stream(stream),
                           ctypes.byref(it), ctypes.byref(rr)), "hcov_pcg")
     return x, it.value, rr.value
+
+
+def norm2_diff(A: "HMatrix", B: "HMatrix", iters: int = 30, seed: int = 1, stream=None) -> float:
+    """hcov_norm2_diff: ||A~ - B~||_2 of two assembled H-matrices on the same points."""
+    o = ctypes.c_double()
+    _check(lib().hcov_norm2_diff(A._h, B._h, iters, seed, _stream(stream), ctypes.byref(o)), "hcov_norm2_diff")
+    return o.value
+
+
+def inv_error(A: "HMatrix", M: "HMatrix", iters: int = 30, seed: int = 1, stream=None) -> float:
+    """hcov_inv_error: ||I - M^{-1} A~||_2 (A assembled, M factored)."""
+    o = ctypes.c_double()
+    _check(lib().hcov_inv_error(A._h, M._h, iters, seed, _stream(stream), ctypes.byref(o)), "hcov_inv_error")
+    return o.value
+
+
+def trace_inv(M: "HMatrix", A: "HMatrix", stream=None) -> float:
+    """hcov_trace_inv: tr(M^{-1} A) (M factored, A assembled)."""
+    o = ctypes.c_double()
+    _check(lib().hcov_trace_inv(M._h, A._h, _stream(stream), ctypes.byref(o)), "hcov_trace_inv")
+    return o.value
+
+
+def kld(tree: Tree, exact_tree: Tree, theta, eps: float, kmax: int = 0, kcap: int = 0) -> dict:
+    """Sec. 4 diagnostics of C~ (eps, kmax) against the exact C: KLD,
+    ||C - C~||_2 and ||C C~^{-1} - I||_2.  exact_tree: the same points with eta = 0 (all dense, C~ = C).
+    Every quantity is computed by the library's kernels; only the closing arithmetic is here."""
+    n = tree.n
+    Ce = HMatrix(exact_tree, theta, 0.0)            # assembled exact C
+    Cf = HMatrix(exact_tree, theta, 0.0)
+    Cf.cholesky()
+    import torch
+    ld_c = Cf.loglik(torch.zeros(n, dtype=torch.float64, device="cuda"))["logdet"]
+    A = HMatrix(tree, theta, eps, kmax, kcap)       # assembled C~
+    M = HMatrix(tree, theta, eps, kmax, kcap)
+    M.cholesky()
+    ld_t = M.loglik(torch.zeros(n, dtype=torch.float64, device="cuda"))["logdet"]
+    tr = trace_inv(M, Ce)
+    return {"kld": 0.5 * (tr - n + ld_t - ld_c), "trace": tr, "logdet_C": ld_c, "logdet_Ct": ld_t,
+            "norm2_C_minus_Ct": norm2_diff(Ce, A), "norm2_C_Ctinv_minus_I": inv_error(Ce, M),
+            "max_rank": A.storage()["max_rank"]}
 
 
 def mle_batch(tree: Tree, Z, thetas, eps: float, kmax: int = 0, kcap: int = 0, stream=None):

@@ -364,13 +364,19 @@ struct Gang {
     int nb;
     int64_t mq, q0;
     double *shared;
+    int split;                 // side-split gang: members [0, G/2) hold X rows, [G/2, G) Y rows
+    int side, gs, Gs;          // side (0 X, 1 Y; -1 both), index within the side, members per side
 };
-// Rows of a gang member: m / G each, the last member also takes the remainder.
+// Rows of a gang member: m / Gs each (Gs = G, or G/2 per side when side-split), the last member
+// of a side also takes the remainder.
 __device__ __forceinline__ void gang_rows(Gang &gg, int64_t m)
 {
-    const int64_t base = m / gg.G;
-    gg.q0 = (int64_t)gg.g * base;
-    gg.mq = (gg.g == gg.G - 1) ? m - (int64_t)(gg.G - 1) * base : base;
+    gg.Gs = gg.split ? gg.G / 2 : gg.G;
+    gg.side = gg.split ? gg.g / gg.Gs : -1;
+    gg.gs = gg.split ? gg.g % gg.Gs : gg.g;
+    const int64_t base = m / gg.Gs;
+    gg.q0 = (int64_t)gg.gs * base;
+    gg.mq = (gg.gs == gg.Gs - 1) ? m - (int64_t)(gg.Gs - 1) * base : base;
 }
 __device__ __forceinline__ void gang_sync(Gang &gg)
 {
@@ -614,7 +620,7 @@ __device__ void tsqr_node_down(double *Ck, const double *Nd, int64_t nslot, int 
 // member b + s, so both proceed in parallel); member 0 truncates the core M = R_X R_Y^T
 // (compress_core); the core factors are pushed down the trees, and every member applies its local
 // Q to its block [C_g; 0] of the result U, V (global, ld ldo, rows q0..q0+mq).
-__device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, int R, double eps, double tol_q,
+__device__ __noinline__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, int R, double eps, double tol_q,
                              bool svd, int kmax, int rlim, double *U, double *V, int64_t ldo, int *cb, int *of,
                              double *red, double *redv, int64_t *redi, double *smem, int64_t smem_dbl)
 {
@@ -688,6 +694,80 @@ __device__ int gang_compress(const CompressWs &w, const GangWs &gw, Gang &gg, in
         local_apply(w.Y, mq, R, w.ty, w.tsr ? w.tsr + ts_region_doubles(mq, K) / 2 : nullptr, K, V + q0, ldo, r, w.G,
                     smem, smem_dbl);
     }
+    PH_END(12, t5);
+    gang_sync(gg);
+    return r;
+}
+
+// Side-split gang truncation of X Y^T: members [0, Gs) hold rows of X (their panel w.X), members
+// [Gs, 2 Gs) rows of Y (panel w.Y); every member factors ONE local panel, the two TSQR trees run on
+// their own members (node (b, s) of a side on that side's member b), member 0 truncates the core,
+// the cores go down the trees and each member writes its rows of U (X side) or V (Y side).  Same
+// arithmetic as gang_compress with the per-side row partition.
+__device__ __noinline__ int gang_compress_split(const CompressWs &w, const GangWs &gw, Gang &gg, int R, double eps,
+                                   double tol_q, bool svd, int kmax, int rlim, double *U, double *V, int64_t ldo,
+                                   int *cb, int *of, double *red, double *redv, int64_t *redi, double *smem,
+                                   int64_t smem_dbl)
+{
+    if (R == 0) { *cb = 0; *of = 0; return 0; }
+    const int Gs = gg.Gs, gs = gg.gs, side = gg.side;
+    const int64_t mq = gg.mq, q0 = gg.q0;
+    const int64_t RR = (int64_t)R * R;
+    const int K = w.K;
+    double *Pn = side ? w.Y : w.X;
+    double *tau = side ? w.ty : w.tx;
+    double *Bk = side ? gw.BY : gw.BX, *Nd = side ? gw.NY : gw.NX, *Ck = side ? gw.CY : gw.CX;
+    PH_BEGIN(t1);
+    local_qr(Pn, mq, R, tau, w.tsr, K, smem, smem_dbl, red);
+    for (int e = threadIdx.x; e < RR; e += NT) {
+        const int i = e % R, k = e / R;
+        __stcg(Bk + (int64_t)gs * RR + e, (k >= i) ? Pn[i + mq * k] : 0.0);
+    }
+    PH_END(9, t1);
+    gang_sync(gg);
+    PH_BEGIN(t2);
+    int top = 1;
+    while (2 * top < Gs) top *= 2;
+    for (int s = 1; s < Gs; s *= 2) {
+        if (gs % (2 * s) == 0 && gs + s < Gs) tsqr_node_up(Bk, Nd, gw.nslot, gs, s, R, smem, smem_dbl, red);
+        gang_sync(gg);
+    }
+    PH_END(10, t2);
+    if (gg.g == 0) {
+        PH_BEGIN(t3);
+        for (int e = threadIdx.x; e < RR; e += NT) {
+            w.RX[e] = __ldcg(gw.BX + e);
+            w.RY[e] = __ldcg(gw.BY + e);
+        }
+        __syncthreads();
+        int c1 = 0, o1 = 0;
+        const int rr = compress_core(core_ws_sm(w, smem, smem_dbl, R), w.RX, R, w.RY, R, R, eps, tol_q, svd, kmax,
+                                     rlim, gw.CX, gw.CY, R, R, &c1, &o1, red, redv, redi);
+        if (threadIdx.x == 0) { gw.ires[0] = rr; gw.ires[1] = c1; gw.ires[2] = o1; }
+        PH_END(11, t3);
+    }
+    gang_sync(gg);
+    const int r = __ldcg(gw.ires);
+    PH_BEGIN(t4);
+    if (r > 0) {
+        for (int s = top; s >= 1; s /= 2) {
+            if (gs % (2 * s) == 0 && gs + s < Gs) tsqr_node_down(Ck, Nd, gw.nslot, gs, s, R, r, w.G, smem, smem_dbl);
+            gang_sync(gg);
+        }
+    }
+    PH_END(10, t4);
+    PH_BEGIN(t5);
+    const int64_t Rr = (int64_t)R * r;
+    double *Out = side ? V : U;
+    for (int64_t e = threadIdx.x; e < mq * r; e += NT) {
+        const int64_t i = e % mq;
+        const int cc = (int)(e / mq);
+        Out[q0 + i + ldo * cc] = (i < R) ? __ldcg(Ck + (int64_t)gs * Rr + i + (int64_t)R * cc) : 0.0;
+    }
+    *cb = __ldcg(gw.ires + 1);
+    *of = __ldcg(gw.ires + 2);
+    __syncthreads();
+    if (r > 0) local_apply(Pn, mq, R, tau, w.tsr, K, Out + q0, ldo, r, w.G, smem, smem_dbl);
     PH_END(12, t5);
     gang_sync(gg);
     return r;
@@ -1135,11 +1215,14 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     GangWs gw{};
     if (gg) gw = make_gws(gg->shared, K, gg->G);
     int cur = r0;
+    // side-split gangs: a member builds (and factors) only its side's panel
+    const bool doX = !gg || gg->side != 1, doY = !gg || gg->side != 0;
+    const bool split = gg && gg->split;
     PH_BEGIN(tl0);
     for (int64_t e = threadIdx.x; e < mq * (int64_t)r0; e += NT) {
         const int64_t i = e % mq, l = e / mq;
-        w.X[i + mq * l] = __ldcg(U + q0 + i + m * l);
-        w.Y[i + mq * l] = __ldcg(V + q0 + i + m * l);
+        if (doX) w.X[i + mq * l] = __ldcg(U + q0 + i + m * l);
+        if (doY) w.Y[i + mq * l] = __ldcg(V + q0 + i + m * l);
     }
     __syncthreads();
     PH_END(14, tl0);
@@ -1152,7 +1235,10 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         if (t.kind == TM_LR && __ldcg(c.rank + c.fac_rank_src[t.a]) == 0) continue;
         if (cur + width > K) {
             int icb = 0, iof = 0, rk;
-            if (gg)
+            if (split)
+                rk = gang_compress_split(w, gw, *gg, cur, c.eps, interm_tol(c), false, 0, K - maxw, X2 - q0, Y2 - q0,
+                                         mq, &icb, &iof, red, redv, redi, smem, c.smem_dbl);
+            else if (gg)
                 rk = gang_compress(w, gw, *gg, cur, c.eps, interm_tol(c), false, 0, K - maxw, X2 - q0, Y2 - q0, mq,
                                    &icb, &iof, red, redv, redi, smem, c.smem_dbl);
             else
@@ -1166,7 +1252,10 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         }
         PH_BEGIN(tap);
         double *xc = w.X + mq * cur, *yc = w.Y + mq * cur;
-        for (int64_t e = threadIdx.x; e < mq * (int64_t)width; e += NT) { xc[e] = 0.0; yc[e] = 0.0; }
+        for (int64_t e = threadIdx.x; e < mq * (int64_t)width; e += NT) {
+            if (doX) xc[e] = 0.0;
+            if (doY) yc[e] = 0.0;
+        }
         __syncthreads();
         if (t.kind == TM_TT) {
             const DNode na = c.nodes[c.tile_node[t.a]], nb = c.nodes[c.tile_node[t.b]];
@@ -1174,8 +1263,8 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
             const double *A = c.tiles + (int64_t)t.a * HCOV_TILE, *B = c.tiles + (int64_t)t.b * HCOV_TILE;
             for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
                 int i = e & 31, k = e >> 5;
-                if (ar + i >= 0 && ar + i < mq) xc[ar + i + mq * k] = -__ldcg(A + e);
-                if (br + i >= 0 && br + i < mq) yc[br + i + mq * k] = __ldcg(B + e);
+                if (doX && ar + i >= 0 && ar + i < mq) xc[ar + i + mq * k] = -__ldcg(A + e);
+                if (doY && br + i >= 0 && br + i < mq) yc[br + i + mq * k] = __ldcg(B + e);
             }
         } else {
             Fac A = get_fac(c, t.a), B = get_fac(c, t.b);
@@ -1183,7 +1272,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
             const int64_t r_lo = max(R0 + q0, A.row0), r_hi = min(R0 + q0 + mq, A.row0 + A.nrows);
             const int64_t c_lo = max(C0 + q0, B.row0), c_hi = min(C0 + q0 + mq, B.row0 + B.nrows);
             const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcap * c.kcap : nullptr;
-            if (r_hi > r_lo) {
+            if (doX && r_hi > r_lo) {
                 if (Kc) {   // xc = -A K  (columns b < rb), staged GEMM
                     cta_gemm_nt(xc + (r_lo - R0 - q0), mq, r_hi - r_lo, rb, ra, A.p + (r_lo - A.row0), A.ld, Kc, c.kcap,
                                 1, -1.0, smem);
@@ -1196,7 +1285,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
                     }
                 }
             }
-            if (c_hi > c_lo)
+            if (doY && c_hi > c_lo)
                 for (int64_t e = threadIdx.x; e < (c_hi - c_lo) * (int64_t)rb; e += NT) {
                     int64_t i = e % (c_hi - c_lo);
                     int b = (int)(e / (c_hi - c_lo));
@@ -1212,7 +1301,11 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     const double tq = fin ? final_tol(c.eps, cur) : interm_tol(c);
     const int kmx = fin ? c.kmax : 0, rl = fin ? c.kcap : 2 * c.kcap;
     int rk;
-    if (gg) {
+    if (split) {
+        rk = gang_compress_split(w, gw, *gg, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi, smem,
+                                 c.smem_dbl);
+        fl += compress_flops(m, cur, rk) / gg->G;
+    } else if (gg) {
         rk = gang_compress(w, gw, *gg, cur, c.eps, tq, fin, kmx, rl, U, V, m, &cb, &of, red, redv, redi, smem,
                            c.smem_dbl);
         fl += compress_flops(m, cur, rk) / gg->G;

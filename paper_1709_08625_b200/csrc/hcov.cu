@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, const Ctx *__res
         __syncthreads();
         const Ctx &ci = s_ctx;
         const DTask tk = c.tasks[t];
-        Gang gang{member, tk.qcls, ci.gbar + t, c.qctl + QC_ABORT, 0, 0, 0, nullptr};
+        Gang gang{member, tk.qcls, ci.gbar + t, c.qctl + QC_ABORT, 0, 0, 0, nullptr, tk.type == TK_RAPP && tk.pad == 1,
+                  -1, member, tk.qcls};
         Gang *gg = nullptr;
         double *tscr = scr;
         bool use_big = false;
@@ -256,7 +257,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, const Ctx *__res
             // the body's last gang barrier by then).
             if (c.n_bgrp > 0 && (tk.type == TK_ACA || tk.type == TK_RAPP)) {
                 const int64_t m = c.rblk[tk.a].m;
-                const int64_t mq_last = m - (int64_t)(tk.qcls - 1) * (m / tk.qcls);
+                const int Gs = gang.split ? tk.qcls / 2 : tk.qcls;
+                const int64_t mq_last = m - (int64_t)(Gs - 1) * (m / Gs);
                 if (mq_last > c.big_mq) {
                     gang_sync(gang);
                     if (gang.g == 0 && threadIdx.x == 0) {
@@ -708,7 +710,8 @@ struct hcov_tree_s {
     std::vector<hcov_hmat> extra;            // instances 1.. of the last theta batch
     // W / product-slot words used by the most demanding run so far at capacity est_kcap (per-instance
     // pool sizing of theta batches)
-    int est_kcap = -1;
+    int est_kcap = -1, est_kmax = -1;
+    double est_eps = -1.0;
     int64_t est_w = 0, est_p = 0;
     ~hcov_tree_s();
 };
@@ -1164,7 +1167,10 @@ hcov_status check_abort(hcov_hmat h, cudaStream_t st, int32_t *hf)
     {
         // pool words this run used: sizing of later theta batches on this tree
         hcov_tree t = h->t;
-        if (t->est_kcap != h->kcap_alloc) { t->est_kcap = h->kcap_alloc; t->est_w = 0; t->est_p = 0; }
+        if (t->est_kcap != h->kcap_alloc || t->est_eps != h->trunc.eps || t->est_kmax != h->trunc.kmax) {
+            t->est_kcap = h->kcap_alloc; t->est_eps = h->trunc.eps; t->est_kmax = h->trunc.kmax;
+            t->est_w = 0; t->est_p = 0;
+        }
         t->est_w = std::max<int64_t>(t->est_w, (int64_t)mem[0]);
         t->est_p = std::max<int64_t>(t->est_p, (int64_t)mem[1]);
     }
@@ -1462,7 +1468,8 @@ hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *t
     size_t next = 0;
     // pool sizes of the batch instances come from the words an earlier run on this tree used; without
     // that, the first candidate runs alone (all free memory) and provides it
-    if (t->est_kcap != kcap || t->est_w + t->est_p == 0) {
+    if (t->est_kcap != kcap || t->est_eps != trunc->eps || t->est_kmax != trunc->kmax || t->est_w + t->est_p == 0 ||
+        !t->cached) {
         hcov_result r{};
         const int k = todo[next++];
         if ((s = record(k, hcov_eval(t, thetas + k, trunc, Z_dev, stream, &r), r))) return s;
@@ -1664,6 +1671,150 @@ hcov_status hcov_pcg(hcov_hmat A, hcov_hmat M, const double *b_dev, double *x_de
     *iters = it;
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
+    return HCOV_OK;
+}
+
+// ---- NEXT (f3): accuracy diagnostics of Sec. 4 (Tables 2-4) ----------
+namespace {
+// x_i in [-1/2, 1/2): a counter-based hash of (i, seed) (deterministic start vector of the power
+// iterations)
+__global__ void k_start_vec(int64_t n, uint64_t seed, double *x)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + seed * 0xD1B54A32D192ED03ull + 0x632BE59BD9B4E019ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        x[i] = (double)(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    }
+}
+// y = a * x (n)
+__global__ void k_scale(int64_t n, double a, const double *x, double *y)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        y[k] = a * x[k];
+}
+// acc[0] += x[j] (one thread: the trace accumulates in column order)
+__global__ void k_pick_add(const double *x, int64_t j, double *acc)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) acc[0] += x[j];
+}
+
+struct DiagBufs {
+    DevBuf B;
+    double *xi, *yi, *t12, *part, *res, *resh = nullptr;
+    ~DiagBufs() { if (resh) cudaFreeHost(resh); }
+    hcov_status init(const Plan &P, int kcap)
+    {
+        CK(B.get(&xi, P.n_pad)); CK(B.get(&yi, P.n_pad));
+        CK(B.get(&t12, 2 * std::max<int64_t>(1, P.n_r()) * std::max(1, kcap)));
+        CK(B.get(&part, DOT_BLOCKS)); CK(B.get(&res, 1));
+        CK(cudaMallocHost(&resh, sizeof(double)));
+        return HCOV_OK;
+    }
+};
+}  // namespace
+
+hcov_status hcov_norm2_diff(hcov_hmat A, hcov_hmat Bm, int32_t iters, uint64_t seed, hcov_stream stream, double *out)
+{
+    if (!A || !Bm || !out || iters < 1) return HCOV_ERR_INVALID_ARG;
+    if (A->state != 1 || Bm->state != 1) return HCOV_ERR_STATE;
+    if (A->t->P.n != Bm->t->P.n) return HCOV_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = A->t->P.n;
+    DiagBufs da, db;
+    hcov_status s;
+    if ((s = da.init(A->t->P, A->ctx.kcap)) || (s = db.init(Bm->t->P, Bm->ctx.kcap))) return s;
+    DevBuf B;
+    double *x, *y, *z;
+    CK(B.get(&x, n)); CK(B.get(&y, n)); CK(B.get(&z, n));
+    k_start_vec<<<296, 256, 0, st>>>(n, seed, x);
+    double nx = std::sqrt(dot_dev(x, x, n, da.part, da.res, da.resh, st));
+    k_scale<<<296, 256, 0, st>>>(n, 1.0 / nx, x, x);
+    g_prof.launches += 2;
+    double lam = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        // y = (A - B) x
+        if ((s = matvec_ext(A, x, y, da.xi, da.yi, da.t12, st))) return s;
+        if ((s = matvec_ext(Bm, x, z, db.xi, db.yi, db.t12, st))) return s;
+        k_axpby<<<296, 256, 0, st>>>(n, -1.0, z, 1.0, y);
+        g_prof.launches += 1;
+        const double ny = std::sqrt(dot_dev(y, y, n, da.part, da.res, da.resh, st));
+        lam = std::max(lam, ny);                 // ||(A - B) x|| with ||x|| = 1: -> |lambda|_max
+        if (!(ny > 0)) break;
+        k_scale<<<296, 256, 0, st>>>(n, 1.0 / ny, y, x);
+        g_prof.launches += 1;
+    }
+    CK(cudaStreamSynchronize(st));
+    *out = lam;
+    return HCOV_OK;
+}
+
+hcov_status hcov_inv_error(hcov_hmat A, hcov_hmat M, int32_t iters, uint64_t seed, hcov_stream stream, double *out)
+{
+    if (!A || !M || !out || iters < 1) return HCOV_ERR_INVALID_ARG;
+    if (A->state != 1 || M->state < 2) return HCOV_ERR_STATE;
+    if (A->t->P.n != M->t->P.n) return HCOV_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = A->t->P.n;
+    DiagBufs da;
+    hcov_status s;
+    if ((s = da.init(A->t->P, A->ctx.kcap))) return s;
+    DevBuf B;
+    double *x, *y, *e, *w;
+    CK(B.get(&x, n)); CK(B.get(&y, n)); CK(B.get(&e, n)); CK(B.get(&w, n));
+    k_start_vec<<<296, 256, 0, st>>>(n, seed, x);
+    double nx = std::sqrt(dot_dev(x, x, n, da.part, da.res, da.resh, st));
+    k_scale<<<296, 256, 0, st>>>(n, 1.0 / nx, x, x);
+    g_prof.launches += 2;
+    double best = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        // e = E x = x - M^{-1} A x;  w = E^T e = e - A M^{-1} e  (A, M symmetric)
+        if ((s = matvec_ext(A, x, y, da.xi, da.yi, da.t12, st))) return s;
+        if ((s = solve_ext(M, y, e, true, true, st))) return s;
+        k_axpby<<<296, 256, 0, st>>>(n, 1.0, x, -1.0, e);
+        const double ne = std::sqrt(dot_dev(e, e, n, da.part, da.res, da.resh, st));
+        best = std::max(best, ne);               // ||E x||, ||x|| = 1: -> ||E||_2
+        if ((s = solve_ext(M, e, y, true, true, st))) return s;
+        if ((s = matvec_ext(A, y, w, da.xi, da.yi, da.t12, st))) return s;
+        k_axpby<<<296, 256, 0, st>>>(n, 1.0, e, -1.0, w);
+        const double nw = std::sqrt(dot_dev(w, w, n, da.part, da.res, da.resh, st));
+        g_prof.launches += 2;
+        if (!(nw > 0)) break;
+        k_scale<<<296, 256, 0, st>>>(n, 1.0 / nw, w, x);
+        g_prof.launches += 1;
+    }
+    CK(cudaStreamSynchronize(st));
+    *out = best;
+    return HCOV_OK;
+}
+
+hcov_status hcov_trace_inv(hcov_hmat M, hcov_hmat A, hcov_stream stream, double *out)
+{
+    if (!M || !A || !out) return HCOV_ERR_INVALID_ARG;
+    if (A->state != 1 || M->state < 2) return HCOV_ERR_STATE;
+    if (A->t->P.n != M->t->P.n) return HCOV_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = A->t->P.n;
+    const int mc = 64;
+    DevBuf B;
+    double *cols, *x, *acc;
+    CK(B.get(&cols, n * mc)); CK(B.get(&x, n)); CK(B.get(&acc, 1));
+    CK(cudaMemsetAsync(acc, 0, sizeof(double), st));
+    std::vector<int64_t> ids(mc);
+    hcov_status s;
+    for (int64_t j0 = 0; j0 < n; j0 += mc) {
+        const int m = (int)std::min<int64_t>(mc, n - j0);
+        for (int k = 0; k < m; ++k) ids[k] = j0 + k;
+        if ((s = hcov_columns(A, ids.data(), m, cols, stream))) return s;
+        for (int k = 0; k < m; ++k) {
+            if ((s = solve_ext(M, cols + n * k, x, true, true, st))) return s;
+            k_pick_add<<<1, 32, 0, st>>>(x, j0 + k, acc);
+            g_prof.launches += 1;
+        }
+    }
+    CK(cudaMemcpyAsync(out, acc, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     return HCOV_OK;
 }
 

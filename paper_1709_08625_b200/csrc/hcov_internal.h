@@ -10,7 +10,7 @@
                               // formed gang per band can hold CTAs, so every gang eventually forms)
 #define HCOV_DENSE_MAX 256    // low-rank blocks up to this size are recompressed from a dense accumulation
 #define HCOV_SMEM_DBL 28160 // dynamic shared memory of the engine CTA (220 KB + static <= 227 KB; one 512-thread CTA per SM)
-#define HCOV_BIG_MQ 4096      // gang members with more rows use a big-member scratch slot (hcov.cu)
+#define HCOV_BIG_MQ 8192      // gang members with more rows use a big-member scratch slot (hcov.cu)
 #define HCOV_BIG_GROUPS 4     // big-member groups (HCOV_GANG slots each)
 #define HCOV_MAX_BATCH 8      // H-matrices (theta candidates) per engine launch in hcov_mle_batch
 #define HCOV_GANG_MIN 512     // low-rank blocks from this size on are processed by gangs of min(8, m/256) CTAs
@@ -60,7 +60,7 @@ struct DTask {
     int32_t a, b, c, d;
     int32_t qcls;      // 0 = one CTA; G > 1 = gang task of G CTAs (G consecutive queue entries)
     int32_t band;      // queue 0 priority band (HCOV_BANDS - 1 = most urgent), by the task's bottom level
-    int32_t pad;
+    int32_t pad;       // RAPP gang: 1 = side-split (members 0..G/2-1 hold X rows, G/2..G-1 Y rows)
 };
 #define HCOV_BANDS 16
 

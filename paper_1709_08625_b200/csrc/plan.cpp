@@ -29,6 +29,14 @@ inline int32_t gang_of(int64_t m)
     const int64_t gmax = m >= 65536 ? HCOV_GANG : 4;
     return (int32_t)std::min<int64_t>(gmax, std::max<int64_t>(2, m / 256));
 }
+// RAPP gangs of blocks below 65,536 rows are side-split (DTask.pad = 1): half the members factor
+// the X panel, half the Y panel (one QR per member instead of two; engine.cuh gang_compress_split)
+inline bool rapp_split(int64_t m) { return m >= HCOV_GANG_MIN && m < 65536; }
+inline int32_t rapp_gang_of(int64_t m)
+{
+    if (!rapp_split(m)) return gang_of(m);
+    return m <= 512 ? 4 : HCOV_GANG;
+}
 
 inline int64_t heap_id(int l, int64_t c) { return ((int64_t)1 << l) - 1 + c; }
 inline uint64_t node_key(int l, int64_t i, int64_t j)
@@ -194,6 +202,7 @@ struct Builder {
             if (last && fin_type >= 0) { ty = fin_type; dp.push_back(extra_dep); }
             const int32_t dd = (app_type == TK_RAPP) ? (last ? 1 : 0) : d;
             prev = task(ty, a, base + b, base + e, dd, qcls, dp);
+            if (app_type == TK_RAPP && rapp_split(P.rblk[a].m)) P.tasks[prev].pad = 1;
         }
         return prev;
     }
@@ -410,7 +419,7 @@ struct Builder {
                 const int32_t dt = P.diag_tile[c];
                 fin_tile[x.idx] = chain(e, tile_fill[x.idx], TK_TAPP, TK_TRSM, x.idx, dt, fin_tile[dt], 0);
             } else if (x.type == ND_R) {
-                const int32_t qc = gang_of(P.rblk[x.idx].m);
+                const int32_t qc = rapp_gang_of(P.rblk[x.idx].m);
                 rfin[x.idx] = chain(e, aca_task[x.idx], TK_RAPP, -1, x.idx, 0, -1, qc);
                 rents.push_back(x.idx);
             }
@@ -705,6 +714,10 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
         P.max_rm = std::max<int64_t>(P.max_rm, r.m);
         const int32_t g = gang_of(r.m);
         if (g > 0) P.max_mq = std::max<int64_t>(P.max_mq, r.m - (int64_t)(g - 1) * (r.m / g));   // last member
+        if (rapp_split(r.m)) {   // side-split RAPP gang: G/2 members per side
+            const int64_t gs = rapp_gang_of(r.m) / 2;
+            P.max_mq = std::max<int64_t>(P.max_mq, r.m - (gs - 1) * (r.m / gs));
+        }
     }
     return 0;
 }
