@@ -16,7 +16,9 @@ Functions and the passages they follow (PAPER.md = the paper's LaTeX text):
   L = -n/2 log(2 pi) - 1/2 log det C - 1/2 Z^T C^{-1} Z, computed through the Cholesky
   factor C = L L^T exactly as Eq. (2) / Def. 1 writes it with the
   exact factor: log det C = 2 sum log L_ii, v = L^{-1} Z, Z^T C^{-1} Z = v^T v.
-  The factorisation and the triangular solve are LAPACK library primitives.
+  The factorisation and the triangular solve are LAPACK library primitives (MKL, through
+  plain PyTorch CPU ops: the OpenBLAS builds of numpy/scipy in this image return a spurious
+  "not positive definite" (scipy, 32-bit LAPACK) or crash (numpy) for n >= 32,768).
 * ``loglik_ou_collinear``  — Eq. (1) in closed form for nu = 1/2, tau^2 = 0 on collinear
   points: the exponential covariance (Eq. (3) at nu = 1/2) on a line is the
   Ornstein-Uhlenbeck process, which is Markov, so the joint density factorises into
@@ -32,13 +34,24 @@ import ctypes
 import os
 import subprocess
 
-import numpy as np
-import scipy.linalg as sla
-from threadpoolctl import threadpool_limits
+import contextlib
 
-# Host threads used by the oracle (OpenMP fill + LAPACK). Half the logical CPUs by
-# default: with all logical CPUs OpenBLAS' dpotrf degrades badly on SMT/cgroup hosts.
-THREADS = int(os.environ.get("HCOV_ORACLE_THREADS", max(1, (os.cpu_count() or 2) // 2)))
+import numpy as np
+import torch
+
+# Host threads used by the oracle (OpenMP fill + MKL LAPACK): every host core by default.
+THREADS = int(os.environ.get("HCOV_ORACLE_THREADS", os.cpu_count() or 1))
+
+
+@contextlib.contextmanager
+def lapack_threads(k: int = 0):
+    """Run MKL (torch CPU) LAPACK/BLAS calls on k (default THREADS) threads."""
+    old = torch.get_num_threads()
+    torch.set_num_threads(k or THREADS)
+    try:
+        yield
+    finally:
+        torch.set_num_threads(old)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "matern.c")
@@ -117,20 +130,28 @@ class NotSPD(Exception):
 
 
 def cholesky(C: np.ndarray) -> np.ndarray:
-    """Lower Cholesky factor (LAPACK dpotrf). Raises NotSPD if a pivot is <= 0."""
-    try:
-        with threadpool_limits(THREADS):
-            return sla.cholesky(C, lower=True, check_finite=False)
-    except np.linalg.LinAlgError as e:  # pragma: no cover - message passthrough
-        raise NotSPD(str(e))
+    """Lower Cholesky factor (LAPACK dpotrf, MKL). Raises NotSPD if a pivot is <= 0."""
+    with lapack_threads():
+        L, info = torch.linalg.cholesky_ex(torch.from_numpy(np.ascontiguousarray(C, dtype=np.float64)))
+    if int(info) != 0:
+        raise NotSPD(f"leading minor {int(info)} is not positive definite")
+    return L.numpy()
+
+
+def solve_lower(L: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """x = L^{-1} b for lower-triangular L (LAPACK dtrtrs / BLAS dtrsm, MKL)."""
+    b = np.asarray(b, dtype=np.float64)
+    B = torch.from_numpy(np.ascontiguousarray(b.reshape(b.shape[0], -1)))
+    with lapack_threads():
+        x = torch.linalg.solve_triangular(torch.from_numpy(L), B, upper=False)
+    return x.numpy().reshape(b.shape)
 
 
 def loglik_from_factor(L: np.ndarray, Z: np.ndarray):
     """Eq. (1) through the factor: returns (loglik, logdet, quad)."""
     n = L.shape[0]
     logdet = 2.0 * float(np.sum(np.log(np.diag(L))))
-    with threadpool_limits(THREADS):
-        v = sla.solve_triangular(L, np.asarray(Z, dtype=np.float64), lower=True, check_finite=False)
+    v = solve_lower(L, Z)
     quad = float(v @ v)
     ll = -0.5 * n * np.log(2.0 * np.pi) - 0.5 * logdet - 0.5 * quad
     return ll, logdet, quad
@@ -148,8 +169,9 @@ def sample_dense(s, xi, sigma2, ell, nu, nugget):
     """Z = L xi with the exact dense Cholesky factor (external order)."""
     C = cov_dense(s, sigma2, ell, nu, nugget)
     L = cholesky(C)
-    with threadpool_limits(THREADS):
-        return L @ np.asarray(xi, dtype=np.float64)
+    del C
+    with lapack_threads():
+        return (torch.from_numpy(L) @ torch.from_numpy(np.ascontiguousarray(xi, dtype=np.float64))).numpy()
 
 
 def loglik_ou_collinear(x, Z, sigma2, ell):

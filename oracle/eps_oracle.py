@@ -22,9 +22,10 @@ from typing import Dict, List, Sequence, Tuple
 
 import numpy as np
 
-from . import cholesky, cov_dense, loglik_from_factor, NotSPD, THREADS
+import torch
+
+from . import cholesky, cov_dense, loglik_from_factor, NotSPD, lapack_threads
 from .htree import cluster_tree, lowrank_blocks
-from threadpoolctl import threadpool_limits
 
 
 def eps_rank(sig: np.ndarray, eps: float, kmax: int = 0) -> int:
@@ -41,11 +42,11 @@ def truncation_spectra(s: np.ndarray, C: np.ndarray, eta: float = 2.0, dense_bel
     """SVD of every admissible lower block of C: list of (rows, cols, U, sig, Vt)."""
     T = cluster_tree(s)
     out = []
-    with threadpool_limits(THREADS):
+    with lapack_threads():
         for rows, cols, _lvl in lowrank_blocks(T, eta, dense_below):
-            B = C[np.ix_(rows, cols)]
-            U, sig, Vt = np.linalg.svd(B, full_matrices=False)
-            out.append((rows, cols, U, sig, Vt))
+            B = torch.from_numpy(np.ascontiguousarray(C[np.ix_(rows, cols)]))
+            U, sig, Vt = torch.linalg.svd(B, full_matrices=False)   # LAPACK gesdd (MKL)
+            out.append((rows, cols, U.numpy(), sig.numpy(), Vt.numpy()))
     return out
 
 

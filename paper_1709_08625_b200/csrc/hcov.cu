@@ -733,6 +733,10 @@ struct hcov_hmat_s {
     unsigned long long *mem = nullptr;
     int64_t wcap = 0, pcap = 0;
     int64_t w_budget = 0, p_budget = 0;   // > 0: pool sizes (words) fixed by a theta batch
+    // pool bump counters once the factor exists (W, P words): every solve-mode run restarts from
+    // them, so repeated solves reuse their product slots instead of growing the pools
+    unsigned long long fac_mem[2] = {0, 0};
+    bool fac_mem_set = false;
     void release_pools()
     {
         cudaFree(W);
@@ -1151,6 +1155,7 @@ hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trun
     CK(cudaMemsetAsync(h->woff, 0xff, std::max<size_t>(1, P.phw.size()) * sizeof(int64_t), st));
     CK(cudaMemsetAsync(h->poff, 0xff, std::max<size_t>(1, P.slots.size()) * sizeof(int64_t), st));
     CK(cudaMemsetAsync(h->mem, 0, 4 * sizeof(unsigned long long), st));
+    h->fac_mem_set = false;
     return HCOV_OK;
 }
 
@@ -1535,6 +1540,13 @@ namespace {
 // in (external) -> vbuf -> [forward] -> [back] -> out (external); factored H-matrix.
 hcov_status solve_ext(hcov_hmat h, const double *in, double *out, bool fwd, bool back, cudaStream_t st)
 {
+    if (!h->fac_mem_set) {
+        CK(cudaMemcpyAsync(h->fac_mem, h->mem, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        h->fac_mem_set = true;
+    } else {
+        CK(cudaMemcpyAsync(h->mem, h->fac_mem, 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+    }
     LAUNCH(PC_AUX, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, in, h->vbuf));
     hcov_status s;
     if (fwd && (s = engine_run(h, 3, st))) return s;
