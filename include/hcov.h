@@ -245,8 +245,10 @@ const char *hcov_prof_task_name(int32_t type);
 
 /* Unit test of the truncation step A6 on one CTA: X, Y (m x R, col-major device
  * arrays) -> U, V (m x rlim device arrays) with X Y^T ~ U V^T, sigma_{r+1} <= eps sigma_1, r <= kmax
- * (kmax > 0), r <= rlim.  path 0: Householder QRs; 1: shifted CholeskyQR3 (taken when m >= 2R).
- * out3_host: rank, cap-bound flag, overflow flag.  Synchronises the device. */
+ * (kmax > 0), r <= rlim.  path 0: Householder QRs; 1: shifted CholeskyQR3 (taken when m >= 2R);
+ * 2: shared-memory Householder (m <= 1024, m R + R within the CTA's shared memory); 3: the dense-mode
+ * pipeline of a small low-rank block (m <= 256): S = X Y^T formed densely, fully pivoted cross
+ * approximation to 0.1 eps, then path 2 (R23).  out3_host: rank, cap-bound flag, overflow flag.  Synchronises the device. */
 hcov_status hcov_test_truncate(const double *X_dev, const double *Y_dev, int64_t m, int32_t R, double eps,
                                int32_t kmax, int32_t rlim, int32_t path, double *U_dev, double *V_dev,
                                int32_t *out3_host);

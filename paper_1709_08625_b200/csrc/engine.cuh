@@ -121,13 +121,19 @@ __device__ __forceinline__ int64_t pool_bump(const Ctx &c, int which, int64_t si
     }
     return off;
 }
-// Product slot s of `size` doubles (single producer task; CTA-collective).
+// Product slot s of `size` doubles (single producer task; CTA-collective).  A slot keeps its offset
+// until the next assembly resets poff[]: later solve-mode runs on the same factor (hcov_solve, PCG,
+// the diagnostics) reuse it (the slot's size depends only on the factor's ranks) instead of
+// growing the pool.
 __device__ double *slot_alloc(const Ctx &c, int s, int64_t size)
 {
     __shared__ int64_t s_off;
     if (threadIdx.x == 0) {
-        const int64_t off = pool_bump(c, 1, size, c.pcap);
-        atomicExch((unsigned long long *)(c.poff + s), (unsigned long long)off);
+        int64_t off = (int64_t)__ldcg(c.poff + s);
+        if (off < 0) {
+            off = pool_bump(c, 1, size, c.pcap);
+            atomicExch((unsigned long long *)(c.poff + s), (unsigned long long)off);
+        }
         s_off = off;
     }
     __syncthreads();
@@ -1652,8 +1658,8 @@ __device__ void task_phwr(const Ctx &c, const DTask &tk, double *smem, double &f
     const int64_t ro = i * HCOV_LEAF - rho0;
     double *Ws = smem;                        // 32 x kcap
     double *Ts = Ws + 32 * (int64_t)c.kcap;   // 32 x 32
-    double *Xs = Ts + HCOV_TILE;              // 32 x kcap
-    double *Us = Xs + 32 * (int64_t)max(32, c.kcap);
+    double *Xs = Ts + HCOV_TILE;              // 32 x rp (tile branch) or the rx x rp core slice
+    double *Us = Xs + max(32 * (int64_t)max(32, c.kcap), (int64_t)c.kcap * c.kcap);   // 32 x rx
     const int tot = partner_prefix(c, q, q.part_cnt);
     double *Wq = w_acquire(c, tk.a, (int64_t)q.m * tot + 1);
     int pre = 0;
@@ -1804,7 +1810,8 @@ __host__ __device__ inline int64_t engine_smem_doubles(int kcap)
     int64_t a = tile_smem_doubles(kcap);
     int64_t k = kcap > 32 ? kcap : 32;
     int64_t b = 32 * SEG_MAXCOL + HCOV_TILE + k * SEG_MAXCOL + 32 * (int64_t)kcap + SEG_MAXCOL + 8;
-    int64_t cc = 32 * (int64_t)kcap + HCOV_TILE + 32 * k + 32 * (int64_t)kcap + 8;
+    int64_t cc = 32 * (int64_t)kcap + HCOV_TILE + (32 * k > (int64_t)kcap * kcap ? 32 * k : (int64_t)kcap * kcap) +
+                 32 * (int64_t)kcap + 8;   // task_phwr
     int64_t m = a > b ? a : b;
     m = m > cc ? m : cc;
     const int64_t floor_dbl = (NT >= 512) ? HCOV_SMEM_DBL : 0;   // one CTA per SM: panels resident in shared memory

@@ -26,8 +26,16 @@ namespace {
         if (e_ != cudaSuccess) return map_err(e_);            \
     } while (0)
 
+static bool verbose()
+{
+    static int v = -1;
+    if (v < 0) { const char *e = std::getenv("HCOV_VERBOSE"); v = (e && *e && *e != '0') ? 1 : 0; }
+    return v == 1;
+}
+
 hcov_status map_err(cudaError_t e)
 {
+    if (verbose()) std::fprintf(stderr, "hcov: CUDA error %d (%s)\n", (int)e, cudaGetErrorString(e));
     if (e == cudaErrorMemoryAllocation) return HCOV_ERR_OUT_OF_MEMORY;
     return HCOV_ERR_CUDA;
 }
@@ -629,14 +637,35 @@ __global__ void k_axpby(int64_t n, double a, const double *x, double b, double *
 // Unit-test kernel for the truncation (A6): one CTA truncates X Y^T (m x m, R columns).
 __global__ void __launch_bounds__(NT) k_test_truncate(double *scr, int64_t m, int R, int K, double eps, int kmax,
                                                       int rlim, int path, double *U, double *V, int *rank,
-                                                      int64_t smem_dbl)
+                                                      int64_t smem_dbl, const double *Xin, const double *Yin)
 {
     extern __shared__ double smem[];
     __shared__ double red[NWARP], redv[NWARP];
     __shared__ int64_t redi[NWARP];
     double *X2, *Y2;
-    CompressWs w = make_ws(scr, m, K, &X2, &Y2);
     int cb = 0, of = 0;
+    if (path == 3) {
+        // the dense-mode pipeline of a small low-rank block (task_rapp, m <= HCOV_DENSE_MAX): S = X Y^T
+        // formed densely (in shared memory when it leaves the GEMM staging room), fully pivoted cross
+        // approximation to 0.1 eps, then the shared-memory truncation path
+        const bool s_sm = m * m + 32 * 256 <= smem_dbl;
+        double *S = s_sm ? smem : scr;
+        CompressWs w = make_ws(scr + m * m, m, K, &X2, &Y2);
+        for (int64_t e = threadIdx.x; e < m * m; e += NT) {
+            const int64_t i = e % m, j = e / m;
+            double a = 0.0;
+            for (int l = 0; l < R; ++l) a = fma(Xin[i + m * l], Yin[j + m * l], a);
+            S[e] = a;
+        }
+        __syncthreads();
+        const int KA = (int)(m < K ? m : K);
+        const int k = aca_full(S, m, w.X, w.Y, KA, 0.1 * eps / (double)m, 0.1 * eps, red, redv, redi);
+        const int r = compress(w, m, k, eps, final_tol(eps, k), true, kmax, rlim, U, V, m, &cb, &of, red, redv, redi,
+                               smem, smem_dbl, 2);
+        if (threadIdx.x == 0) { rank[0] = r; rank[1] = cb; rank[2] = of; }
+        return;
+    }
+    CompressWs w = make_ws(scr, m, K, &X2, &Y2);
     const int r = compress(w, m, R, eps, final_tol(eps, R), true, kmax, rlim, U, V, m, &cb, &of, red, redv, redi,
                            path >= 1 ? smem : nullptr, smem_dbl, path);
     if (threadIdx.x == 0) { rank[0] = r; rank[1] = cb; rank[2] = of; }
@@ -733,10 +762,6 @@ struct hcov_hmat_s {
     unsigned long long *mem = nullptr;
     int64_t wcap = 0, pcap = 0;
     int64_t w_budget = 0, p_budget = 0;   // > 0: pool sizes (words) fixed by a theta batch
-    // pool bump counters once the factor exists (W, P words): every solve-mode run restarts from
-    // them, so repeated solves reuse their product slots instead of growing the pools
-    unsigned long long fac_mem[2] = {0, 0};
-    bool fac_mem_set = false;
     void release_pools()
     {
         cudaFree(W);
@@ -1155,7 +1180,6 @@ hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trun
     CK(cudaMemsetAsync(h->woff, 0xff, std::max<size_t>(1, P.phw.size()) * sizeof(int64_t), st));
     CK(cudaMemsetAsync(h->poff, 0xff, std::max<size_t>(1, P.slots.size()) * sizeof(int64_t), st));
     CK(cudaMemsetAsync(h->mem, 0, 4 * sizeof(unsigned long long), st));
-    h->fac_mem_set = false;
     return HCOV_OK;
 }
 
@@ -1168,7 +1192,12 @@ hcov_status check_abort(hcov_hmat h, cudaStream_t st, int32_t *hf)
     CK(cudaMemcpyAsync(hf, h->fail, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hf + 1, h->flags, 5 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (mem[2]) return HCOV_ERR_OUT_OF_MEMORY;   // a pool overflow also raises the abort flag
+    if (mem[2]) {   // a pool overflow also raises the abort flag
+        if (verbose())
+            std::fprintf(stderr, "hcov: pool overflow: W used %llu of %lld, P used %llu of %lld, overflows %llu\n",
+                         mem[0], (long long)h->wcap, mem[1], (long long)h->pcap, mem[2]);
+        return HCOV_ERR_OUT_OF_MEMORY;
+    }
     {
         // pool words this run used: sizing of later theta batches on this tree
         hcov_tree t = h->t;
@@ -1540,13 +1569,6 @@ namespace {
 // in (external) -> vbuf -> [forward] -> [back] -> out (external); factored H-matrix.
 hcov_status solve_ext(hcov_hmat h, const double *in, double *out, bool fwd, bool back, cudaStream_t st)
 {
-    if (!h->fac_mem_set) {
-        CK(cudaMemcpyAsync(h->fac_mem, h->mem, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        h->fac_mem_set = true;
-    } else {
-        CK(cudaMemcpyAsync(h->mem, h->fac_mem, 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
-    }
     LAUNCH(PC_AUX, st, k_permute_in<<<256, 256, 0, st>>>(h->ctx, in, h->vbuf));
     hcov_status s;
     if (fwd && (s = engine_run(h, 3, st))) return s;
@@ -2085,17 +2107,21 @@ hcov_status hcov_test_truncate(const double *X_dev, const double *Y_dev, int64_t
                                int32_t *out3_host)
 {
     if (!X_dev || !Y_dev || !U_dev || !V_dev || !out3_host || m < 1 || R < 0 || R > 224 || rlim < 1) return HCOV_ERR_INVALID_ARG;
-    const int K = R > 0 ? R : 1;
-    const int64_t need = 6 * m * K + 8 * (int64_t)K * K + 10 * K + m / 8 + 64;
+    if (path == 3 && m > HCOV_DENSE_MAX) return HCOV_ERR_INVALID_ARG;
+    const int K = path == 3 ? (int)std::max<int64_t>(m, R) : (R > 0 ? R : 1);
+    const int64_t need = (path == 3 ? m * m : 0) + 6 * m * K + 8 * (int64_t)K * K + 10 * K + m / 8 + 64;
     double *scr = nullptr;
     int *rk = nullptr;
     CK(cudaMalloc(&scr, need * sizeof(double)));
     CK(cudaMalloc(&rk, 3 * sizeof(int)));
-    CK(cudaMemcpy(scr, X_dev, m * (int64_t)R * sizeof(double), cudaMemcpyDeviceToDevice));
-    CK(cudaMemcpy(scr + m * K, Y_dev, m * (int64_t)R * sizeof(double), cudaMemcpyDeviceToDevice));
+    if (path != 3) {
+        CK(cudaMemcpy(scr, X_dev, m * (int64_t)R * sizeof(double), cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpy(scr + m * K, Y_dev, m * (int64_t)R * sizeof(double), cudaMemcpyDeviceToDevice));
+    }
     const int64_t smem = HCOV_SMEM_DBL * sizeof(double);
     CK(cudaFuncSetAttribute(k_test_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_test_truncate<<<1, NT, smem, 0>>>(scr, m, R, K, eps, kmax, rlim, path, U_dev, V_dev, rk, HCOV_SMEM_DBL);
+    k_test_truncate<<<1, NT, smem, 0>>>(scr, m, R, K, eps, kmax, rlim, path, U_dev, V_dev, rk, HCOV_SMEM_DBL,
+                                        X_dev, Y_dev);
     cudaError_t e = cudaDeviceSynchronize();
     if (e == cudaSuccess) e = cudaMemcpy(out3_host, rk, 3 * sizeof(int), cudaMemcpyDeviceToHost);
     cudaFree(scr);

@@ -61,3 +61,19 @@ def _check(path, kind, m, R, eps):
 @pytest.mark.parametrize("m,R,eps", [(512, 150, 1e-10), (256, 200, 1e-12), (1024, 120, 1e-9), (300, 224, 1e-13)])
 def test_truncation_large_capacity(path, kind, m, R, eps):
     _check(path, kind, m, R, eps)
+
+
+# the dense-mode pipeline of small low-rank blocks (R23: dense S, fully pivoted ACA, shared-memory
+# truncation) at tight eps, where the cross approximation runs to (or near) full rank
+@pytest.mark.parametrize("kind", ["decay", "dependent", "scaled"])
+@pytest.mark.parametrize("m,R,eps", [(128, 128, 1e-13), (128, 100, 1e-13), (64, 64, 1e-13), (128, 90, 3e-13),
+                                     (256, 200, 1e-13), (200, 150, 1e-12), (96, 60, 1e-8)])
+def test_truncation_dense_mode_pipeline(kind, m, R, eps):
+    _check(3, kind, m, R, eps)
+
+
+# the smem path with R = m (a full-rank cross approximation of a dense-mode block) at tight eps
+@pytest.mark.parametrize("kind", ["decay", "dependent", "scaled"])
+@pytest.mark.parametrize("m,R,eps", [(128, 128, 1e-13), (120, 110, 1e-13), (64, 64, 1e-13)])
+def test_truncation_smem_full_rank_tight(kind, m, R, eps):
+    _check(2, kind, m, R, eps)

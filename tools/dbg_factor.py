@@ -13,12 +13,14 @@ import oracle, synth
 import paper_1709_08625_b200 as H
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1200
+mode = sys.argv[2] if len(sys.argv) > 2 else "base"
 th = (1.0, 0.1, 0.5, 1e-6)
 s = synth.uniform_points(n, 11)
 Z = oracle.sample_dense(s, synth.xi(n, 12), *th)
 ref = oracle.loglik_dense(s, Z, *th)
 dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
 T = H.Tree(dev(s))
+Tdb = {db: H.Tree(dev(s), dense_below=db) for db in (64, 128, 256)}
 perm = T.perm_i2e()
 real = np.nonzero(perm >= 0)[0]            # internal positions of real points
 pr = perm[real]
@@ -34,9 +36,13 @@ for e in (1e-13, 1e-11, 1e-9):
           f"logdet rel {abs(v[1]-ref[1])/abs(ref[1]):.2e} quad rel {abs(v[2]-ref[2])/abs(ref[2]):.2e}")
           + f" max_rank {eo[('info', e)]['max_rank']}", flush=True)
 
-cases = [(1e-13, 64), (1e-13, 24), (1e-11, 64), (1e-11, 24), (1e-9, 64), (1e-9, 24), (1e-9, 21)]
-for eps, kcap in cases:
-    hm = H.HMatrix(T, th, eps=eps, kcap=kcap)
+if mode == "base":
+    cases = [(1e-13, 64, 32), (1e-13, 24, 32), (1e-11, 64, 32), (1e-11, 24, 32), (1e-9, 64, 32), (1e-9, 24, 32), (1e-9, 21, 32)]
+else:   # bisection of the eps <= 1e-12 defect
+    cases = [(1e-12, 64, 32), (3e-13, 64, 32), (1e-13, 64, 64), (1e-13, 64, 128), (1e-13, 64, 256),
+             (1e-13, 80, 32), (1e-13, 96, 32), (1e-12, 96, 32), (3e-12, 64, 32)]
+for eps, kcap, db in cases:
+    hm = H.HMatrix(T if db == 32 else Tdb[db], th, eps=eps, kcap=kcap)
     # assembled C~ columns (external order) vs exact
     cols = hm.columns(list(range(n)))
     Ct = cols.cpu().numpy()
@@ -44,7 +50,7 @@ for eps, kcap in cases:
     try:
         st = hm.cholesky()
     except H.HcovError as e:
-        print(f"eps={eps:g} kcap={kcap}: cholesky error {e}", flush=True)
+        print(f"eps={eps:g} kcap={kcap} dense_below={db}: cholesky error {e}", flush=True)
         continue
     r = hm.loglik(dev(Z))
     Lt = np.zeros((real.size, real.size))
@@ -65,7 +71,7 @@ for eps, kcap in cases:
                 first = (I, J, M[I, J]); break
         if first: break
     rec = np.abs(Lt @ Lt.T - Cint).max()
-    print(f"eps={eps:g} kcap={kcap}: L rel {abs(r['loglik']-ref[0])/abs(ref[0]):.2e} max_rank {r['max_rank']} "
+    print(f"eps={eps:g} kcap={kcap} dense_below={db}: L rel {abs(r['loglik']-ref[0])/abs(ref[0]):.2e} max_rank {r['max_rank']} "
           f"acc_loss {r['acc_loss']} | max|C~-C| {ea:.2e} | max|L~-L| {E.max():.2e} | max|L~L~^T - C| {rec:.2e} "
           f"| first bad leaf block {first}", flush=True)
     colerr = M.max(axis=0)
