@@ -53,9 +53,8 @@ CONFIGS = {
 
 
 # eps of the tight H-Cholesky factor whose samples Z = L~ xi are the data of
-# C3 / C4 / C5 (no rank cap for C3 / C4).  C3 uses 1e-9: at 1e-10 the clustered C3 field is not
-# SPD under the method (R25).  C5: 1e-8, "if memory forbids, 1e-7" (bench.py).
-EPS_GEN = {"C3": 1e-9, "C4": 1e-10, "C5": 1e-8}
+# C3 / C4 / C5 (no rank cap for C3 / C4).  C5: 1e-8, "if memory forbids, 1e-7" (bench.py).
+EPS_GEN = {"C3": 1e-10, "C4": 1e-10, "C5": 1e-8}
 
 def uniform_points(n: int, seed: int) -> np.ndarray:
     """n points U[0,1]^2, (n, 2) float64, external order."""

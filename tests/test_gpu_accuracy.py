@@ -51,9 +51,8 @@ def test_c3_sampled_columns():
 
 
 def test_c3_evaluation_and_chi2():
-    """C3 as BASELINE writes it: Z from a tight uncapped H-Cholesky factor (eps_gen = 1e-9: the
-    row-15 value 1e-10 is not SPD under the method on C3's clustered points, R25), one
-    evaluation at eps = 1e-6, k = 16.  At theta_gen, q = Z^T C~^{-1} Z ~ chi^2_n: |q - n| <= 5 sqrt(2n)
+    """C3 as BASELINE writes it: Z from a tight uncapped H-Cholesky factor (eps_gen = 1e-10, SURVEY
+    8(c) row 15), one evaluation at eps = 1e-6, k = 16.  At theta_gen, q = Z^T C~^{-1} Z ~ chi^2_n: |q - n| <= 5 sqrt(2n)
     (SURVEY 8(c) pin (vi)) for the tight factor itself."""
     cfg = synth.CONFIGS["C3"]
     s = synth.points(cfg)
