@@ -106,6 +106,24 @@ hcov_status hcov_build_tree(const double *s_dev, int64_t n, int32_t leaf_size, d
  * hcov_build_tree with s_host a host array.  Device arrays are uploaded on first use. */
 hcov_status hcov_build_tree_host(const double *s_host, int64_t n, int32_t leaf_size, double eta,
                                  int32_t dense_below, hcov_tree *out);
+/* Tree options (hcov_build_tree_ex).  factor_trunc = 1 selects the SPD-preserving variant of the
+ * H-Cholesky (NEXT (f4); reading R27): the assembled C~ and the accumulated Schur updates
+ * of each low-rank block are kept near-losslessly (eps * 1e-2, no rank cap, within the work capacity
+ * kcap), and the (eps, kmax) truncation of Remark 2 (applied per sub-block of L~
+ * as Table 4's caption states) is applied to the FACTOR block
+ * L_21 = A_21 L_11^{-T} after its solve.  A truncated SVD of L_21 is an orthogonal projection from
+ * the right, so the Schur complement A_22 - L~_21 L~_21^T is >= A_22 - L_21 L_21^T in the Loewner
+ * order: truncation can only raise the remaining pivots.  Use with kcap > kmax (e.g. kcap = 64,
+ * kmax = 20).  factor_trunc = 0 is the paper's order (truncate, then solve). */
+typedef struct {
+    int32_t leaf_size;     /* 32 */
+    double eta;            /* admissibility parameter (2.0; 0 = all dense) */
+    int32_t dense_below;   /* 32 */
+    int32_t factor_trunc;  /* 0 or 1 */
+} hcov_tree_opts;
+hcov_status hcov_build_tree_ex(const double *s_dev, int64_t n, const hcov_tree_opts *opts, hcov_stream stream,
+                               hcov_tree *out);
+hcov_status hcov_build_tree_host_ex(const double *s_host, int64_t n, const hcov_tree_opts *opts, hcov_tree *out);
 hcov_status hcov_tree_get_info(hcov_tree t, hcov_tree_info *info);
 /* Block-tree nodes (lower triangle incl. diagonal), 4 int32 per node: level, i, j, type
  * (0 = inadmissible/subdivided, 1 = low-rank leaf, 2 = dense 32x32 leaf).  With out4 == NULL

@@ -59,6 +59,11 @@ class TreeInfo(ctypes.Structure):
                 ("n_edges", ctypes.c_int64), ("n_xterm", ctypes.c_int64), ("max_mq", ctypes.c_int64)]
 
 
+class TreeOpts(ctypes.Structure):
+    _fields_ = [("leaf_size", ctypes.c_int32), ("eta", ctypes.c_double), ("dense_below", ctypes.c_int32),
+                ("factor_trunc", ctypes.c_int32)]
+
+
 class Prof(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("n_classes", ctypes.c_int32), ("n_task_types", ctypes.c_int32),
                 ("count", ctypes.c_int64 * 16), ("ms", ctypes.c_double * 16),
@@ -72,6 +77,8 @@ _P, _I32, _I64, _D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_d
 _SIGS = {
     "hcov_build_tree": (_I32, [_P, _I64, _I32, _D, _I32, _P, _P]),
     "hcov_build_tree_host": (_I32, [_P, _I64, _I32, _D, _I32, _P]),
+    "hcov_build_tree_ex": (_I32, [_P, _I64, _P, _P, _P]),
+    "hcov_build_tree_host_ex": (_I32, [_P, _I64, _P, _P]),
     "hcov_tree_get_info": (_I32, [_P, _P]),
     "hcov_tree_blocks": (_I32, [_P, _P, _I64, _P]),
     "hcov_tree_bbox": (_I32, [_P, _P, _I64]),
@@ -149,18 +156,22 @@ def _dev_f64(x, n=None, name="array"):
 class Tree:
     """Cluster tree + block tree + theta-independent schedule (hcov_tree)."""
 
-    def __init__(self, s, eta: float = 2.0, dense_below: int = 32, leaf_size: int = 32, stream=None):
+    def __init__(self, s, eta: float = 2.0, dense_below: int = 32, leaf_size: int = 32, stream=None,
+                 factor_trunc: bool = False):
+        """factor_trunc: the SPD-preserving H-Cholesky variant (hcov_tree_opts.factor_trunc, R27)."""
         L = lib()
         h = ctypes.c_void_p()
+        o = TreeOpts(leaf_size, eta, dense_below, 1 if factor_trunc else 0)
+        self.factor_trunc = bool(factor_trunc)
         if isinstance(s, np.ndarray):
             a = np.ascontiguousarray(s, dtype=np.float64)
             self.n = a.shape[0]
-            _check(L.hcov_build_tree_host(a.ctypes.data, self.n, leaf_size, eta, dense_below, ctypes.byref(h)),
-                   "hcov_build_tree_host")
+            _check(L.hcov_build_tree_host_ex(a.ctypes.data, self.n, ctypes.byref(o), ctypes.byref(h)),
+                   "hcov_build_tree_host_ex")
         else:
             self.n = s.shape[0]
-            _check(L.hcov_build_tree(_dev_f64(s, 2 * self.n, "s"), self.n, leaf_size, eta, dense_below,
-                                     _stream(stream), ctypes.byref(h)), "hcov_build_tree")
+            _check(L.hcov_build_tree_ex(_dev_f64(s, 2 * self.n, "s"), self.n, ctypes.byref(o), _stream(stream),
+                                        ctypes.byref(h)), "hcov_build_tree_ex")
         self._h = h
 
     def __del__(self):

@@ -75,7 +75,11 @@ struct Ctx {
     uint32_t *qctl;            // see QC_* in hcov.cu
     int32_t nq[2];
     int32_t ninst;             // instances (H-matrices of one tree) run by this engine launch
-    int32_t pad1;
+    int32_t kcore;             // leading dimension / stride of the PRR cores (kcap; kmax in the
+                               // SPD-preserving mode, where products see truncated factors only)
+    int32_t factor_trunc;      // 1: SPD-preserving mode (tree option; R27): C~ and the pending
+                               // updates kept near-losslessly, the (eps, kmax) truncation applied to the
+                               // factor block L_21 = A_21 L_11^{-T} after its solve (a TRUNC task)
     int32_t *gbar;             // per-task gang barrier counters
     int32_t *gslot;            // per-task: CTA index of the gang's member 0 (-1 until it joined)
     int64_t gshared_off;       // offset (doubles) of the shared gang workspace in a gang CTA's scratch
@@ -230,10 +234,10 @@ __device__ double tile_apply_term(const Ctx &c, const DTerm &t, int64_t R0, int6
     const double *T1 = sm.A;
     double fl = 2.0 * 32 * 32 * rb;
     if (t.core >= 0) {
-        const double *K = c.cores + (int64_t)t.core * c.kcap * c.kcap;
+        const double *K = c.cores + (int64_t)t.core * c.kcore * c.kcore;
         for (int e = threadIdx.x; e < ra * rb; e += NT) {
             int a = e % ra, b = e / ra;
-            sm.K[e] = __ldcg(K + a + (int64_t)c.kcap * b);
+            sm.K[e] = __ldcg(K + a + (int64_t)c.kcore * b);
         }
         __syncthreads();
         for (int e = threadIdx.x; e < 32 * rb; e += NT) {
@@ -337,6 +341,17 @@ __device__ void record_rank(const Ctx &c, int r, int rk, int cb, int of)
         if (cb) atomicAdd(c.flags + 0, 1);
         if (of) atomicAdd(c.flags + 1, 1);
         atomicMax(c.flags + 2, rk);
+    }
+    __syncthreads();
+}
+
+// Rank of a near-lossless (not yet final) representation: stored, not counted in the rank
+// statistics; a cut for lack of capacity is counted like an intermediate cut.
+__device__ void record_interm(const Ctx &c, int r, int rk, int of)
+{
+    if (threadIdx.x == 0) {
+        __stcg(c.rank + r, rk);
+        if (of) atomicAdd(c.flags + (c.kmax > 0 ? 4 : 3), 1);
     }
     __syncthreads();
 }
@@ -913,29 +928,37 @@ __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *sme
     const int64_t m = b.m;
     const int K = aca_kmax(m, c.kcap);
     const int KB = kbuf_of(c.kcap);
+    // SPD-preserving mode: C~ near-lossless (eps * interm_rel, no rank cap; the (eps, kmax) truncation
+    // comes after the block's solve, R27)
+    const double ea = c.factor_trunc ? interm_tol(c) : c.eps;
+    const int km = c.factor_trunc ? 0 : c.kmax;
     double *X2, *Y2;
     int cb = 0, of = 0, k, rk;
     if (!gg) {
         CompressWs w = make_ws(scr, m, KB, &X2, &Y2);
         uint8_t *used = (uint8_t *)w.tail;
         PH_BEGIN(tp);
-        k = aca_partial(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, K, 0.1 * c.eps, used, red, redv, redi);
+        k = aca_partial(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, K, 0.1 * ea, used, red, redv, redi);
         PH_END(8, tp);
         if (k == K && K < m && threadIdx.x == 0) atomicAdd(c.flags + cut_flag(c), 1);   // ACA not converged
-        rk = compress(w, m, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m, &cb, &of,
+        rk = compress(w, m, k, ea, final_tol(ea, k), true, km, c.kcap, r_U(c, r), r_V(c, r), m, &cb, &of,
                       red, redv, redi, smem, c.smem_dbl);
-        record_rank(c, r, rk, cb, of);
+        if (c.factor_trunc) record_interm(c, r, rk, of);
+        else record_rank(c, r, rk, cb, of);
     } else {
         gang_rows(*gg, m);
         CompressWs w = make_ws(scr, gg->mq, KB, &X2, &Y2, 4);
         w.tsr = scr + task_scratch_base(gg->mq, c.kcap, 4);
         GangWs gw = make_gws(gg->shared, KB, gg->G);
-        k = gang_aca(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, (uint8_t *)w.tail, K, 0.1 * c.eps, gw, *gg, red,
+        k = gang_aca(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, (uint8_t *)w.tail, K, 0.1 * ea, gw, *gg, red,
                      redv, redi);
         if (k == K && K < m && gg->g == 0 && threadIdx.x == 0) atomicAdd(c.flags + cut_flag(c), 1);
-        rk = gang_compress(w, gw, *gg, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, r_U(c, r), r_V(c, r), m,
+        rk = gang_compress(w, gw, *gg, k, ea, final_tol(ea, k), true, km, c.kcap, r_U(c, r), r_V(c, r), m,
                            &cb, &of, red, redv, redi, smem, c.smem_dbl);
-        if (gg->g == 0) record_rank(c, r, rk, cb, of);
+        if (gg->g == 0) {
+            if (c.factor_trunc) record_interm(c, r, rk, of);
+            else record_rank(c, r, rk, cb, of);
+        }
     }
     const double share = gg ? 1.0 / gg->G : 1.0;
     fl_asm += share * 2.0 * m * k;                       // kernel evaluations (rows + columns)
@@ -1097,12 +1120,12 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
                 const int ra = A.ncols;
                 const int64_t r_lo = max(R0, A.row0), r_hi = min(R0 + m, A.row0 + A.nrows);
                 const int64_t c_lo = max(C0, B.row0), c_hi = min(C0 + m, B.row0 + B.nrows);
-                const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcap * c.kcap : nullptr;
+                const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcore * c.kcore : nullptr;
                 // the core K (ra x w) staged in this warp's slice of shared memory: kb[a + ra b]
                 double *kb = sb + (int64_t)warp * kbw;
                 const bool kstaged = Kc && ra * w <= kbw;
                 if (kstaged) {
-                    for (int e = lane; e < ra * w; e += 32) kb[e] = __ldcg(Kc + (e % ra) + (int64_t)c.kcap * (e / ra));
+                    for (int e = lane; e < ra * w; e += 32) kb[e] = __ldcg(Kc + (e % ra) + (int64_t)c.kcore * (e / ra));
                     __syncwarp();
                 }
                 for (int64_t i = lane; i < m; i += 32) {
@@ -1130,7 +1153,7 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
                                         for (int bb = 0; bb < 8; ++bb)
                                             if (b0 + bb < w) {
                                                 const double kv = kstaged ? kb[a + ra * (b0 + bb)]
-                                                                          : __ldcg(Kc + a + (int64_t)c.kcap * (b0 + bb));
+                                                                          : __ldcg(Kc + a + (int64_t)c.kcore * (b0 + bb));
                                                 acc[bb] = fma(xa[u], kv, acc[bb]);
                                             }
                                     }
@@ -1207,10 +1230,14 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         PH_END(5, ta);
         fl += 2.0 * m * m * k;
         if (k == KA && KA < m && threadIdx.x == 0) atomicAdd(c.flags + cut_flag(c), 1);
-        int rk = compress(wd, m, k, c.eps, final_tol(c.eps, k), true, c.kmax, c.kcap, U, V, m, &cb, &of, red, redv,
-                          redi, smem, c.smem_dbl);
+        // tk.d == 2: the pre-solve state of the SPD-preserving mode (near-lossless, no cap, R27)
+        const bool pre = (tk.d == 2);
+        const double ed = pre ? interm_tol(c) : c.eps;
+        int rk = compress(wd, m, k, ed, final_tol(ed, k), true, pre ? 0 : c.kmax, c.kcap, U, V, m, &cb, &of, red,
+                          redv, redi, smem, c.smem_dbl);
         fl += compress_flops(m, k, rk);
-        record_rank(c, r, rk, cb, of);
+        if (pre) record_interm(c, r, rk, of);
+        else record_rank(c, r, rk, cb, of);
         return;
     }
     // factor mode (m > HCOV_DENSE_MAX); rows [q0, q0 + mq) belong to this CTA (the whole block
@@ -1277,10 +1304,10 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
             const int ra = A.ncols, rb = B.ncols;
             const int64_t r_lo = max(R0 + q0, A.row0), r_hi = min(R0 + q0 + mq, A.row0 + A.nrows);
             const int64_t c_lo = max(C0 + q0, B.row0), c_hi = min(C0 + q0 + mq, B.row0 + B.nrows);
-            const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcap * c.kcap : nullptr;
+            const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcore * c.kcore : nullptr;
             if (doX && r_hi > r_lo) {
                 if (Kc) {   // xc = -A K  (columns b < rb), staged GEMM
-                    cta_gemm_nt(xc + (r_lo - R0 - q0), mq, r_hi - r_lo, rb, ra, A.p + (r_lo - A.row0), A.ld, Kc, c.kcap,
+                    cta_gemm_nt(xc + (r_lo - R0 - q0), mq, r_hi - r_lo, rb, ra, A.p + (r_lo - A.row0), A.ld, Kc, c.kcore,
                                 1, -1.0, smem);
                     fl += 2.0 * (r_hi - r_lo) * ra * rb;
                 } else {
@@ -1606,13 +1633,13 @@ __device__ void task_prr(const Ctx &c, const DTask &tk, double &fl)
     const int ra = __ldcg(c.rank + tk.a), rb = __ldcg(c.rank + tk.b);
     const int64_t m = c.rblk[tk.a].m;
     const double *Va = r_V(c, tk.a), *Vb = r_V(c, tk.b);
-    double *K = c.cores + (int64_t)tk.c * c.kcap * c.kcap;
+    double *K = c.cores + (int64_t)tk.c * c.kcore * c.kcore;
     for (int pq = warp; pq < ra * rb; pq += NWARP) {
         int a = pq % ra, b = pq / ra;
         double s = 0.0;
         for (int64_t i = lane; i < m; i += 32) s += __ldcg(Va + i + m * a) * __ldcg(Vb + i + m * b);
         s = warp_sum(s);
-        if (lane == 0) __stcg(K + a + (int64_t)c.kcap * b, s);
+        if (lane == 0) __stcg(K + a + (int64_t)c.kcore * b, s);
     }
     fl += 2.0 * m * ra * rb;
 }

@@ -23,7 +23,7 @@ namespace {
 #define CK(x)                                                 \
     do {                                                      \
         cudaError_t e_ = (x);                                 \
-        if (e_ != cudaSuccess) return map_err(e_);            \
+        if (e_ != cudaSuccess) return map_err_at(e_, __LINE__); \
     } while (0)
 
 static bool verbose()
@@ -31,6 +31,18 @@ static bool verbose()
     static int v = -1;
     if (v < 0) { const char *e = std::getenv("HCOV_VERBOSE"); v = (e && *e && *e != '0') ? 1 : 0; }
     return v == 1;
+}
+
+hcov_status map_err(cudaError_t e);
+hcov_status map_err_at(cudaError_t e, int line)
+{
+    if (verbose()) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        std::fprintf(stderr, "hcov: hcov.cu:%d: CUDA error %d, device memory free %.2f of %.2f GB\n", line, (int)e,
+                     fr / 1e9, tot / 1e9);
+    }
+    return map_err(e);
 }
 
 hcov_status map_err(cudaError_t e)
@@ -751,7 +763,7 @@ struct hcov_hmat_s {
     hcov_theta theta{};
     hcov_trunc trunc{};
     int state = 0;   // 1 assembled, 2 factored, 3 solved
-    int kcap_alloc = -1;
+    int kcap_alloc = -1, kcore_alloc = -1;
     double *tiles = nullptr, *U = nullptr, *V = nullptr, *cores = nullptr, *W = nullptr, *P = nullptr;
     double *vbuf = nullptr, *tbuf = nullptr, *logdet_part = nullptr, *minpiv_part = nullptr, *quad_part = nullptr;
     int32_t *rank = nullptr, *fail = nullptr, *flags = nullptr;
@@ -893,30 +905,37 @@ int eff_kcap(const hcov_trunc *tr)
     if (tr->kmax > 0) return tr->kmax;
     return 64;
 }
+// Core capacity: the products of the SPD-preserving mode see factors truncated to kmax only.
+int eff_kcore(const Plan &P, const hcov_trunc *tr)
+{
+    const int kc = eff_kcap(tr);
+    return (P.opt.factor_trunc && tr->kmax > 0) ? std::min(kc, (int)tr->kmax) : kc;
+}
 
 
 // Device bytes of one H-matrix instance outside its W / product-slot pools (memory planning of
 // theta batches; must follow hmat_alloc).
-int64_t inst_fixed_bytes(const Plan &P, int64_t kc)
+int64_t inst_fixed_bytes(const Plan &P, int64_t kc, int64_t kco)
 {
     const int64_t ntk = (int64_t)P.tasks.size();
-    return 8 * (P.n_tiles() * HCOV_TILE + 2 * P.uv_elems * kc + (int64_t)P.n_cores * kc * kc + P.n_pad +
+    return 8 * (P.n_tiles() * HCOV_TILE + 2 * P.uv_elems * kc + (int64_t)P.n_cores * kco * kco + P.n_pad +
                 P.n_r() * kc + 3 * P.n_leaves + (int64_t)P.phw.size() + (int64_t)P.slots.size()) +
            4 * (P.n_r() + 3 * ntk) + (int64_t)KTAB_NI * KTAB_NC * 8 + (1 << 20);
 }
 
 // (Re)allocate the numeric buffers of h for the tree's plan and capacity kcap.
-hcov_status hmat_alloc(hcov_hmat h, int kcap)
+hcov_status hmat_alloc(hcov_hmat h, int kcap, int kcore)
 {
     hcov_tree t = h->t;
     Plan &P = t->P;
-    if (h->tiles && h->kcap_alloc == kcap) return HCOV_OK;
+    if (h->tiles && h->kcap_alloc == kcap && h->kcore_alloc == kcore) return HCOV_OK;
     h->release_all();
     const int64_t kc = kcap;
+    h->kcore_alloc = kcore;
     CK(cudaMalloc(&h->tiles, std::max<int64_t>(1, P.n_tiles()) * HCOV_TILE * sizeof(double)));
     CK(cudaMalloc(&h->U, std::max<int64_t>(1, P.uv_elems * kc) * sizeof(double)));
     CK(cudaMalloc(&h->V, std::max<int64_t>(1, P.uv_elems * kc) * sizeof(double)));
-    CK(cudaMalloc(&h->cores, std::max<int64_t>(1, (int64_t)P.n_cores * kc * kc) * sizeof(double)));
+    CK(cudaMalloc(&h->cores, std::max<int64_t>(1, (int64_t)P.n_cores * kcore * kcore) * sizeof(double)));
     CK(cudaMalloc(&h->woff, std::max<size_t>(1, P.phw.size()) * sizeof(int64_t)));
     CK(cudaMalloc(&h->poff, std::max<size_t>(1, P.slots.size()) * sizeof(int64_t)));
     CK(cudaMalloc(&h->mem, 4 * sizeof(unsigned long long)));
@@ -1008,8 +1027,11 @@ hcov_status pools_alloc(hcov_hmat h)
     if (h->W) return HCOV_OK;
     const Plan &P = h->t->P;
     const int64_t kc = h->kcap_alloc;
-    const int64_t wfull = P.w_elems * kc + (int64_t)P.phw.size() + 64;
-    const int64_t pfull = P.slot_a * kc * kc + P.slot_b * kc + (int64_t)P.slots.size() + 64;
+    // SPD-preserving mode: the solves inside the factorization see the pre-truncation blocks (ranks up
+    // to 2 kcap for blocks > HCOV_DENSE_MAX), so product slots may need up to 4x the capacity bound
+    const int64_t fm = P.opt.factor_trunc ? 4 : 1;
+    const int64_t wfull = fm * P.w_elems * kc + (int64_t)P.phw.size() + 64;
+    const int64_t pfull = fm * (P.slot_a * kc * kc + P.slot_b * kc) + (int64_t)P.slots.size() + 64;
     if (h->w_budget > 0) {
         h->wcap = std::min(wfull, h->w_budget);
         h->pcap = std::min(pfull, h->p_budget);
@@ -1046,7 +1068,7 @@ void fill_ctx(hcov_hmat h)
     c.woff = h->woff; c.poff = h->poff; c.mem = h->mem; c.wcap = h->wcap; c.pcap = h->pcap;
     c.vbuf = h->vbuf; c.tbuf = h->tbuf; c.logdet_part = h->logdet_part; c.minpiv_part = h->minpiv_part; c.quad_part = h->quad_part;
     c.fail_leaf = h->fail; c.flags = h->flags;
-    c.kcap = h->kcap_alloc; c.kmax = h->trunc.kmax; c.eps = h->trunc.eps;
+    c.kcap = h->kcap_alloc; c.kcore = h->kcore_alloc; c.kmax = h->trunc.kmax; c.eps = h->trunc.eps;
     {
         // R22: intermediate chunk recompressions at eps * interm_rel (default 1e-2; HCOV_INTERM_REL
         // overrides it for the accuracy study in tests/test_gpu_accuracy.py)
@@ -1058,6 +1080,7 @@ void fill_ctx(hcov_hmat h)
     if (c.mp.kind == 3) c.mp.tab = h->ktab;
     c.indeg = h->indeg; c.gbar = h->gbar; c.gslot = h->gslot;
     c.band_off = t->d_band_off;
+    c.factor_trunc = P.opt.factor_trunc ? 1 : 0;
     c.flop = nullptr;
     const char *wd = std::getenv("HCOV_WATCHDOG_S");
     double wds = wd ? std::atof(wd) : 300.0;
@@ -1162,7 +1185,7 @@ hcov_status assemble_setup(hcov_hmat h, const hcov_theta *theta, const hcov_trun
     if (s) return s;
     h->theta = *theta;
     h->trunc = *trunc;
-    if ((s = hmat_alloc(h, kcap))) return s;
+    if ((s = hmat_alloc(h, kcap, eff_kcore(t->P, trunc)))) return s;
     if (!h->ktab) CK(cudaMalloc(&h->ktab, KTAB_NI * KTAB_NC * sizeof(double)));
     {
         const MaternParams mp = hcov_matern_params(theta->sigma2, theta->ell, theta->nu, theta->nugget);
@@ -1293,18 +1316,20 @@ const char *hcov_status_string(hcov_status s)
     return "unknown";
 }
 
-hcov_status hcov_build_tree_host(const double *s_host, int64_t n, int32_t leaf_size, double eta, int32_t dense_below,
-                                 hcov_tree *out)
+hcov_status hcov_build_tree_host_ex(const double *s_host, int64_t n, const hcov_tree_opts *opts, hcov_tree *out)
 {
-    if (!out) return HCOV_ERR_INVALID_ARG;
+    if (!out || !opts) return HCOV_ERR_INVALID_ARG;
     *out = nullptr;
     if (n == 0) return HCOV_ERR_EMPTY_INPUT;
-    if (!s_host || n < 0 || leaf_size != HCOV_LEAF || !(eta >= 0) || dense_below < 0) return HCOV_ERR_INVALID_ARG;
+    if (!s_host || n < 0 || opts->leaf_size != HCOV_LEAF || !(opts->eta >= 0) || opts->dense_below < 0 ||
+        (opts->factor_trunc != 0 && opts->factor_trunc != 1))
+        return HCOV_ERR_INVALID_ARG;
     std::unique_ptr<hcov_tree_s> t(new (std::nothrow) hcov_tree_s());
     if (!t) return HCOV_ERR_OUT_OF_MEMORY;
     PlanOpts o;
-    o.eta = eta;
-    o.dense_below = dense_below;
+    o.eta = opts->eta;
+    o.dense_below = opts->dense_below;
+    o.factor_trunc = opts->factor_trunc != 0;
     int rc = plan_build(t->P, s_host, n, o);
     if (rc == 2) return HCOV_ERR_EMPTY_INPUT;
     if (rc) return HCOV_ERR_INVALID_ARG;
@@ -1312,23 +1337,37 @@ hcov_status hcov_build_tree_host(const double *s_host, int64_t n, int32_t leaf_s
     return HCOV_OK;
 }
 
-hcov_status hcov_build_tree(const double *s_dev, int64_t n, int32_t leaf_size, double eta, int32_t dense_below,
-                            hcov_stream stream, hcov_tree *out)
+hcov_status hcov_build_tree_host(const double *s_host, int64_t n, int32_t leaf_size, double eta, int32_t dense_below,
+                                 hcov_tree *out)
+{
+    const hcov_tree_opts o{leaf_size, eta, dense_below, 0};
+    return hcov_build_tree_host_ex(s_host, n, &o, out);
+}
+
+hcov_status hcov_build_tree_ex(const double *s_dev, int64_t n, const hcov_tree_opts *opts, hcov_stream stream,
+                               hcov_tree *out)
 {
     if (!out) return HCOV_ERR_INVALID_ARG;
     *out = nullptr;
     if (n == 0) return HCOV_ERR_EMPTY_INPUT;
-    if (!s_dev || n < 0) return HCOV_ERR_INVALID_ARG;
+    if (!s_dev || n < 0 || !opts) return HCOV_ERR_INVALID_ARG;
     std::vector<double> s(2 * n);
     CK(cudaMemcpyAsync(s.data(), s_dev, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     hcov_tree t = nullptr;
-    hcov_status st = hcov_build_tree_host(s.data(), n, leaf_size, eta, dense_below, &t);
+    hcov_status st = hcov_build_tree_host_ex(s.data(), n, opts, &t);
     if (st) return st;
     st = tree_upload(t);
     if (st) { delete t; return st; }
     *out = t;
     return HCOV_OK;
+}
+
+hcov_status hcov_build_tree(const double *s_dev, int64_t n, int32_t leaf_size, double eta, int32_t dense_below,
+                            hcov_stream stream, hcov_tree *out)
+{
+    const hcov_tree_opts o{leaf_size, eta, dense_below, 0};
+    return hcov_build_tree_ex(s_dev, n, &o, stream, out);
 }
 
 hcov_status hcov_tree_get_info(hcov_tree t, hcov_tree_info *info)
@@ -1516,7 +1555,7 @@ hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *t
     const Plan &P = t->P;
     const int64_t wb = (int64_t)(1.3 * (double)t->est_w) + ((int64_t)1 << 20);
     const int64_t pb = (int64_t)(1.3 * (double)t->est_p) + ((int64_t)1 << 20);
-    const int64_t fixed = inst_fixed_bytes(P, kcap), pools = 8 * (wb + pb);
+    const int64_t fixed = inst_fixed_bytes(P, kcap, eff_kcore(P, trunc)), pools = 8 * (wb + pb);
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
     const int64_t avail = (int64_t)fr - ((int64_t)2 << 30);
@@ -1530,7 +1569,7 @@ hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *t
         if (!h) break;
         h->t = t;
         t->extra.push_back(h);
-        if (hmat_alloc(h, kcap)) { free_extra(t); inst.resize(1); break; }   // (fixed memory only: B shrinks)
+        if (hmat_alloc(h, kcap, eff_kcore(P, trunc))) { free_extra(t); inst.resize(1); break; }   // (fixed memory only: B shrinks)
         inst.push_back(h);
     }
     B = (int)inst.size();
@@ -1943,7 +1982,7 @@ hcov_status hcov_hmat_mem_info(hcov_hmat h, int64_t *out)
     if (h->mem) CK(cudaMemcpy(mem, h->mem, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     out[0] = P.n_tiles() * HCOV_TILE * 8;
     out[1] = 2 * P.uv_elems * kc * 8;
-    out[2] = (int64_t)P.n_cores * kc * kc * 8;
+    out[2] = (int64_t)P.n_cores * std::max(0, h->kcore_alloc) * std::max(0, h->kcore_alloc) * 8;
     out[3] = h->wcap * 8;
     out[4] = h->pcap * 8;
     out[5] = (int64_t)mem[0] * 8;

@@ -200,7 +200,7 @@ struct Builder {
             for (int z = b; z < e; ++z) add_term_prods(dp, tl[z]);
             int32_t ty = app_type;
             if (last && fin_type >= 0) { ty = fin_type; dp.push_back(extra_dep); }
-            const int32_t dd = (app_type == TK_RAPP) ? (last ? 1 : 0) : d;
+            const int32_t dd = (app_type == TK_RAPP) ? (last ? (O.factor_trunc ? 2 : 1) : 0) : d;
             prev = task(ty, a, base + b, base + e, dd, qcls, dp);
             if (app_type == TK_RAPP && rapp_split(P.rblk[a].m)) P.tasks[prev].pad = 1;
         }
@@ -430,11 +430,26 @@ struct Builder {
             const int32_t s_id = (int32_t)P.solves.size();
             for (int32_t r : rents) P.rblk[r].solve = s_id;
             const int32_t done = build_solve(l, c, rents);
-            for (int32_t r : rents) rdone[r] = done;
+            int32_t pdone = done;
+            if (O.factor_trunc) {
+                // SPD-preserving mode: truncate every factor block L_21 = U (L_ss^{-1} V)^T of the
+                // column once its solve is done; the products use the truncated blocks
+                std::vector<int32_t> tt;
+                for (int32_t r : rents) {
+                    const int32_t base = (int32_t)P.xterm.size();
+                    const int32_t t = task(TK_RAPP, r, base, base, 1, rapp_gang_of(P.rblk[r].m), {done});
+                    if (rapp_split(P.rblk[r].m)) P.tasks[t].pad = 1;
+                    rdone[r] = t;
+                    tt.push_back(t);
+                }
+                pdone = task(TK_NOP, 0, 0, 0, 0, 0, tt);
+            } else {
+                for (int32_t r : rents) rdone[r] = done;
+            }
             for (int32_t e : ents) {
                 if (P.nodes[e].type != ND_H) continue;
                 h2phw[e] = (int32_t)P.phw.size();
-                h2done[e] = build_phw(e, rents, col_off, done);
+                h2done[e] = build_phw(e, rents, col_off, pdone);
             }
         }
         // Schur-complement terms L_{e1} L_{e2}^T (e1.i >= e2.i) onto the owner of (e1.i, e2.i)

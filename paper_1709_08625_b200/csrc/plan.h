@@ -14,6 +14,10 @@ struct PlanOpts {
     int rchunk = 3;         // pending terms appended per RAPP task of a large low-rank block
     int fill_tiles = 8;     // tiles per FILL task
     int64_t big_m = HCOV_DENSE_MAX;   // larger low-rank blocks: chunked recompression, capacity 2 kcap
+    bool factor_trunc = false;  // SPD-preserving mode (R27): per low-rank block, the last
+                                // update chunk keeps the block near-lossless (d = 2), the block's
+                                // forward solve runs on that, then a TRUNC task (a RAPP without terms,
+                                // d = 1) truncates the factor block L_21 to (eps, kmax)
 };
 
 struct Plan {

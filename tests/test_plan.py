@@ -143,3 +143,46 @@ def test_backsolve_dag_is_the_transposed_solve():
                 assert t[k, 1] == 3
             if d in seg_of and k in seg_of:
                 assert seg_of[k] > seg_of[d]
+
+
+@pytest.mark.parametrize("n,seed", [(3000, 21), (9000, 22)])
+def test_factor_trunc_schedule(n, seed):
+    """SPD-preserving mode (hcov_tree_opts.factor_trunc, R27): every low-rank block gets
+    exactly one TRUNC task (a RAPP without terms, d = 1) that runs after the block's last update
+    (d = 2 chunk or its ACA) and after the solve of its column; no other RAPP truncates (d = 1)."""
+    s = synth.uniform_points(n, seed)
+    T0 = H.Tree(s)
+    T1 = H.Tree(s, factor_trunc=True)
+    t0, t1 = T0.tasks(), T1.tasks()
+    RAPP, ACA, SEG = 5, 1, 6
+    nr = int(np.sum(t0[:, 0] == ACA))
+    assert nr > 0 and int(np.sum(t1[:, 0] == ACA)) == nr
+    tr = np.nonzero((t1[:, 0] == RAPP) & (t1[:, 5] == 1))[0]
+    assert tr.size == nr                                        # one TRUNC per low-rank block
+    assert np.all(t1[tr, 3] == t1[tr, 4])                       # ... without terms
+    assert sorted(t1[tr, 2].tolist()) == sorted(t1[t1[:, 0] == ACA, 2].tolist())
+    last0 = (t0[:, 0] == RAPP) & (t0[:, 5] == 1)
+    last1 = (t1[:, 0] == RAPP) & (t1[:, 5] == 2)
+    assert int(np.sum(last1)) == int(np.sum(last0))             # the last update chunk stays near-lossless
+    # predecessors of each TRUNC: reachable from a SEG task of its column's solve
+    off, sc = T1.succ()
+    pred = {}
+    for u in range(len(off) - 1):
+        for v in sc[off[u]:off[u + 1]]:
+            pred.setdefault(int(v), []).append(u)
+
+    def ancestors_have(t, ty, depth=4):
+        frontier = [t]
+        for _ in range(depth):
+            nxt = []
+            for x in frontier:
+                for p in pred.get(x, []):
+                    if t1[p, 0] == ty:
+                        return True
+                    nxt.append(p)
+            frontier = nxt
+        return False
+    for t in tr[:50]:
+        assert ancestors_have(int(t), SEG), t
+    # the rest of the schedule is unchanged in size: standard tasks + one TRUNC per block + one join per column
+    assert t1.shape[0] > t0.shape[0] + nr - 1
