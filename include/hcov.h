@@ -91,11 +91,20 @@ typedef struct {
     /* pool sizes (for memory planning): U/V and W elements per unit rank capacity, product slots
      * (slot_a * kcap^2 + slot_b * kcap doubles), cores (kcap^2 each), DAG edges, term-list entries */
     int64_t uv_elems, w_elems, slot_a, slot_b, n_cores, n_edges, n_xterm, max_mq;
+    /* 1 if A1 / A2 ran on the device (hcov_build_tree[_ex]: kernels K1 / K2 of tree.cu), 0 for the
+     * host planner (hcov_build_tree_host[_ex]); geo_ms: wall time of the device A1 + A2 stage (device
+     * path) or of the whole host plan including the task schedule (host path) */
+    int32_t tree_on_device;
+    double geo_ms;
 } hcov_tree_info;
 
 /* A1 + A2: cluster tree by median bisection on the longest bounding-box axis (leaves <= leaf_size,
  * uniform depth), eta-admissible block tree (min(diam) <= eta * dist, dist > 0; PAPER.md:475,
- * 723-743), and the theta-independent H-Cholesky task schedule.
+ * 723-743), and the theta-independent H-Cholesky task schedule.  A1 and A2 run on the device
+ * (level-synchronous kernels: segmented bounding boxes + stable radix sort per level; pair
+ * classification + scan per level), bitwise equal to the host planner's trees; the task schedule
+ * is planned on the host from their output.  Errors: HCOV_ERR_INVALID_ARG for non-finite
+ * coordinates or n >= 2^31 - 32, HCOV_ERR_EMPTY_INPUT for n == 0, HCOV_ERR_CUDA on a device error.
  *   s_dev: n x 2 row-major device array of locations (external order).
  *   leaf_size: 32 (the only supported value).  eta: admissibility parameter (2.0; 0 = all dense).
  *   dense_below: admissible blocks with cluster size <= dense_below are stored as dense tiles

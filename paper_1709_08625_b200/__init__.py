@@ -56,7 +56,8 @@ class TreeInfo(ctypes.Structure):
                 ("n_lowrank", ctypes.c_int64), ("n_tasks", ctypes.c_int64), ("n_waves", ctypes.c_int64),
                 ("eta", ctypes.c_double), ("uv_elems", ctypes.c_int64), ("w_elems", ctypes.c_int64),
                 ("slot_a", ctypes.c_int64), ("slot_b", ctypes.c_int64), ("n_cores", ctypes.c_int64),
-                ("n_edges", ctypes.c_int64), ("n_xterm", ctypes.c_int64), ("max_mq", ctypes.c_int64)]
+                ("n_edges", ctypes.c_int64), ("n_xterm", ctypes.c_int64), ("max_mq", ctypes.c_int64),
+                ("tree_on_device", ctypes.c_int32), ("geo_ms", ctypes.c_double)]
 
 
 class TreeOpts(ctypes.Structure):

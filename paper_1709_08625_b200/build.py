@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libhcov.so")
-SOURCES = ["hcov.cu", "plan.cpp"]
+SOURCES = ["hcov.cu", "plan.cpp", "tree.cu"]
 HEADERS = ["hcov_internal.h", "plan.h", "matern.cuh", "dev.cuh", "la.cuh", "engine.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -717,6 +718,8 @@ struct Engine {
 struct hcov_tree_s {
     Plan P;
     bool uploaded = false;
+    bool tree_on_device = false;             // A1 / A2 built by tree.cu's kernels
+    double geo_ms = 0.0;                     // wall time of A1 + A2
     DNode *d_nodes = nullptr;
     int32_t *d_tile_node = nullptr;
     DRBlk *d_rblk = nullptr;
@@ -1330,7 +1333,9 @@ hcov_status hcov_build_tree_host_ex(const double *s_host, int64_t n, const hcov_
     o.eta = opts->eta;
     o.dense_below = opts->dense_below;
     o.factor_trunc = opts->factor_trunc != 0;
+    const auto g0 = std::chrono::steady_clock::now();
     int rc = plan_build(t->P, s_host, n, o);
+    t->geo_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - g0).count();
     if (rc == 2) return HCOV_ERR_EMPTY_INPUT;
     if (rc) return HCOV_ERR_INVALID_ARG;
     *out = t.release();
@@ -1351,13 +1356,33 @@ hcov_status hcov_build_tree_ex(const double *s_dev, int64_t n, const hcov_tree_o
     *out = nullptr;
     if (n == 0) return HCOV_ERR_EMPTY_INPUT;
     if (!s_dev || n < 0 || !opts) return HCOV_ERR_INVALID_ARG;
-    std::vector<double> s(2 * n);
-    CK(cudaMemcpyAsync(s.data(), s_dev, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
-    CK(cudaStreamSynchronize((cudaStream_t)stream));
-    hcov_tree t = nullptr;
-    hcov_status st = hcov_build_tree_host_ex(s.data(), n, opts, &t);
-    if (st) return st;
-    st = tree_upload(t);
+    if (opts->leaf_size != HCOV_LEAF || !(opts->eta >= 0) || opts->dense_below < 0 ||
+        (opts->factor_trunc != 0 && opts->factor_trunc != 1))
+        return HCOV_ERR_INVALID_ARG;
+    // A1 / A2 on the device (tree.cu: K1 cluster tree, K2 block tree); the task DAG is planned on
+    // the host from their output
+    std::unique_ptr<hcov_tree_s> tp(new (std::nothrow) hcov_tree_s());
+    if (!tp) return HCOV_ERR_OUT_OF_MEMORY;
+    PlanOpts o;
+    o.eta = opts->eta;
+    o.dense_below = opts->dense_below;
+    o.factor_trunc = opts->factor_trunc != 0;
+    {
+        PlanGeo geo;
+        const auto g0 = std::chrono::steady_clock::now();
+        const int rg = tree_geo_device(s_dev, n, o, (cudaStream_t)stream, geo);
+        tp->geo_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - g0).count();
+        if (rg == 2) return HCOV_ERR_EMPTY_INPUT;
+        if (rg == 1) return HCOV_ERR_INVALID_ARG;
+        if (rg) return HCOV_ERR_CUDA;
+        const int rc = plan_build(tp->P, nullptr, n, o, &geo);
+        if (rc == 2) return HCOV_ERR_EMPTY_INPUT;
+        if (rc == 3) return HCOV_ERR_CUDA;    // device trees inconsistent with the planner's rules
+        if (rc) return HCOV_ERR_INVALID_ARG;
+    }
+    tp->tree_on_device = true;
+    hcov_tree t = tp.release();
+    hcov_status st = tree_upload(t);
     if (st) { delete t; return st; }
     *out = t;
     return HCOV_OK;
@@ -1380,6 +1405,8 @@ hcov_status hcov_tree_get_info(hcov_tree t, hcov_tree_info *info)
     info->uv_elems = P.uv_elems; info->w_elems = P.w_elems; info->slot_a = P.slot_a; info->slot_b = P.slot_b;
     info->n_cores = P.n_cores; info->n_edges = (int64_t)P.succ.size(); info->n_xterm = (int64_t)P.xterm.size();
     info->max_mq = P.max_mq;
+    info->tree_on_device = t->tree_on_device ? 1 : 0;
+    info->geo_ms = t->geo_ms;
     return HCOV_OK;
 }
 

@@ -48,6 +48,8 @@ struct Builder {
     Plan &P;
     const PlanOpts &O;
     int L;
+    std::unordered_map<uint64_t, int8_t> geo_type;   // device-built block tree (PlanGeo), if given
+    bool use_geo = false, geo_miss = false;
     std::unordered_map<uint64_t, int32_t> key2node;
     std::vector<std::vector<int32_t>> node_terms;   // term ids per node
     std::vector<std::vector<int32_t>> col;          // per cluster heap id: off-diagonal entries
@@ -93,7 +95,12 @@ struct Builder {
         for (int k = 0; k < 4; ++k) P.children.push_back(-1);
         key2node[node_key(l, i, j)] = id;
         int type;
-        if (i == j) {
+        if (use_geo) {
+            auto it = geo_type.find(node_key(l, i, j));
+            if (it == geo_type.end()) { geo_miss = true; type = ND_T; }
+            else type = it->second;
+            if (type == ND_T && l != L && i == j) geo_miss = true;
+        } else if (i == j) {
             type = (l == L) ? ND_T : ND_H;
         } else {
             bool adm = !forced && admissible(l, i, j);
@@ -483,11 +490,12 @@ struct Builder {
 
 }  // namespace
 
-int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
+int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt, const PlanGeo *geo)
 {
     if (n <= 0) return 2;
-    for (int64_t k = 0; k < 2 * n; ++k)
-        if (!std::isfinite(s[k])) return 1;
+    if (!geo)
+        for (int64_t k = 0; k < 2 * n; ++k)
+            if (!std::isfinite(s[k])) return 1;
     P.opt = opt;
     P.opt.dense_below = std::max(opt.dense_below, HCOV_LEAF);
     P.opt.chunk = std::max(1, opt.chunk);
@@ -498,8 +506,18 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
     P.n_clusters = ((int64_t)2 << L) - 1;
     P.bb.assign(4 * P.n_clusters, 0.0);
 
+    if (geo) {   // A1 done on the device (tree.cu K1)
+        if (geo->depth != L || (int64_t)geo->perm_i2e.size() != P.n_pad || (int64_t)geo->xs.size() != P.n_pad ||
+            (int64_t)geo->ys.size() != P.n_pad || (int64_t)geo->bb.size() != 4 * P.n_clusters)
+            return 3;
+        P.perm_i2e = geo->perm_i2e;
+        P.xs = geo->xs;
+        P.ys = geo->ys;
+        P.bb = geo->bb;
+    }
     // ---- A1 -------------------------------------------------------------------------------
-    std::vector<int64_t> perm(n);
+    std::vector<int64_t> perm(geo ? 0 : n);
+    if (!geo) {
     std::iota(perm.begin(), perm.end(), 0);
     std::vector<int64_t> rs{0}, re{n};
     for (int l = 0; l <= L; ++l) {
@@ -538,11 +556,25 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt)
             P.ys[pos] = s[2 * perm[k] + 1];
         }
     }
+    }   // !geo
 
     // ---- A2 -------------------------------------------------------------------------------
     Builder B(P, P.opt);
+    if (geo) {   // A2 done on the device (tree.cu K2): the recursion below only reads its node types
+        B.use_geo = true;
+        size_t cnt = 0;
+        for (const auto &v : geo->level_pairs) cnt += v.size();
+        B.geo_type.reserve(cnt);
+        for (int l = 0; l < (int)geo->level_pairs.size(); ++l) {
+            if (geo->level_types[l].size() != geo->level_pairs[l].size()) return 3;
+            for (size_t p = 0; p < geo->level_pairs[l].size(); ++p)
+                B.geo_type[node_key(l, geo->level_pairs[l][p].first, geo->level_pairs[l][p].second)] =
+                    geo->level_types[l][p];
+        }
+    }
     P.diag_tile.assign(P.n_leaves, -1);
     B.make(0, 0, 0, -1, false);
+    if (B.use_geo && (B.geo_miss || P.nodes.size() != B.geo_type.size())) return 3;
     const size_t nn = P.nodes.size();
     B.node_terms.assign(nn, {});
     B.col.assign(P.n_clusters, {});

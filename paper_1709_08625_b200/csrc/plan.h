@@ -3,6 +3,7 @@
 // See DESIGN.md "H-Cholesky formulation" and "Engine".
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "hcov_internal.h"
@@ -82,6 +83,24 @@ struct Plan {
     int64_t cluster_size(int level) const { return (int64_t)HCOV_LEAF << (depth - level); }
 };
 
-// Build everything from host coordinates s (n x 2 row-major, external order).
-// Returns 0 on success, 1 invalid input, 2 empty input.
-int plan_build(Plan &P, const double *s_host, int64_t n, const PlanOpts &opt);
+// Cluster tree and block tree built on the device (tree.cu, kernels K1 / K2): the internal order,
+// the cluster bounding boxes, and every block-tree node per level with its type (NodeType).
+struct PlanGeo {
+    int depth = 0;
+    std::vector<int64_t> perm_i2e;   // n_pad
+    std::vector<double> xs, ys;      // n_pad
+    std::vector<double> bb;          // 4 per cluster heap id
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> level_pairs;   // (i, j) per level
+    std::vector<std::vector<int8_t>> level_types;                        // NodeType per pair
+};
+
+// Build everything from host coordinates s (n x 2 row-major, external order), or, when geo is
+// given, from the device-built trees (s_host is then unused and may be null).
+// Returns 0 on success, 1 invalid input, 2 empty input, 3 inconsistent geo.
+int plan_build(Plan &P, const double *s_host, int64_t n, const PlanOpts &opt, const PlanGeo *geo = nullptr);
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+// K1 + K2 on the device (tree.cu).  0 ok, 1 invalid input, 2 empty input, -1 CUDA error.
+int tree_geo_device(const double *s_dev, int64_t n, const PlanOpts &opt, cudaStream_t st, PlanGeo &g);
+#endif

@@ -128,23 +128,58 @@ def evaluate_all(C: np.ndarray, evaluate: Callable[[Sequence[Sequence[float]]], 
     return f
 
 
+def _save_state(path: str, S: Simplex, it_done: int) -> None:
+    # exact round trip: float.hex of every vertex coordinate and value
+    st = {"iters_done": it_done, "X": [[float(v).hex() for v in row] for row in S.X],
+          "F": [float(v).hex() for v in S.F], "history": S.history}
+    tmp = path + ".tmp"
+    with open(tmp, "w") as fh:
+        json.dump(st, fh)
+    import os
+    os.replace(tmp, path)
+
+
+def _load_state(path: str):
+    with open(path) as fh:
+        st = json.load(fh)
+    X = np.array([[float.fromhex(v) for v in row] for row in st["X"]])
+    F = np.array([float.fromhex(v) for v in st["F"]])
+    return Simplex(X, F, list(st["history"])), int(st["iters_done"])
+
+
 def run_mle(evaluate, x0: Sequence[float], iters: int = 20, rank: int = 0, world: int = 1, group=None,
-            device=None, trace: Optional[str] = None) -> Simplex:
-    """theta-batched Nelder-Mead + grid MLE from x0 = (nu, ell, sigma2); steps 20% of x0 (R17)."""
+            device=None, trace: Optional[str] = None, state: Optional[str] = None,
+            max_new_iters: Optional[int] = None) -> Simplex:
+    """theta-batched Nelder-Mead + grid MLE from x0 = (nu, ell, sigma2); steps 20% of x0 (R17).
+
+    state: checkpoint file (rank 0 writes it after every iteration; every rank reads it on entry),
+    so a long MLE can run over several processes; a resumed run is bitwise the same as one run.
+    max_new_iters: stop after this many iterations in this call (the checkpoint holds the rest)."""
+    import os
     x0 = np.asarray(x0, dtype=np.float64)
-    X = np.vstack([x0] + [x0 + np.eye(3)[k] * 0.2 * x0[k] for k in range(3)])
-    F = evaluate_all(X, evaluate, rank, world, group, device)
-    S = Simplex(X, F)
-    for it in range(iters):
+    if state and os.path.exists(state):
+        S, it0 = _load_state(state)
+    else:
+        X = np.vstack([x0] + [x0 + np.eye(3)[k] * 0.2 * x0[k] for k in range(3)])
+        F = evaluate_all(X, evaluate, rank, world, group, device)
+        S, it0 = Simplex(X, F), 0
+        if state and rank == 0:
+            _save_state(state, S, 0)
+    stop = iters if max_new_iters is None else min(iters, it0 + max_new_iters)
+    for it in range(it0, stop):
         C = candidates(S)
         f = evaluate_all(C, evaluate, rank, world, group, device)
         resolve(S, C, f)
         rec = {"iter": it, "best": S.X[0].tolist(), "negloglik": float(S.F[0]),
-               "size": float(np.max(S.X.max(0) - S.X.min(0)))}
+               "size": float(np.max(S.X.max(0) - S.X.min(0))),
+               "rejected": int(np.sum(~np.isfinite(f)))}
         S.history.append(rec)
         if trace and rank == 0:
             with open(trace, "a") as fh:
                 fh.write(json.dumps(rec) + "\n")
+        if state and rank == 0:
+            _save_state(state, S, it + 1)
+    S.iters_done = stop
     return S
 
 

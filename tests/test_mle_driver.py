@@ -78,6 +78,20 @@ def test_mle_converges_on_bowl():
     np.testing.assert_allclose(S.X[0], [0.5, 0.1, 1.0], rtol=0.02, atol=1e-3)
 
 
+def test_checkpoint_resume_bitwise(tmp_path):
+    """A run split over three calls through the state file equals one uninterrupted run."""
+    f = lambda xs: [-quad(x) for x in xs]  # noqa: E731
+    ref = mle.run_mle(f, (0.75, 0.15, 1.5), iters=9)
+    st = str(tmp_path / "state.json")
+    for _ in range(3):
+        S = mle.run_mle(f, (0.75, 0.15, 1.5), iters=9, state=st, max_new_iters=3)
+    assert S.iters_done == 9
+    assert np.array_equal(S.X, ref.X) and np.array_equal(S.F, ref.F)
+    assert [h["best"] for h in S.history] == [h["best"] for h in ref.history]
+    again = mle.run_mle(f, (0.75, 0.15, 1.5), iters=9, state=st)     # already done: no new iterations
+    assert np.array_equal(again.X, ref.X) and len(again.history) == 9
+
+
 def _oracle_evaluator(n=300):
     import oracle
     import synth
