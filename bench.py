@@ -52,6 +52,9 @@ def _args():
     p.add_argument("--kmax", type=int, default=-1, help="override the rank cap (-1 = the workload's)")
     p.add_argument("--acc-cols", type=int, default=64, help="sampled columns for ||C - C~||_F / ||C||_F")
     p.add_argument("--out", default="", help="also write the JSON line to this file")
+    p.add_argument("--factor-trunc", action="store_true",
+                   help="SPD-preserving H-Cholesky order (hcov_tree_opts.factor_trunc, DESIGN.md R27)")
+    p.add_argument("--kcap", type=int, default=0, help="rank capacity of the low-rank pools (0 = kmax)")
     p.add_argument("--cands-per-rank", type=int, default=1,
                    help="theta candidates per rank and step (> 1: hcov_mle_batch runs them in shared engine "
                         "launches); the batch is the config's theta with ell log-spaced in ell*[0.8, 1.25]")
@@ -218,7 +221,10 @@ def run_hcov(args, cfg, rank: int, world: int):
         wl = f"{wl}[n={n}]"
     stream = torch.cuda.current_stream()
     s_dev = torch.from_numpy(s).to(dev)
-    tree = H.Tree(s_dev)                       # A1-A2: theta-independent, untimed
+    tree = H.Tree(s_dev, factor_trunc=args.factor_trunc)   # A1-A2 (device kernels): theta-independent, untimed
+    kcap = args.kcap
+    if args.factor_trunc:
+        wl = f"{wl}[SPD-preserving order, kcap={kcap}]"
     info = tree.info()
     # data: Z = L~_gen xi from a TIGHTER H-Cholesky factor than the one
     # evaluated (eps_gen = 1e-8, same rank cap), so v = L~^{-1} Z is not xi by construction
@@ -232,7 +238,7 @@ def run_hcov(args, cfg, rank: int, world: int):
              (eps, max(1, kmax - 4) if kmax else 0)]
     for eg, kg in tries:
         try:
-            hgen = H.HMatrix(tree, th0, eg, kg)
+            hgen = H.HMatrix(tree, th0, eg, kg, kcap)
             try:
                 hgen.cholesky()
                 Z = hgen.sample(xi)
@@ -260,7 +266,7 @@ def run_hcov(args, cfg, rank: int, world: int):
     # both sides on the device: C~ e_j from the assembled H-matrix, C e_j by direct Eq. (3) evaluation
     acc = None
     if args.acc_cols > 0:
-        hacc = H.HMatrix(tree, my_theta, eps, kmax)
+        hacc = H.HMatrix(tree, my_theta, eps, kmax, kcap)
         cols = np.random.default_rng(7000 + rank).choice(n, args.acc_cols, replace=False)
         ct = hacc.columns(cols)
         ce = H.cov_columns(tree, my_theta, cols)
@@ -273,9 +279,9 @@ def run_hcov(args, cfg, rank: int, world: int):
 
     def step():
         if cpr == 1:
-            r = H.eval_loglik(tree, my_theta, Z, eps, kmax)
+            r = H.eval_loglik(tree, my_theta, Z, eps, kmax, kcap)
             return r, [r["loglik"]]
-        ll, st = H.mle_batch(tree, Z, my_thetas, eps, kmax)
+        ll, st = H.mle_batch(tree, Z, my_thetas, eps, kmax, kcap)
         if any(int(x) != 0 for x in st):
             raise RuntimeError(f"candidate rejected: {list(st)}")
         return None, list(ll)
@@ -283,7 +289,7 @@ def run_hcov(args, cfg, rank: int, world: int):
     for _ in range(max(3, args.warmup)):
         r, lls = step()
     if cpr > 1:   # the first candidate once more on its own: result fields and the work model below
-        r = H.eval_loglik(tree, my_theta, Z, eps, kmax)
+        r = H.eval_loglik(tree, my_theta, Z, eps, kmax, kcap)
     if r["status"] != 0:
         raise RuntimeError(f"evaluation failed: {r}")
     # ---- timed region -----------------------------------------------------------------------
@@ -315,7 +321,7 @@ def run_hcov(args, cfg, rank: int, world: int):
     ms_step = ms / args.steps
     value = m_total * args.steps / (ms * 1e-3)
     if cpr > 1:
-        H.eval_loglik(tree, my_theta, Z, eps, kmax)   # (outside the clock) the handle of the work model
+        H.eval_loglik(tree, my_theta, Z, eps, kmax, kcap)   # (outside the clock) the handle of the work model
     last = H.last_eval(tree)
     model = last.model_flops()
     st_l = last.storage()
@@ -331,7 +337,7 @@ def run_hcov(args, cfg, rank: int, world: int):
         e0.record(stream)
         for _ in range(k_e):
             Zd.copy_(Zh, non_blocking=True)
-            H.eval_loglik(tree, my_theta, Zd, eps, kmax)    # returns host scalars (D2H inside)
+            H.eval_loglik(tree, my_theta, Zd, eps, kmax, kcap)    # returns host scalars (D2H inside)
         e1.record(stream)
         torch.cuda.synchronize()
         ms_e2e = e0.elapsed_time(e1)
@@ -344,7 +350,7 @@ def run_hcov(args, cfg, rank: int, world: int):
         e0.record(stream)
         for _ in range(k_e):
             Zd.copy_(Zh, non_blocking=True)
-            H.mle_batch(tree, Zd, my_thetas, eps, kmax)
+            H.mle_batch(tree, Zd, my_thetas, eps, kmax, kcap)
         e1.record(stream)
         torch.cuda.synchronize()
         ms_e2e = e0.elapsed_time(e1)
@@ -383,7 +389,8 @@ def run_hcov(args, cfg, rank: int, world: int):
            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": wl, "n": n, "nu": my_theta[2], "ell": my_theta[1], "sigma2": my_theta[0],
-                      "nugget": my_theta[3], "eps": eps, "kmax": kmax, "Z_from_factor": eps_gen,
+                      "nugget": my_theta[3], "eps": eps, "kmax": kmax, "kcap": kcap or kmax,
+                      "factor_trunc": bool(args.factor_trunc), "Z_from_factor": eps_gen,
                       "theta_note": note, "config_as_written": {"name": cfg.name, "nu": cfg.nu, "ell": cfg.ell,
                                                                 "eps": cfg.eps[0], "kmax": cfg.kmax},
                       "leaf": 32, "eta": 2.0, "parallelism": f"theta-batch dp{world}",

@@ -96,6 +96,7 @@ typedef struct {
      * path) or of the whole host plan including the task schedule (host path) */
     int32_t tree_on_device;
     double geo_ms;
+    int32_t dim;           /* 2 or 3 (hcov_tree_opts.dim) */
 } hcov_tree_info;
 
 /* A1 + A2: cluster tree by median bisection on the longest bounding-box axis (leaves <= leaf_size,
@@ -129,6 +130,10 @@ typedef struct {
     double eta;            /* admissibility parameter (2.0; 0 = all dense) */
     int32_t dense_below;   /* 32 */
     int32_t factor_trunc;  /* 0 or 1 */
+    int32_t dim;           /* 2 (also 0), or 3: the 3-D variant ("replace dim = 2 by
+                            * dim = 3"): s is n x 3, boxes, diameters, distances and the longest-axis
+                            * split run over 3 axes (ties -> x, then y), and the Matern argument is the
+                            * 3-D distance; everything else is unchanged */
 } hcov_tree_opts;
 hcov_status hcov_build_tree_ex(const double *s_dev, int64_t n, const hcov_tree_opts *opts, hcov_stream stream,
                                hcov_tree *out);
@@ -148,7 +153,8 @@ hcov_status hcov_tree_tasks(hcov_tree t, int32_t *out6, int64_t cap, int64_t *co
  * HCOV_TIMELINE=<file> makes every engine launch write (start_ns, end_ns, cta) as 3 uint64 per
  * task (0 for tasks outside the launched mode) to <file>. */
 hcov_status hcov_tree_succ(hcov_tree t, int32_t *off, int32_t *succ, int64_t cap, int64_t *count);
-/* Cluster bounding boxes, 4 doubles per cluster heap id (2^l - 1 + c): lo_x, lo_y, hi_x, hi_y. */
+/* Cluster bounding boxes, 2 dim doubles per cluster heap id (2^l - 1 + c): lo_x, lo_y, hi_x, hi_y
+ * (dim 2) or lo_x, lo_y, lo_z, hi_x, hi_y, hi_z (dim 3). */
 hcov_status hcov_tree_bbox(hcov_tree t, double *bb, int64_t cap);
 /* perm_i2e: n_pad int64 (host); entry k = external index of internal position k, -1 for phantom rows. */
 hcov_status hcov_tree_perm(hcov_tree t, int64_t *perm_i2e_host);

@@ -85,9 +85,9 @@ def _load():
         lib.oracle_matern_integral.restype = d
         lib.oracle_matern_integral.argtypes = [d, d, d, d]
         lib.oracle_cov_dense.restype = None
-        lib.oracle_cov_dense.argtypes = [i64, p, d, d, d, d, p]
+        lib.oracle_cov_dense.argtypes = [i64, ctypes.c_int, p, d, d, d, d, p]
         lib.oracle_cov_entries.restype = None
-        lib.oracle_cov_entries.argtypes = [i64, p, d, d, d, d, p, i64, p, i64, p]
+        lib.oracle_cov_entries.argtypes = [i64, ctypes.c_int, p, d, d, d, d, p, i64, p, i64, p]
         _lib = lib
     return _lib
 
@@ -104,22 +104,30 @@ def matern(h: float, sigma2: float, ell: float, nu: float, integral: bool = Fals
     return f(float(h), float(sigma2), float(ell), float(nu))
 
 
-def cov_dense(s: np.ndarray, sigma2: float, ell: float, nu: float, nugget: float) -> np.ndarray:
-    """Dense n x n covariance in external order (Eq. (1) definition + nugget)."""
+def _coords(s) -> np.ndarray:
     s = np.ascontiguousarray(s, dtype=np.float64)
+    if s.ndim != 2 or s.shape[1] not in (2, 3):
+        raise ValueError("locations must be n x 2 or n x 3")
+    return s
+
+
+def cov_dense(s: np.ndarray, sigma2: float, ell: float, nu: float, nugget: float) -> np.ndarray:
+    """Dense n x n covariance in external order (Eq. (1) definition + nugget); s: n x 2, or n x 3
+    for the 3-D variant."""
+    s = _coords(s)
     n = s.shape[0]
     C = np.empty((n, n), dtype=np.float64)
-    _load().oracle_cov_dense(n, s.ctypes.data, sigma2, ell, nu, nugget, C.ctypes.data)
+    _load().oracle_cov_dense(n, s.shape[1], s.ctypes.data, sigma2, ell, nu, nugget, C.ctypes.data)
     return C
 
 
 def cov_entries(s, sigma2, ell, nu, nugget, rows, cols) -> np.ndarray:
     """C[rows][:, cols] (external indices) without forming C."""
-    s = np.ascontiguousarray(s, dtype=np.float64)
+    s = _coords(s)
     rows = np.ascontiguousarray(rows, dtype=np.int64)
     cols = np.ascontiguousarray(cols, dtype=np.int64)
     out = np.empty((rows.size, cols.size), dtype=np.float64)
-    _load().oracle_cov_entries(s.shape[0], s.ctypes.data, sigma2, ell, nu, nugget,
+    _load().oracle_cov_entries(s.shape[0], s.shape[1], s.ctypes.data, sigma2, ell, nu, nugget,
                                rows.ctypes.data, rows.size, cols.ctypes.data, cols.size,
                                out.ctypes.data)
     return out

@@ -57,12 +57,13 @@ def cluster_tree(s: np.ndarray) -> ClusterTree:
                 P = s[idx]
                 lo, hi = P.min(axis=0), P.max(axis=0)
             else:
-                lo = hi = np.full(2, np.nan)
+                lo = hi = np.full(s.shape[1], np.nan)
             boxes[(l, c)] = (lo, hi)
             if l == L:
                 continue
             ext = hi - lo
-            axis = 0 if (idx.size == 0 or ext[0] >= ext[1]) else 1
+            # longest extent, ties -> the lowest axis (x, then y); 2-D or 3-D
+            axis = 0 if idx.size == 0 else int(np.argmax(ext))
             order = np.argsort(s[idx, axis], kind="stable")   # ties keep the current order
             idx = idx[order]
             m1 = (idx.size + 1) // 2

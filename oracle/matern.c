@@ -79,17 +79,27 @@ double oracle_matern_integral(double h, double sigma2, double ell, double nu)
     return sigma2 * pre * oracle_besselk_scaled(nu, x);
 }
 
+/* Euclidean distance |s_i - s_j| of dim-dimensional points (dim = 2, or 3 for the 3-D variant,
+ * PAPER.md:684-686), s: n x dim row-major. */
+static double dist_ij(const double *s, int dim, int64_t i, int64_t j)
+{
+    double h2 = 0.0;
+    for (int k = 0; k < dim; ++k) {
+        double d = s[dim * i + k] - s[dim * j + k];
+        h2 += d * d;
+    }
+    return sqrt(h2);
+}
+
 /* Dense covariance, EXTERNAL order, full symmetric n x n row-major:
- *   C_ij = C(|s_i - s_j|; theta) + nugget * [i == j].     s: n x 2 row-major. */
-void oracle_cov_dense(int64_t n, const double *s, double sigma2, double ell, double nu,
+ *   C_ij = C(|s_i - s_j|; theta) + nugget * [i == j].     s: n x dim row-major. */
+void oracle_cov_dense(int64_t n, int dim, const double *s, double sigma2, double ell, double nu,
                       double nugget, double *C)
 {
     #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t i = 0; i < n; ++i) {
         for (int64_t j = 0; j <= i; ++j) {
-            double dx = s[2 * i] - s[2 * j], dy = s[2 * i + 1] - s[2 * j + 1];
-            double h = sqrt(dx * dx + dy * dy);
-            double c = oracle_matern(h, sigma2, ell, nu);
+            double c = oracle_matern(dist_ij(s, dim, i, j), sigma2, ell, nu);
             if (i == j) c += nugget;
             C[i * n + j] = c;
             C[j * n + i] = c;
@@ -99,7 +109,7 @@ void oracle_cov_dense(int64_t n, const double *s, double sigma2, double ell, dou
 
 /* Selected entries C_{rows[a], cols[b]} (external indices), out: nr x nc row-major.
  * Used for sampled-column checks at oracle-infeasible n. */
-void oracle_cov_entries(int64_t n, const double *s, double sigma2, double ell, double nu,
+void oracle_cov_entries(int64_t n, int dim, const double *s, double sigma2, double ell, double nu,
                         double nugget, const int64_t *rows, int64_t nr,
                         const int64_t *cols, int64_t nc, double *out)
 {
@@ -108,8 +118,7 @@ void oracle_cov_entries(int64_t n, const double *s, double sigma2, double ell, d
     for (int64_t a = 0; a < nr; ++a)
         for (int64_t b = 0; b < nc; ++b) {
             int64_t i = rows[a], j = cols[b];
-            double dx = s[2 * i] - s[2 * j], dy = s[2 * i + 1] - s[2 * j + 1];
-            double c = oracle_matern(sqrt(dx * dx + dy * dy), sigma2, ell, nu);
+            double c = oracle_matern(dist_ij(s, dim, i, j), sigma2, ell, nu);
             if (i == j) c += nugget;
             out[a * nc + b] = c;
         }

@@ -17,7 +17,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhcov.so")
+LIB_PATH = os.environ.get("HCOV_LIB") or os.path.join(_HERE, "libhcov.so")   # HCOV_LIB: an in-tree build variant (experiments)
 
 HCOV_OK = 0
 STATUS = {0: "ok", 1: "invalid argument", 2: "empty input", 3: "not SPD", 4: "out of memory",
@@ -57,12 +57,12 @@ class TreeInfo(ctypes.Structure):
                 ("eta", ctypes.c_double), ("uv_elems", ctypes.c_int64), ("w_elems", ctypes.c_int64),
                 ("slot_a", ctypes.c_int64), ("slot_b", ctypes.c_int64), ("n_cores", ctypes.c_int64),
                 ("n_edges", ctypes.c_int64), ("n_xterm", ctypes.c_int64), ("max_mq", ctypes.c_int64),
-                ("tree_on_device", ctypes.c_int32), ("geo_ms", ctypes.c_double)]
+                ("tree_on_device", ctypes.c_int32), ("geo_ms", ctypes.c_double), ("dim", ctypes.c_int32)]
 
 
 class TreeOpts(ctypes.Structure):
     _fields_ = [("leaf_size", ctypes.c_int32), ("eta", ctypes.c_double), ("dense_below", ctypes.c_int32),
-                ("factor_trunc", ctypes.c_int32)]
+                ("factor_trunc", ctypes.c_int32), ("dim", ctypes.c_int32)]
 
 
 class Prof(ctypes.Structure):
@@ -162,7 +162,10 @@ class Tree:
         """factor_trunc: the SPD-preserving H-Cholesky variant (hcov_tree_opts.factor_trunc, R27)."""
         L = lib()
         h = ctypes.c_void_p()
-        o = TreeOpts(leaf_size, eta, dense_below, 1 if factor_trunc else 0)
+        if len(s.shape) != 2 or s.shape[1] not in (2, 3):
+            raise ValueError("locations must be n x 2, or n x 3 (the 3-D variant)")
+        self.dim = int(s.shape[1])
+        o = TreeOpts(leaf_size, eta, dense_below, 1 if factor_trunc else 0, self.dim)
         self.factor_trunc = bool(factor_trunc)
         if isinstance(s, np.ndarray):
             a = np.ascontiguousarray(s, dtype=np.float64)
@@ -171,7 +174,7 @@ class Tree:
                    "hcov_build_tree_host_ex")
         else:
             self.n = s.shape[0]
-            _check(L.hcov_build_tree_ex(_dev_f64(s, 2 * self.n, "s"), self.n, ctypes.byref(o), _stream(stream),
+            _check(L.hcov_build_tree_ex(_dev_f64(s, self.dim * self.n, "s"), self.n, ctypes.byref(o), _stream(stream),
                                         ctypes.byref(h)), "hcov_build_tree_ex")
         self._h = h
 
@@ -223,7 +226,7 @@ class Tree:
     def bbox(self) -> np.ndarray:
         d = self.info()["depth"]
         nc = (2 << d) - 1
-        out = np.empty((nc, 4), dtype=np.float64)
+        out = np.empty((nc, 2 * self.dim), dtype=np.float64)
         _check(lib().hcov_tree_bbox(self._h, out.ctypes.data, out.size), "hcov_tree_bbox")
         return out
 

@@ -43,6 +43,7 @@ struct Ctx {
     const int32_t *succ_off, *succ;
     const int32_t *diag_tile;
     const double *xs, *ys;
+    const double *zs;          // 3-D variant (tree option dim = 3); nullptr for 2-D locations
     const int64_t *perm_i2e;
     int32_t depth, n_r, root_solve, ntasks;
     int64_t n_pad, n_leaves, n_real, n_tiles;
@@ -265,7 +266,7 @@ __device__ void task_fill(const Ctx &c, const DTask &tk, double &fl)
         for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
             int i = e & 31, j = e >> 5;
             int64_t a = r0 + i, b = c0 + j;
-            __stcg(T + e, hcov_cov_entry(c.mp, c.xs[a], c.ys[a], c.xs[b], c.ys[b], a == b));
+            __stcg(T + e, pts_cov(c.mp, Pts{c.xs, c.ys, c.zs}, a, b));
         }
     }
     fl += (double)tk.b * HCOV_TILE;   // kernel evaluations
@@ -799,7 +800,7 @@ __device__ __noinline__ int gang_compress_split(const CompressWs &w, const GangW
 // Member g evaluates the columns j and rows i in [q0, q0 + mq) of each cross; the pivot row of U
 // and the pivot column of V are published through the shared workspace.  Ul, Vl: local panels
 // (mq x Kmax, ld mq).  Returns k.
-__device__ int gang_aca(const MaternParams &mp, const double *xs, const double *ys, int64_t R0, int64_t C0, int64_t m,
+__device__ int gang_aca(const MaternParams &mp, const Pts P, int64_t R0, int64_t C0, int64_t m,
                         double *Ul, double *Vl, uint8_t *used, int Kmax, double eps_aca, const GangWs &gw, Gang &gg,
                         double *red, double *redv, int64_t *redi)
 {
@@ -813,12 +814,14 @@ __device__ int gang_aca(const MaternParams &mp, const double *xs, const double *
     gang_sync(gg);
     while (k < Kmax && guard++ < m + Kmax) {
         // row residual of row istar (U[istar, :k] published in urow)
-        const double xi = xs[R0 + istar], yi = ys[R0 + istar];
+        const bool d3 = P.z != nullptr;
+        const double xi = P.x[R0 + istar], yi = P.y[R0 + istar], zi = d3 ? P.z[R0 + istar] : 0.0;
         double *vk = Vl + mq * k;
         double bv = 0.0;
         int64_t bi = 0;
         for (int64_t j = threadIdx.x; j < mq; j += NT) {
-            double a = hcov_cov_entry(mp, xi, yi, xs[C0 + q0 + j], ys[C0 + q0 + j], (R0 + istar) == (C0 + q0 + j));
+            double a = hcov_cov_entry_d(mp, xi, yi, zi, P.x[C0 + q0 + j], P.y[C0 + q0 + j], d3 ? P.z[C0 + q0 + j] : 0.0,
+                                        (R0 + istar) == (C0 + q0 + j), d3);
             for (int l = 0; l < k; ++l) a -= __ldcg(gw.urow + l) * Vl[j + mq * l];
             vk[j] = a;
             const double aa = fabs(a);
@@ -863,13 +866,15 @@ __device__ int gang_aca(const MaternParams &mp, const double *xs, const double *
             for (int l = threadIdx.x; l <= k; l += NT) __stcg(gw.vrow + l, Vl[(js - q0) + mq * l]);
         gang_sync(gg);
         const double piv = __ldcg(gw.vrow + k);
-        const double xj = xs[C0 + js], yj = ys[C0 + js];
+        const bool d3j = P.z != nullptr;
+        const double xj = P.x[C0 + js], yj = P.y[C0 + js], zj = d3j ? P.z[C0 + js] : 0.0;
         double *uk = Ul + mq * k;
         bv = -1.0;
         bi = m;
         double su = 0.0, sv = 0.0;
         for (int64_t i = threadIdx.x; i < mq; i += NT) {
-            double cc = hcov_cov_entry(mp, xs[R0 + q0 + i], ys[R0 + q0 + i], xj, yj, (R0 + q0 + i) == (C0 + js));
+            double cc = hcov_cov_entry_d(mp, P.x[R0 + q0 + i], P.y[R0 + q0 + i], d3j ? P.z[R0 + q0 + i] : 0.0, xj, yj, zj,
+                                         (R0 + q0 + i) == (C0 + js), d3j);
             for (int l = 0; l < k; ++l) cc -= Ul[i + mq * l] * __ldcg(gw.vrow + l);
             const double u = cc / piv;
             uk[i] = u;
@@ -938,7 +943,7 @@ __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *sme
         CompressWs w = make_ws(scr, m, KB, &X2, &Y2);
         uint8_t *used = (uint8_t *)w.tail;
         PH_BEGIN(tp);
-        k = aca_partial(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, K, 0.1 * ea, used, red, redv, redi);
+        k = aca_partial(c.mp, Pts{c.xs, c.ys, c.zs}, b.row0, b.col0, m, w.X, w.Y, K, 0.1 * ea, used, red, redv, redi);
         PH_END(8, tp);
         if (k == K && K < m && threadIdx.x == 0) atomicAdd(c.flags + cut_flag(c), 1);   // ACA not converged
         rk = compress(w, m, k, ea, final_tol(ea, k), true, km, c.kcap, r_U(c, r), r_V(c, r), m, &cb, &of,
@@ -950,7 +955,7 @@ __device__ void task_aca(const Ctx &c, const DTask &tk, double *scr, double *sme
         CompressWs w = make_ws(scr, gg->mq, KB, &X2, &Y2, 4);
         w.tsr = scr + task_scratch_base(gg->mq, c.kcap, 4);
         GangWs gw = make_gws(gg->shared, KB, gg->G);
-        k = gang_aca(c.mp, c.xs, c.ys, b.row0, b.col0, m, w.X, w.Y, (uint8_t *)w.tail, K, 0.1 * ea, gw, *gg, red,
+        k = gang_aca(c.mp, Pts{c.xs, c.ys, c.zs}, b.row0, b.col0, m, w.X, w.Y, (uint8_t *)w.tail, K, 0.1 * ea, gw, *gg, red,
                      redv, redi);
         if (k == K && K < m && gg->g == 0 && threadIdx.x == 0) atomicAdd(c.flags + cut_flag(c), 1);
         rk = gang_compress(w, gw, *gg, k, ea, final_tol(ea, k), true, km, c.kcap, r_U(c, r), r_V(c, r), m,

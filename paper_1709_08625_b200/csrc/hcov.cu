@@ -537,7 +537,7 @@ __global__ void k_cov_columns(Ctx c, const int64_t *pc, int mcols, double *out)
         const int64_t ex = c.perm_i2e[p];
         if (ex < 0) continue;
         const int64_t q = pc[k];
-        out[ex + c.n_real * k] = hcov_cov_entry(c.mp, c.xs[p], c.ys[p], c.xs[q], c.ys[q], p == q);
+        out[ex + c.n_real * k] = pts_cov(c.mp, Pts{c.xs, c.ys, c.zs}, p, q);
     }
 }
 
@@ -744,7 +744,7 @@ struct hcov_tree_s {
     int32_t *d_col_off = nullptr, *d_col_nodes = nullptr;
     int32_t *d_band_off = nullptr;
     int32_t *d_diag_tile = nullptr;
-    double *d_xs = nullptr, *d_ys = nullptr;
+    double *d_xs = nullptr, *d_ys = nullptr, *d_zs = nullptr;   // d_zs: 3-D variant only
     int64_t *d_perm_i2e = nullptr;
     int32_t *d_leafnodes = nullptr;
     int32_t n_leafnodes = 0;
@@ -814,7 +814,7 @@ hcov_tree_s::~hcov_tree_s()
     eng.release();
     void *ps[] = {d_nodes, d_tile_node, d_rblk, d_terms, d_xterm, d_fac_row0, d_fac_nrows, d_fac_rank_src,
                   d_fac_off, d_fac_pool, d_solves, d_solve_rhs, d_slots, d_ctr, d_phw, d_col_r, d_tasks, d_phase,
-                  d_succ_off, d_succ, d_diag_tile, d_xs, d_ys, d_perm_i2e, d_leafnodes, d_row_off, d_row_nodes,
+                  d_succ_off, d_succ, d_diag_tile, d_xs, d_ys, d_zs, d_perm_i2e, d_leafnodes, d_row_off, d_row_nodes,
                   d_col_off, d_col_nodes};
     for (void *p : ps) cudaFree(p);
     for (int m = 0; m < HCOV_MODES; ++m) {
@@ -867,6 +867,7 @@ hcov_status tree_upload(hcov_tree t)
     CK(upload(&t->d_diag_tile, P.diag_tile));
     CK(upload(&t->d_xs, P.xs));
     CK(upload(&t->d_ys, P.ys));
+    if (P.dim == 3) CK(upload(&t->d_zs, P.zs));
     CK(upload(&t->d_perm_i2e, P.perm_i2e));
     std::vector<int32_t> leafnodes;
     std::vector<std::vector<int32_t>> rows(P.n_leaves);
@@ -1064,7 +1065,7 @@ void fill_ctx(hcov_hmat h)
     c.fac_rank_src = t->d_fac_rank_src; c.fac_off = t->d_fac_off; c.fac_pool = t->d_fac_pool;
     c.solves = t->d_solves; c.solve_rhs = t->d_solve_rhs; c.slots = t->d_slots; c.ctr = t->d_ctr;
     c.phw = t->d_phw; c.col_r = t->d_col_r; c.tasks = t->d_tasks; c.succ_off = t->d_succ_off; c.succ = t->d_succ;
-    c.diag_tile = t->d_diag_tile; c.xs = t->d_xs; c.ys = t->d_ys; c.perm_i2e = t->d_perm_i2e;
+    c.diag_tile = t->d_diag_tile; c.xs = t->d_xs; c.ys = t->d_ys; c.zs = t->d_zs; c.perm_i2e = t->d_perm_i2e;
     c.depth = P.depth; c.n_r = (int32_t)P.n_r(); c.root_solve = P.root_solve; c.ntasks = (int32_t)P.tasks.size();
     c.n_pad = P.n_pad; c.n_leaves = P.n_leaves; c.n_real = P.n; c.n_tiles = P.n_tiles();
     c.tiles = h->tiles; c.U = h->U; c.V = h->V; c.rank = h->rank; c.cores = h->cores; c.W = h->W; c.P = h->P;
@@ -1319,13 +1320,21 @@ const char *hcov_status_string(hcov_status s)
     return "unknown";
 }
 
+// schedule-granularity experiments (not part of the method): HCOV_RCHUNK = pending terms per RAPP
+// chunk of a large low-rank block, HCOV_TCHUNK = pending terms per TAPP task
+static void plan_env_overrides(PlanOpts &o)
+{
+    if (const char *e = std::getenv("HCOV_RCHUNK")) { const int v = std::atoi(e); if (v >= 1 && v <= 16) o.rchunk = v; }
+    if (const char *e = std::getenv("HCOV_TCHUNK")) { const int v = std::atoi(e); if (v >= 1 && v <= 64) o.chunk = v; }
+}
+
 hcov_status hcov_build_tree_host_ex(const double *s_host, int64_t n, const hcov_tree_opts *opts, hcov_tree *out)
 {
     if (!out || !opts) return HCOV_ERR_INVALID_ARG;
     *out = nullptr;
     if (n == 0) return HCOV_ERR_EMPTY_INPUT;
     if (!s_host || n < 0 || opts->leaf_size != HCOV_LEAF || !(opts->eta >= 0) || opts->dense_below < 0 ||
-        (opts->factor_trunc != 0 && opts->factor_trunc != 1))
+        (opts->factor_trunc != 0 && opts->factor_trunc != 1) || (opts->dim != 0 && opts->dim != 2 && opts->dim != 3))
         return HCOV_ERR_INVALID_ARG;
     std::unique_ptr<hcov_tree_s> t(new (std::nothrow) hcov_tree_s());
     if (!t) return HCOV_ERR_OUT_OF_MEMORY;
@@ -1333,6 +1342,8 @@ hcov_status hcov_build_tree_host_ex(const double *s_host, int64_t n, const hcov_
     o.eta = opts->eta;
     o.dense_below = opts->dense_below;
     o.factor_trunc = opts->factor_trunc != 0;
+    o.dim = opts->dim == 3 ? 3 : 2;
+    plan_env_overrides(o);
     const auto g0 = std::chrono::steady_clock::now();
     int rc = plan_build(t->P, s_host, n, o);
     t->geo_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - g0).count();
@@ -1345,7 +1356,7 @@ hcov_status hcov_build_tree_host_ex(const double *s_host, int64_t n, const hcov_
 hcov_status hcov_build_tree_host(const double *s_host, int64_t n, int32_t leaf_size, double eta, int32_t dense_below,
                                  hcov_tree *out)
 {
-    const hcov_tree_opts o{leaf_size, eta, dense_below, 0};
+    const hcov_tree_opts o{leaf_size, eta, dense_below, 0, 2};
     return hcov_build_tree_host_ex(s_host, n, &o, out);
 }
 
@@ -1357,7 +1368,7 @@ hcov_status hcov_build_tree_ex(const double *s_dev, int64_t n, const hcov_tree_o
     if (n == 0) return HCOV_ERR_EMPTY_INPUT;
     if (!s_dev || n < 0 || !opts) return HCOV_ERR_INVALID_ARG;
     if (opts->leaf_size != HCOV_LEAF || !(opts->eta >= 0) || opts->dense_below < 0 ||
-        (opts->factor_trunc != 0 && opts->factor_trunc != 1))
+        (opts->factor_trunc != 0 && opts->factor_trunc != 1) || (opts->dim != 0 && opts->dim != 2 && opts->dim != 3))
         return HCOV_ERR_INVALID_ARG;
     // A1 / A2 on the device (tree.cu: K1 cluster tree, K2 block tree); the task DAG is planned on
     // the host from their output
@@ -1367,6 +1378,8 @@ hcov_status hcov_build_tree_ex(const double *s_dev, int64_t n, const hcov_tree_o
     o.eta = opts->eta;
     o.dense_below = opts->dense_below;
     o.factor_trunc = opts->factor_trunc != 0;
+    o.dim = opts->dim == 3 ? 3 : 2;
+    plan_env_overrides(o);
     {
         PlanGeo geo;
         const auto g0 = std::chrono::steady_clock::now();
@@ -1391,7 +1404,7 @@ hcov_status hcov_build_tree_ex(const double *s_dev, int64_t n, const hcov_tree_o
 hcov_status hcov_build_tree(const double *s_dev, int64_t n, int32_t leaf_size, double eta, int32_t dense_below,
                             hcov_stream stream, hcov_tree *out)
 {
-    const hcov_tree_opts o{leaf_size, eta, dense_below, 0};
+    const hcov_tree_opts o{leaf_size, eta, dense_below, 0, 2};
     return hcov_build_tree_ex(s_dev, n, &o, stream, out);
 }
 
@@ -1407,6 +1420,7 @@ hcov_status hcov_tree_get_info(hcov_tree t, hcov_tree_info *info)
     info->max_mq = P.max_mq;
     info->tree_on_device = t->tree_on_device ? 1 : 0;
     info->geo_ms = t->geo_ms;
+    info->dim = P.dim;
     return HCOV_OK;
 }
 
@@ -1988,7 +2002,7 @@ hcov_status hcov_cov_columns(hcov_tree t, const hcov_theta *theta, const int64_t
         pc[k] = e2i[cols_host[k]];
     }
     Ctx c{};
-    c.xs = t->d_xs; c.ys = t->d_ys; c.perm_i2e = t->d_perm_i2e; c.n_pad = P.n_pad; c.n_real = P.n;
+    c.xs = t->d_xs; c.ys = t->d_ys; c.zs = t->d_zs; c.perm_i2e = t->d_perm_i2e; c.n_pad = P.n_pad; c.n_real = P.n;
     c.mp = hcov_matern_params(theta->sigma2, theta->ell, theta->nu, theta->nugget);   // tab = null: direct K_nu
     int64_t *d_pc = nullptr;
     CK(cudaMalloc(&d_pc, std::max(1, m) * sizeof(int64_t)));

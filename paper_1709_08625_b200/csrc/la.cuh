@@ -1292,7 +1292,7 @@ __device__ int aca_full(double *S, int64_t m, double *X, double *Y, int Kmax, do
 // first row i* = 0; ties -> lowest index; column scaled by 1/pivot; a zero residual row is
 // skipped (next unused row); stop after adding term k when ||u_k|| ||v_k|| <= eps_aca ||u_1|| ||v_1||.
 // ------------------------------------------------------------------------------------------
-__device__ int aca_partial(const MaternParams &mp, const double *xs, const double *ys, int64_t r0,
+__device__ int aca_partial(const MaternParams &mp, const Pts P, int64_t r0,
                            int64_t c0, int64_t m, double *U, double *V, int Kmax, double eps_aca,
                            uint8_t *used, double *red, double *redv, int64_t *redi)
 {
@@ -1304,11 +1304,13 @@ __device__ int aca_partial(const MaternParams &mp, const double *xs, const doubl
     int64_t guard = 0;
     while (k < Kmax && guard++ < m + Kmax) {
         // row residual -> V[:,k]
-        const double xi = xs[r0 + istar], yi = ys[r0 + istar];
+        const bool d3 = P.z != nullptr;
+        const double xi = P.x[r0 + istar], yi = P.y[r0 + istar], zi = d3 ? P.z[r0 + istar] : 0.0;
         double bv = 0.0; int64_t bi = 0;
         double *vk = V + m * k;
         for (int64_t j = threadIdx.x; j < m; j += NT) {
-            double a = hcov_cov_entry(mp, xi, yi, xs[c0 + j], ys[c0 + j], (r0 + istar) == (c0 + j));
+            double a = hcov_cov_entry_d(mp, xi, yi, zi, P.x[c0 + j], P.y[c0 + j], d3 ? P.z[c0 + j] : 0.0,
+                                        (r0 + istar) == (c0 + j), d3);
             for (int l = 0; l < k; ++l) a -= U[istar + m * l] * V[j + m * l];
             vk[j] = a;
             double aa = fabs(a);
@@ -1329,12 +1331,13 @@ __device__ int aca_partial(const MaternParams &mp, const double *xs, const doubl
         }
         const int64_t js = b.i;
         const double piv = vk[js];
-        const double xj = xs[c0 + js], yj = ys[c0 + js];
+        const double xj = P.x[c0 + js], yj = P.y[c0 + js], zj = d3 ? P.z[c0 + js] : 0.0;
         double *uk = U + m * k;
         bv = -1.0; bi = m;
         double su = 0.0, sv = 0.0;
         for (int64_t i = threadIdx.x; i < m; i += NT) {
-            double c = hcov_cov_entry(mp, xs[r0 + i], ys[r0 + i], xj, yj, (r0 + i) == (c0 + js));
+            double c = hcov_cov_entry_d(mp, P.x[r0 + i], P.y[r0 + i], d3 ? P.z[r0 + i] : 0.0, xj, yj, zj,
+                                        (r0 + i) == (c0 + js), d3);
             for (int l = 0; l < k; ++l) c -= U[i + m * l] * V[js + m * l];
             double u = c / piv;
             uk[i] = u;

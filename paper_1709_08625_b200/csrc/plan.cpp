@@ -63,18 +63,28 @@ struct Builder {
     Builder(Plan &p, const PlanOpts &o) : P(p), O(o), L(p.depth) {}
 
     // ---------------------------------------------------------------- A2 geometry
+    // box of cluster h: lo[d] = b[d], hi[d] = b[D + d] (D = dim)
     double diam(int64_t h) const
     {
-        const double *b = &P.bb[4 * h];
-        double dx = b[2] - b[0], dy = b[3] - b[1];
-        return std::sqrt(dx * dx + dy * dy);
+        const int D = P.dim;
+        const double *b = &P.bb[2 * D * h];
+        double s2 = 0.0;
+        for (int d = 0; d < D; ++d) {
+            const double e = b[D + d] - b[d];
+            s2 = (d == 0) ? e * e : s2 + e * e;
+        }
+        return std::sqrt(s2);
     }
     double dist(int64_t h1, int64_t h2) const
     {
-        const double *a = &P.bb[4 * h1], *b = &P.bb[4 * h2];
-        double gx = std::max(0.0, std::max(a[0] - b[2], b[0] - a[2]));
-        double gy = std::max(0.0, std::max(a[1] - b[3], b[1] - a[3]));
-        return std::sqrt(gx * gx + gy * gy);
+        const int D = P.dim;
+        const double *a = &P.bb[2 * D * h1], *b = &P.bb[2 * D * h2];
+        double s2 = 0.0;
+        for (int d = 0; d < D; ++d) {
+            const double g = std::max(0.0, std::max(a[d] - b[D + d], b[d] - a[D + d]));
+            s2 = (d == 0) ? g * g : s2 + g * g;
+        }
+        return std::sqrt(s2);
     }
     bool admissible(int l, int64_t i, int64_t j) const
     {
@@ -493,8 +503,10 @@ struct Builder {
 int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt, const PlanGeo *geo)
 {
     if (n <= 0) return 2;
+    if (opt.dim != 2 && opt.dim != 3) return 1;
+    const int D = opt.dim;
     if (!geo)
-        for (int64_t k = 0; k < 2 * n; ++k)
+        for (int64_t k = 0; k < D * n; ++k)
             if (!std::isfinite(s[k])) return 1;
     P.opt = opt;
     P.opt.dense_below = std::max(opt.dense_below, HCOV_LEAF);
@@ -504,15 +516,18 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt, const P
     while (((int64_t)HCOV_LEAF << L) < n) ++L;
     P.n = n; P.depth = L; P.n_leaves = (int64_t)1 << L; P.n_pad = (int64_t)HCOV_LEAF << L;
     P.n_clusters = ((int64_t)2 << L) - 1;
-    P.bb.assign(4 * P.n_clusters, 0.0);
+    P.dim = D;
+    P.bb.assign(2 * D * P.n_clusters, 0.0);
 
     if (geo) {   // A1 done on the device (tree.cu K1)
         if (geo->depth != L || (int64_t)geo->perm_i2e.size() != P.n_pad || (int64_t)geo->xs.size() != P.n_pad ||
-            (int64_t)geo->ys.size() != P.n_pad || (int64_t)geo->bb.size() != 4 * P.n_clusters)
+            (int64_t)geo->ys.size() != P.n_pad || (int64_t)geo->bb.size() != 2 * D * P.n_clusters ||
+            (D == 3 && (int64_t)geo->zs.size() != P.n_pad))
             return 3;
         P.perm_i2e = geo->perm_i2e;
         P.xs = geo->xs;
         P.ys = geo->ys;
+        if (D == 3) P.zs = geo->zs;
         P.bb = geo->bb;
     }
     // ---- A1 -------------------------------------------------------------------------------
@@ -525,19 +540,25 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt, const P
         std::vector<int64_t> rs2, re2;
         if (l < L) { rs2.resize(2 * nc); re2.resize(2 * nc); }
         for (int64_t c = 0; c < nc; ++c) {
-            double lx = std::numeric_limits<double>::infinity(), ly = lx, hx = -lx, hy = -lx;
-            for (int64_t k = rs[c]; k < re[c]; ++k) {
-                double x = s[2 * perm[k]], y = s[2 * perm[k] + 1];
-                lx = std::min(lx, x); hx = std::max(hx, x);
-                ly = std::min(ly, y); hy = std::max(hy, y);
+            double lo[3], hi[3];
+            for (int d = 0; d < D; ++d) { lo[d] = std::numeric_limits<double>::infinity(); hi[d] = -lo[d]; }
+            for (int64_t k = rs[c]; k < re[c]; ++k)
+                for (int d = 0; d < D; ++d) {
+                    const double x = s[D * perm[k] + d];
+                    lo[d] = std::min(lo[d], x); hi[d] = std::max(hi[d], x);
+                }
+            double *b = &P.bb[2 * D * heap_id(l, c)];
+            for (int d = 0; d < D; ++d) {
+                b[d] = (re[c] > rs[c]) ? lo[d] : std::numeric_limits<double>::quiet_NaN();
+                b[D + d] = (re[c] > rs[c]) ? hi[d] : std::numeric_limits<double>::quiet_NaN();
             }
-            double *b = &P.bb[4 * heap_id(l, c)];
-            if (re[c] > rs[c]) { b[0] = lx; b[1] = ly; b[2] = hx; b[3] = hy; }
-            else { b[0] = b[1] = b[2] = b[3] = std::numeric_limits<double>::quiet_NaN(); }
             if (l == L) continue;
-            int axis = (hx - lx >= hy - ly) ? 0 : 1;
+            // longest extent, ties -> lowest axis (x, then y)
+            int axis = 0;
+            for (int d = 1; d < D; ++d)
+                if (hi[d] - lo[d] > hi[axis] - lo[axis]) axis = d;
             std::stable_sort(perm.begin() + rs[c], perm.begin() + re[c],
-                             [&](int64_t a, int64_t b2) { return s[2 * a + axis] < s[2 * b2 + axis]; });
+                             [&](int64_t a, int64_t b2) { return s[D * a + axis] < s[D * b2 + axis]; });
             int64_t m = re[c] - rs[c], m1 = (m + 1) / 2;
             rs2[2 * c] = rs[c]; re2[2 * c] = rs[c] + m1;
             rs2[2 * c + 1] = rs[c] + m1; re2[2 * c + 1] = re[c];
@@ -547,13 +568,15 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt, const P
     P.perm_i2e.assign(P.n_pad, -1);
     P.xs.assign(P.n_pad, std::numeric_limits<double>::quiet_NaN());
     P.ys.assign(P.n_pad, std::numeric_limits<double>::quiet_NaN());
+    if (D == 3) P.zs.assign(P.n_pad, std::numeric_limits<double>::quiet_NaN());
     for (int64_t c = 0; c < P.n_leaves; ++c) {
         if (re[c] - rs[c] > HCOV_LEAF) return 3;  // cannot happen (sizes <= ceil(n / 2^L) <= 32)
         for (int64_t k = rs[c]; k < re[c]; ++k) {
             int64_t pos = c * HCOV_LEAF + (k - rs[c]);
             P.perm_i2e[pos] = perm[k];
-            P.xs[pos] = s[2 * perm[k]];
-            P.ys[pos] = s[2 * perm[k] + 1];
+            P.xs[pos] = s[D * perm[k]];
+            P.ys[pos] = s[D * perm[k] + 1];
+            if (D == 3) P.zs[pos] = s[D * perm[k] + 2];
         }
     }
     }   // !geo

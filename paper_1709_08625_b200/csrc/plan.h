@@ -15,6 +15,7 @@ struct PlanOpts {
     int rchunk = 3;         // pending terms appended per RAPP task of a large low-rank block
     int fill_tiles = 8;     // tiles per FILL task
     int64_t big_m = HCOV_DENSE_MAX;   // larger low-rank blocks: chunked recompression, capacity 2 kcap
+    int dim = 2;            // 2-D locations, or 3 (the 3-D variant)
     bool factor_trunc = false;  // SPD-preserving mode (R27): per low-rank block, the last
                                 // update chunk keeps the block near-lossless (d = 2), the block's
                                 // forward solve runs on that, then a TRUNC task (a RAPP without terms,
@@ -28,8 +29,9 @@ struct Plan {
     int depth = 0;                  // L; leaves = 2^L clusters of 32 (padded) positions
     int64_t n_leaves = 0;
     std::vector<int64_t> perm_i2e;  // n_pad, -1 for phantom positions
-    std::vector<double> xs, ys;     // n_pad internal coordinates (NaN for phantom)
-    std::vector<double> bb;         // 4 per cluster heap id: lo_x, lo_y, hi_x, hi_y
+    int dim = 2;                    // 2 or 3
+    std::vector<double> xs, ys, zs; // n_pad internal coordinates (NaN for phantom); zs only for dim 3
+    std::vector<double> bb;         // 2 dim per cluster heap id: lo_x, lo_y[, lo_z], hi_x, hi_y[, hi_z]
     int64_t n_clusters = 0;         // 2^(L+1) - 1 (heap ids: id = 2^l - 1 + c)
 
     // ---- A2: block tree (lower triangle incl. diagonal) ------------------------------
@@ -88,8 +90,8 @@ struct Plan {
 struct PlanGeo {
     int depth = 0;
     std::vector<int64_t> perm_i2e;   // n_pad
-    std::vector<double> xs, ys;      // n_pad
-    std::vector<double> bb;          // 4 per cluster heap id
+    std::vector<double> xs, ys, zs;  // n_pad (zs: dim 3 only)
+    std::vector<double> bb;          // 2 dim per cluster heap id
     std::vector<std::vector<std::pair<int32_t, int32_t>>> level_pairs;   // (i, j) per level
     std::vector<std::vector<int8_t>> level_types;                        // NodeType per pair
 };

@@ -73,43 +73,47 @@ __global__ void k_iota(int32_t *p, int64_t n)
 }
 
 // Bounding box and split axis of every cluster of one level (one CTA per cluster, grid-stride).
-__global__ void __launch_bounds__(256) k_seg_bbox(const double *s, const int32_t *perm, const int64_t *rs,
+// s: n x D row-major; box layout lo[0..D), hi[0..D) (as the host planner).
+__global__ void __launch_bounds__(256) k_seg_bbox(const double *s, int D, const int32_t *perm, const int64_t *rs,
                                                   int64_t nseg, int64_t heap0, double *bb, int8_t *axis)
 {
-    __shared__ double red[4][8];
+    __shared__ double red[6][8];
     for (int64_t c = blockIdx.x; c < nseg; c += gridDim.x) {
         const int64_t a = rs[c], b = rs[c + 1];
-        double lx = INFINITY, ly = INFINITY, hx = -INFINITY, hy = -INFINITY;
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
         for (int64_t k = a + threadIdx.x; k < b; k += blockDim.x) {
             const int64_t e = perm[k];
-            const double x = s[2 * e], y = s[2 * e + 1];
-            lx = fmin(lx, x); hx = fmax(hx, x);
-            ly = fmin(ly, y); hy = fmax(hy, y);
+            for (int d = 0; d < D; ++d) {
+                const double x = s[D * e + d];
+                lo[d] = fmin(lo[d], x); hi[d] = fmax(hi[d], x);
+            }
         }
         // min / max are exact (order-independent) for finite values
-        for (int o = 16; o > 0; o >>= 1) {
-            lx = fmin(lx, __shfl_xor_sync(0xffffffffu, lx, o));
-            ly = fmin(ly, __shfl_xor_sync(0xffffffffu, ly, o));
-            hx = fmax(hx, __shfl_xor_sync(0xffffffffu, hx, o));
-            hy = fmax(hy, __shfl_xor_sync(0xffffffffu, hy, o));
-        }
+        for (int d = 0; d < D; ++d)
+            for (int o = 16; o > 0; o >>= 1) {
+                lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+                hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+            }
         const int w = threadIdx.x >> 5;
-        if ((threadIdx.x & 31) == 0) { red[0][w] = lx; red[1][w] = ly; red[2][w] = hx; red[3][w] = hy; }
+        if ((threadIdx.x & 31) == 0)
+            for (int d = 0; d < D; ++d) { red[d][w] = lo[d]; red[3 + d][w] = hi[d]; }
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
-                lx = fmin(lx, red[0][k]); ly = fmin(ly, red[1][k]);
-                hx = fmax(hx, red[2][k]); hy = fmax(hy, red[3][k]);
-            }
-            double *o = bb + 4 * (heap0 + c);
+            for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+                for (int d = 0; d < D; ++d) { lo[d] = fmin(lo[d], red[d][k]); hi[d] = fmax(hi[d], red[3 + d][k]); }
+            double *o = bb + 2 * D * (heap0 + c);
             if (b > a) {
                 // with both -0.0 and +0.0 among the coordinates the stored zero's sign may differ
                 // from the host's (which keeps the first met); every use of a box is a difference
                 // followed by a square or a comparison, so the trees are the same either way
-                o[0] = lx; o[1] = ly; o[2] = hx; o[3] = hy;
-                axis[c] = (__dsub_rn(hx, lx) >= __dsub_rn(hy, ly)) ? 0 : 1;
+                for (int d = 0; d < D; ++d) { o[d] = lo[d]; o[D + d] = hi[d]; }
+                // longest extent, ties -> lowest axis
+                int ax = 0;
+                for (int d = 1; d < D; ++d)
+                    if (__dsub_rn(hi[d], lo[d]) > __dsub_rn(hi[ax], lo[ax])) ax = d;
+                axis[c] = (int8_t)ax;
             } else {
-                o[0] = o[1] = o[2] = o[3] = __longlong_as_double(0x7ff8000000000000ll);
+                for (int d = 0; d < 2 * D; ++d) o[d] = __longlong_as_double(0x7ff8000000000000ll);
                 axis[c] = 0;
             }
         }
@@ -118,8 +122,8 @@ __global__ void __launch_bounds__(256) k_seg_bbox(const double *s, const int32_t
 }
 
 // Sort keys of one level: coordinate bits on the cluster's split axis, and the cluster id.
-__global__ void k_keys(const double *s, const int32_t *perm, const int64_t *rs, int64_t nseg, const int8_t *axis,
-                       int64_t n, uint64_t *key, uint32_t *seg)
+__global__ void k_keys(const double *s, int D, const int32_t *perm, const int64_t *rs, int64_t nseg,
+                       const int8_t *axis, int64_t n, uint64_t *key, uint32_t *seg)
 {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
         // cluster containing position k: last c with rs[c] <= k
@@ -129,7 +133,7 @@ __global__ void k_keys(const double *s, const int32_t *perm, const int64_t *rs, 
             if (rs[mid] <= k) lo = mid; else hi = mid - 1;
         }
         const int64_t e = perm[k];
-        key[k] = order_bits(s[2 * e + axis[lo]]);
+        key[k] = order_bits(s[D * e + axis[lo]]);
         seg[k] = (uint32_t)lo;
     }
 }
@@ -250,19 +254,22 @@ __global__ void k_to_i32(const int64_t *a, int64_t n, int32_t *b)
 }
 
 // Leaf level: padded internal order (32 positions per leaf; phantoms -1 / NaN).
-__global__ void k_leaves(const double *s, const int32_t *perm, const int64_t *rs, int64_t nleaf, int64_t *i2e,
-                         double *xs, double *ys)
+__global__ void k_leaves(const double *s, int D, const int32_t *perm, const int64_t *rs, int64_t nleaf, int64_t *i2e,
+                         double *xs, double *ys, double *zs)
 {
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nleaf * HCOV_LEAF;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = q / HCOV_LEAF, o = q % HCOV_LEAF;
         const int64_t k = rs[c] + o;
         if (k < rs[c + 1]) {
             const int64_t e = perm[k];
-            i2e[q] = e; xs[q] = s[2 * e]; ys[q] = s[2 * e + 1];
+            i2e[q] = e; xs[q] = s[D * e]; ys[q] = s[D * e + 1];
+            if (zs) zs[q] = s[D * e + 2];
         } else {
             i2e[q] = -1;
-            xs[q] = ys[q] = __longlong_as_double(0x7ff8000000000000ll);
+            xs[q] = ys[q] = qnan;
+            if (zs) zs[q] = qnan;
         }
     }
 }
@@ -270,25 +277,32 @@ __global__ void k_leaves(const double *s, const int32_t *perm, const int64_t *rs
 // ---- A2 ------------------------------------------------------------------------------------
 struct Pair { int32_t i, j, forced; };
 
-__device__ __forceinline__ double diam_of(const double *b)
+__device__ __forceinline__ double diam_of(const double *b, int D)
 {
-    const double dx = __dsub_rn(b[2], b[0]), dy = __dsub_rn(b[3], b[1]);
-    return __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+    double s2 = 0.0;
+    for (int d = 0; d < D; ++d) {
+        const double e = __dsub_rn(b[D + d], b[d]);
+        s2 = (d == 0) ? __dmul_rn(e, e) : __dadd_rn(s2, __dmul_rn(e, e));
+    }
+    return __dsqrt_rn(s2);
 }
 
-__device__ __forceinline__ bool admissible(const double *bb, int64_t heap0, int32_t i, int32_t j, double eta)
+__device__ __forceinline__ bool admissible(const double *bb, int D, int64_t heap0, int32_t i, int32_t j, double eta)
 {
     if (eta <= 0.0) return false;
-    const double *a = bb + 4 * (heap0 + i), *b = bb + 4 * (heap0 + j);
-    const double gx = hmax(0.0, hmax(__dsub_rn(a[0], b[2]), __dsub_rn(b[0], a[2])));
-    const double gy = hmax(0.0, hmax(__dsub_rn(a[1], b[3]), __dsub_rn(b[1], a[3])));
-    const double d = __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)));
-    if (!(d > 0.0)) return false;
-    return hmin(diam_of(a), diam_of(b)) <= __dmul_rn(eta, d);
+    const double *a = bb + 2 * D * (heap0 + i), *b = bb + 2 * D * (heap0 + j);
+    double s2 = 0.0;
+    for (int d = 0; d < D; ++d) {
+        const double g = hmax(0.0, hmax(__dsub_rn(a[d], b[D + d]), __dsub_rn(b[d], a[D + d])));
+        s2 = (d == 0) ? __dmul_rn(g, g) : __dadd_rn(s2, __dmul_rn(g, g));
+    }
+    const double dd = __dsqrt_rn(s2);
+    if (!(dd > 0.0)) return false;
+    return hmin(diam_of(a, D), diam_of(b, D)) <= __dmul_rn(eta, dd);
 }
 
-__global__ void k_bclass(const Pair *pr, int64_t np, const double *bb, int l, int L, int64_t csize, int dense_below,
-                         double eta, int8_t *type, int32_t *nchild)
+__global__ void k_bclass(const Pair *pr, int64_t np, const double *bb, int D, int l, int L, int64_t csize,
+                         int dense_below, double eta, int8_t *type, int32_t *nchild)
 {
     const int64_t heap0 = ((int64_t)1 << l) - 1;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
@@ -298,7 +312,7 @@ __global__ void k_bclass(const Pair *pr, int64_t np, const double *bb, int l, in
             t = (l == L) ? ND_T : ND_H;
             nc = (t == ND_H) ? 3 : 0;
         } else {
-            const bool adm = !x.forced && admissible(bb, heap0, x.i, x.j, eta);
+            const bool adm = !x.forced && admissible(bb, D, heap0, x.i, x.j, eta);
             if (adm && l < L && csize > dense_below) t = ND_R;
             else if (l == L) t = ND_T;
             else t = ND_H;
@@ -310,8 +324,8 @@ __global__ void k_bclass(const Pair *pr, int64_t np, const double *bb, int l, in
     }
 }
 
-__global__ void k_bexpand(const Pair *pr, int64_t np, const int8_t *type, const int64_t *off, const double *bb, int l,
-                          double eta, Pair *out)
+__global__ void k_bexpand(const Pair *pr, int64_t np, const int8_t *type, const int64_t *off, const double *bb, int D,
+                          int l, double eta, Pair *out)
 {
     const int64_t heap0 = ((int64_t)1 << l) - 1;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x) {
@@ -323,7 +337,7 @@ __global__ void k_bexpand(const Pair *pr, int64_t np, const int8_t *type, const 
             o[1] = {2 * x.i + 1, 2 * x.j, x.forced};
             o[2] = {2 * x.i + 1, 2 * x.j + 1, x.forced};
         } else {
-            const int f = (x.forced || admissible(bb, heap0, x.i, x.j, eta)) ? 1 : 0;
+            const int f = (x.forced || admissible(bb, D, heap0, x.i, x.j, eta)) ? 1 : 0;
             for (int a = 0; a < 2; ++a)
                 for (int b = 0; b < 2; ++b) o[2 * a + b] = {2 * x.i + a, 2 * x.j + b, f};
         }
@@ -373,11 +387,13 @@ int tree_geo_device(const double *s, int64_t n, const PlanOpts &opt, cudaStream_
 {
     if (n <= 0) return 2;
     if (n >= ((int64_t)1 << 31) - HCOV_LEAF) return 1;
+    const int D = opt.dim;
+    if (D != 2 && D != 3) return 1;
     {
         DBuf<int> bad;
         if (bad.alloc(1)) return -1;
         TCK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-        k_finite<<<grid_for(2 * n), 256, 0, st>>>(s, 2 * n, bad.p);
+        k_finite<<<grid_for(D * n), 256, 0, st>>>(s, D * n, bad.p);
         int h = 0;
         TCK(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
         TCK(cudaStreamSynchronize(st));
@@ -405,21 +421,22 @@ int tree_geo_device(const double *s, int64_t n, const PlanOpts &opt, cudaStream_
     DBuf<uint64_t> key, key2;
     DBuf<uint32_t> seg, seg2;
     DBuf<int64_t> offs, bsum, tot, drs, i2e;
-    DBuf<double> bb, xs, ys;
+    DBuf<double> bb, xs, ys, zs;
     DBuf<int8_t> axis;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     if (perm.alloc(n) || perm2.alloc(n) || key.alloc(n) || key2.alloc(n) || seg.alloc(n) || seg2.alloc(n) ||
-        hist.alloc((size_t)RD * ntiles) || offs.alloc((size_t)RD * ntiles) || bb.alloc(4 * ncl) ||
-        axis.alloc(nleaf) || drs.alloc(nleaf + 1) || i2e.alloc(npad) || xs.alloc(npad) || ys.alloc(npad))
+        hist.alloc((size_t)RD * ntiles) || offs.alloc((size_t)RD * ntiles) || bb.alloc(2 * D * ncl) ||
+        axis.alloc(nleaf) || drs.alloc(nleaf + 1) || i2e.alloc(npad) || xs.alloc(npad) || ys.alloc(npad) ||
+        (D == 3 && zs.alloc(npad)))
         return -1;
     k_iota<<<grid_for(n), 256, 0, st>>>(perm.p, n);
     for (int l = 0; l <= L; ++l) {
         const int64_t nseg = (int64_t)1 << l;
         TCK(cudaMemcpyAsync(drs.p, rs[l].data(), (nseg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        k_seg_bbox<<<(unsigned)std::min<int64_t>(nseg, 148 * 8), 256, 0, st>>>(s, perm.p, drs.p, nseg, nseg - 1, bb.p,
-                                                                                axis.p);
+        k_seg_bbox<<<(unsigned)std::min<int64_t>(nseg, 148 * 8), 256, 0, st>>>(s, D, perm.p, drs.p, nseg, nseg - 1,
+                                                                                bb.p, axis.p);
         if (l == L) break;
-        k_keys<<<grid_for(n), 256, 0, st>>>(s, perm.p, drs.p, nseg, axis.p, n, key.p, seg.p);
+        k_keys<<<grid_for(n), 256, 0, st>>>(s, D, perm.p, drs.p, nseg, axis.p, n, key.p, seg.p);
         const int npass = 8 + (l + RB - 1) / RB;     // coordinate bytes, then the cluster id bytes
         for (int pass = 0; pass < npass; ++pass) {
             const unsigned nb = (unsigned)((ntiles + WPB - 1) / WPB);
@@ -430,13 +447,15 @@ int tree_geo_device(const double *s, int64_t n, const PlanOpts &opt, cudaStream_
             std::swap(key.p, key2.p); std::swap(seg.p, seg2.p); std::swap(perm.p, perm2.p);
         }
     }
-    k_leaves<<<grid_for(npad), 256, 0, st>>>(s, perm.p, drs.p, nleaf, i2e.p, xs.p, ys.p);
+    k_leaves<<<grid_for(npad), 256, 0, st>>>(s, D, perm.p, drs.p, nleaf, i2e.p, xs.p, ys.p, D == 3 ? zs.p : nullptr);
     TCK(cudaGetLastError());
-    g.perm_i2e.resize(npad); g.xs.resize(npad); g.ys.resize(npad); g.bb.resize(4 * ncl);
+    g.perm_i2e.resize(npad); g.xs.resize(npad); g.ys.resize(npad); g.bb.resize(2 * D * ncl);
+    if (D == 3) g.zs.resize(npad);
     TCK(cudaMemcpyAsync(g.perm_i2e.data(), i2e.p, npad * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     TCK(cudaMemcpyAsync(g.xs.data(), xs.p, npad * sizeof(double), cudaMemcpyDeviceToHost, st));
     TCK(cudaMemcpyAsync(g.ys.data(), ys.p, npad * sizeof(double), cudaMemcpyDeviceToHost, st));
-    TCK(cudaMemcpyAsync(g.bb.data(), bb.p, 4 * ncl * sizeof(double), cudaMemcpyDeviceToHost, st));
+    TCK(cudaMemcpyAsync(g.bb.data(), bb.p, 2 * D * ncl * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (D == 3) TCK(cudaMemcpyAsync(g.zs.data(), zs.p, npad * sizeof(double), cudaMemcpyDeviceToHost, st));
     TCK(cudaStreamSynchronize(st));
 
     // ---- A2: level-synchronous block tree ------------------------------------------------------
@@ -452,7 +471,7 @@ int tree_geo_device(const double *s, int64_t n, const PlanOpts &opt, cudaStream_
     g.level_types.assign(L + 1, {});
     for (int l = 0; l <= L && np > 0; ++l) {
         if (ty.alloc(np) || nch.alloc(np) || coff.alloc(np)) return -1;
-        k_bclass<<<grid_for(np), 256, 0, st>>>(pa.p, np, bb.p, l, L, (int64_t)HCOV_LEAF << (L - l), dense_below,
+        k_bclass<<<grid_for(np), 256, 0, st>>>(pa.p, np, bb.p, D, l, L, (int64_t)HCOV_LEAF << (L - l), dense_below,
                                               opt.eta, ty.p, nch.p);
         int64_t nnext = 0;
         if (scan_counts(nch.p, np, coff.p, bsum, tot, st, &nnext)) return -1;
@@ -462,7 +481,7 @@ int tree_geo_device(const double *s, int64_t n, const PlanOpts &opt, cudaStream_
         TCK(cudaMemcpyAsync(g.level_types[l].data(), ty.p, np, cudaMemcpyDeviceToHost, st));
         if (nnext > 0) {
             if (pb.alloc(nnext)) return -1;
-            k_bexpand<<<grid_for(np), 256, 0, st>>>(pa.p, np, ty.p, coff.p, bb.p, l, opt.eta, pb.p);
+            k_bexpand<<<grid_for(np), 256, 0, st>>>(pa.p, np, ty.p, coff.p, bb.p, D, l, opt.eta, pb.p);
         }
         TCK(cudaStreamSynchronize(st));
         TCK(cudaGetLastError());

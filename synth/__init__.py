@@ -61,6 +61,11 @@ def uniform_points(n: int, seed: int) -> np.ndarray:
     return np.random.default_rng(seed).random((n, 2))
 
 
+def uniform_points_3d(n: int, seed: int) -> np.ndarray:
+    """n points U[0,1]^3, (n, 3) float64 (the 3-D variant)."""
+    return np.random.default_rng(seed).random((n, 3))
+
+
 def clustered_points(n: int, seed: int, seed_cluster: int, frac: float = 0.05,
                      lo: float = 0.40, hi: float = 0.45) -> np.ndarray:
     """DESIGN.md R14: U[0,1]^2 with floor(frac*n) seeded indices moved to U[lo,hi]^2."""

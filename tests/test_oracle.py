@@ -201,3 +201,36 @@ def test_ou_sampler_matches_dense_factor():
     Z = oracle.sample_ou_collinear(s[:, 0], xi, 1.3, 0.07)
     ll, ld, q = oracle.loglik_dense(s, Z, 1.3, 0.07, 0.5, 0.0)
     assert abs(q - float(xi @ xi)) <= 1e-8 * q
+
+
+# ---- 3-D variant (only dim changes) ---------------------------------------
+def test_3d_distance_by_hand_and_n2_closed_form():
+    # |(0,0,0) - (1,2,2)| = 3 exactly; nu = 1/2: C_01 = s2 exp(-3/ell)
+    s = np.array([[0.0, 0.0, 0.0], [1.0, 2.0, 2.0]])
+    s2, ell, tau2 = 1.4, 2.0, 1e-3
+    C = oracle.cov_dense(s, s2, ell, 0.5, tau2)
+    assert abs(C[0, 1] - s2 * math.exp(-1.5)) < 1e-15 and C[0, 0] == s2 + tau2
+    z = np.array([0.7, -0.2])
+    a, b = s2 + tau2, s2 * math.exp(-1.5)
+    det = a * a - b * b
+    _, ld, q = oracle.loglik_dense(s, z, s2, ell, 0.5, tau2)
+    assert abs(ld - math.log(det)) < 1e-13
+    assert abs(q - (a * z[0] ** 2 - 2 * b * z[0] * z[1] + a * z[1] ** 2) / det) < 1e-13
+
+
+def test_3d_plane_embedding_equals_2d():
+    # points of the plane z = c in 3-D give the 2-D covariance exactly
+    s = synth.uniform_points(300, 17)
+    s3 = np.column_stack([s, np.full(300, 0.25)])
+    for nu in (0.5, 1.0, 1.5):
+        assert np.array_equal(oracle.cov_dense(s, 1.0, 0.1, nu, 1e-6), oracle.cov_dense(s3, 1.0, 0.1, nu, 1e-6))
+
+
+def test_3d_rotation_invariance():
+    # an orthogonal map of the locations leaves C and L unchanged (up to rounding of the distances)
+    s = synth.uniform_points_3d(400, 18)
+    q, _ = np.linalg.qr(np.random.default_rng(19).standard_normal((3, 3)))
+    z = synth.xi(400, 20)
+    a = oracle.loglik_dense(s, z, 1.0, 0.2, 1.0, 1e-4)
+    b = oracle.loglik_dense(s @ q.T + 0.3, z, 1.0, 0.2, 1.0, 1e-4)
+    assert abs(a[0] - b[0]) <= 1e-9 * abs(a[0])

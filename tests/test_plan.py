@@ -186,3 +186,31 @@ def test_factor_trunc_schedule(n, seed):
         assert ancestors_have(int(t), SEG), t
     # the rest of the schedule is unchanged in size: standard tasks + one TRUNC per block + one join per column
     assert t1.shape[0] > t0.shape[0] + nr - 1
+
+
+@pytest.mark.parametrize("n,seed", [(1, 1), (33, 2), (3000, 3)])
+def test_3d_tree_and_blocks_match_mirror(n, seed):
+    """3-D variant: host planner vs the oracle's restatement (argmax-extent axis,
+    3-D boxes, diameters and gaps)."""
+    s = synth.uniform_points_3d(n, seed)
+    T = H.Tree(s)
+    info = T.info()
+    Tm = htree.cluster_tree(s)
+    assert info["dim"] == 3 and info["depth"] == Tm.depth
+    assert np.array_equal(T.perm_i2e(), Tm.perm)
+    assert {tuple(int(v) for v in b) for b in T.blocks()} == set(htree.block_tree(Tm, 2.0, 32))
+    bb = T.bbox()
+    assert bb.shape[1] == 6
+    lo, hi = Tm.boxes[(0, 0)]
+    assert np.array_equal(bb[0, :3], lo) and np.array_equal(bb[0, 3:], hi)
+
+
+def test_3d_flat_points_give_the_2d_tree():
+    """Points with a constant z: the z extent is 0, never the longest, so the 3-D planner splits
+    exactly as the 2-D one."""
+    s = synth.uniform_points(5000, 4)
+    T2 = H.Tree(s)
+    T3 = H.Tree(np.column_stack([s, np.full(5000, 0.5)]))
+    assert np.array_equal(T2.perm_i2e(), T3.perm_i2e())
+    assert np.array_equal(T2.blocks(), T3.blocks())
+    assert np.array_equal(T2.tasks(), T3.tasks())
