@@ -197,6 +197,13 @@ hcov_status hcov_mle_batch(hcov_tree t, const double *Z_dev, const hcov_theta *t
  * Factored: state after hcov_cholesky (or hcov_eval's handle).  Synchronise the stream. */
 hcov_status hcov_forward_solve(hcov_hmat h, const double *z_dev, double *v_dev, hcov_stream stream);
 hcov_status hcov_backsolve(hcov_hmat h, const double *v_dev, double *u_dev, hcov_stream stream);
+/* NEXT (f4): the point-wise LDL^T form of the factor (the listing's ldl_inv with point_wise
+ * pivots; reading R8).  C~ = L' D L'^T with L' = L~ diag(L~)^{-1} unit lower and
+ * D = diag(L~)^2: the same factorization (log det = sum log D_i = 2 sum log L~_ii; the forward solve
+ * of L' is D^{1/2} times the one of L~).  D_dev: n fp64 device array, EXTERNAL order; D_e is the
+ * pivot of point e = its conditional variance given the points before it in the internal order
+ * (>= tau^2).  Factored handle required (HCOV_ERR_STATE otherwise); stream-ordered, no sync. */
+hcov_status hcov_ldl_diag(hcov_hmat h, double *D_dev, hcov_stream stream);
 hcov_status hcov_solve(hcov_hmat h, const double *b_dev, double *x_dev, hcov_stream stream);
 hcov_status hcov_matvec(hcov_hmat h, const double *x_dev, double *y_dev, hcov_stream stream);
 hcov_status hcov_pcg(hcov_hmat A, hcov_hmat M, const double *b_dev, double *x_dev, int32_t maxit, double tol,

@@ -99,6 +99,7 @@ _SIGS = {
     "hcov_forward_solve": (_I32, [_P, _P, _P, _P]),
     "hcov_backsolve": (_I32, [_P, _P, _P, _P]),
     "hcov_solve": (_I32, [_P, _P, _P, _P]),
+    "hcov_ldl_diag": (_I32, [_P, _P, _P]),
     "hcov_matvec": (_I32, [_P, _P, _P, _P]),
     "hcov_pcg": (_I32, [_P, _P, _P, _P, _I32, _D, _P, _P, _P]),
     "hcov_norm2_diff": (_I32, [_P, _P, _I32, ctypes.c_uint64, _P, _P]),
@@ -309,6 +310,13 @@ class HMatrix:
     def forward_solve(self, z, stream=None):
         """hcov_forward_solve: v = P L~^{-1} P^T z (external order)."""
         return self._vec_op("hcov_forward_solve", z, "z", stream)
+
+    def ldl_diag(self, stream=None):
+        """hcov_ldl_diag: D of the point-wise LDL^T form (n, external order) of the factored matrix."""
+        import torch
+        D = torch.empty(self.tree.n, dtype=torch.float64, device="cuda")
+        _check(lib().hcov_ldl_diag(self._h, _dev_f64(D), _stream(stream)), "hcov_ldl_diag")
+        return D
 
     def backsolve(self, v, stream=None):
         """hcov_backsolve: u = P L~^{-T} P^T v (external order)."""

@@ -414,6 +414,19 @@ __global__ void k_permute_out(Ctx c, const double *y, double *Zext)
     }
 }
 
+// Point-wise LDL^T read-out (NEXT (f4)): D_e = L~_pp^2 for the internal position p of point e
+// (the diagonal of the factor's diagonal leaf tiles, col-major 32 x 32).
+__global__ void k_ldl_diag(Ctx c, double *Dext)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < c.n_pad; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = c.perm_i2e[p];
+        if (e < 0) continue;
+        const int64_t leaf = p / HCOV_LEAF, i = p % HCOV_LEAF;
+        const double l = c.tiles[(int64_t)c.diag_tile[leaf] * HCOV_TILE + i + HCOV_LEAF * i];
+        Dext[e] = l * l;
+    }
+}
+
 // out[0] = log det, out[1] = quad, out[2] = min pivot (fixed-order reductions, one CTA)
 __global__ void __launch_bounds__(NT) k_reduce(Ctx c, double *out)
 {
@@ -1701,6 +1714,16 @@ hcov_status hcov_forward_solve(hcov_hmat h, const double *z_dev, double *v_dev, 
     if (!h || !z_dev || !v_dev) return HCOV_ERR_INVALID_ARG;
     if (h->state < 2) return HCOV_ERR_STATE;
     return solve_ext(h, z_dev, v_dev, true, false, (cudaStream_t)stream);
+}
+
+hcov_status hcov_ldl_diag(hcov_hmat h, double *D_dev, hcov_stream stream)
+{
+    if (!h || !D_dev) return HCOV_ERR_INVALID_ARG;
+    if (h->state < 2) return HCOV_ERR_STATE;
+    cudaStream_t st = (cudaStream_t)stream;
+    LAUNCH(PC_AUX, st, k_ldl_diag<<<256, 256, 0, st>>>(h->ctx, D_dev));
+    CK(cudaGetLastError());
+    return HCOV_OK;
 }
 
 hcov_status hcov_backsolve(hcov_hmat h, const double *v_dev, double *u_dev, hcov_stream stream)
