@@ -1339,6 +1339,7 @@ static void plan_env_overrides(PlanOpts &o)
 {
     if (const char *e = std::getenv("HCOV_RCHUNK")) { const int v = std::atoi(e); if (v >= 1 && v <= 16) o.rchunk = v; }
     if (const char *e = std::getenv("HCOV_TCHUNK")) { const int v = std::atoi(e); if (v >= 1 && v <= 64) o.chunk = v; }
+    if (const char *e = std::getenv("HCOV_GANG1_BELOW")) o.gang1_below = std::atoll(e);
 }
 
 hcov_status hcov_build_tree_host_ex(const double *s_host, int64_t n, const hcov_tree_opts *opts, hcov_tree *out)

@@ -20,10 +20,14 @@
 
 namespace {
 
+// blocks below this size (and >= HCOV_GANG_MIN) are "gangs" of one CTA (PlanOpts.gang1_below)
+thread_local int64_t t_gang1_below = 0;
+
 // gang size of an ACA / RAPP task of a low-rank block of size m (0 = a single CTA, queue 0)
 inline int32_t gang_of(int64_t m)
 {
     if (m < HCOV_GANG_MIN) return 0;
+    if (m < t_gang1_below) return 1;
     // gangs of up to 4 CTAs (faster to form, fewer idle members in the serial phases); 8 only for
     // the largest blocks, which bounds a member's rows (and the per-CTA scratch) at m/8
     const int64_t gmax = m >= 65536 ? HCOV_GANG : 4;
@@ -31,7 +35,7 @@ inline int32_t gang_of(int64_t m)
 }
 // RAPP gangs of blocks below 65,536 rows are side-split (DTask.pad = 1): half the members factor
 // the X panel, half the Y panel (one QR per member instead of two; engine.cuh gang_compress_split)
-inline bool rapp_split(int64_t m) { return m >= HCOV_GANG_MIN && m < 65536; }
+inline bool rapp_split(int64_t m) { return m >= HCOV_GANG_MIN && m >= t_gang1_below && m < 65536; }
 inline int32_t rapp_gang_of(int64_t m)
 {
     if (!rapp_split(m)) return gang_of(m);
@@ -509,6 +513,7 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt, const P
         for (int64_t k = 0; k < D * n; ++k)
             if (!std::isfinite(s[k])) return 1;
     P.opt = opt;
+    t_gang1_below = opt.gang1_below;
     P.opt.dense_below = std::max(opt.dense_below, HCOV_LEAF);
     P.opt.chunk = std::max(1, opt.chunk);
     P.opt.fill_tiles = std::max(1, opt.fill_tiles);

@@ -16,6 +16,8 @@ struct PlanOpts {
     int fill_tiles = 8;     // tiles per FILL task
     int64_t big_m = HCOV_DENSE_MAX;   // larger low-rank blocks: chunked recompression, capacity 2 kcap
     int dim = 2;            // 2-D locations, or 3 (the 3-D variant)
+    int64_t gang1_below = 0;   // low-rank blocks with HCOV_GANG_MIN <= m < gang1_below run their ACA /
+                               // RAPP tasks as one-CTA gangs (in-CTA TSQR, no inter-CTA barriers)
     bool factor_trunc = false;  // SPD-preserving mode (R27): per low-rank block, the last
                                 // update chunk keeps the block near-lossless (d = 2), the block's
                                 // forward solve runs on that, then a TRUNC task (a RAPP without terms,
