@@ -406,11 +406,14 @@ __device__ __forceinline__ void gang_sync(Gang &gg)
     __syncthreads();
     ++gg.nb;
     if (threadIdx.x == 0) {
+        // the Gang fields in registers for the spin (a reference into the engine's local frame)
+        volatile int32_t *bar = gg.bar;
+        volatile const uint32_t *abort = gg.abort;
+        const int target = gg.nb * gg.G;
         __threadfence();
         atomicAdd(gg.bar, 1);
-        const int target = gg.nb * gg.G;
-        while (*(volatile int32_t *)gg.bar < target) {
-            if (*(volatile const uint32_t *)gg.abort) break;
+        while (*bar < target) {
+            if (*abort) break;
             __nanosleep(64);
         }
         __threadfence();

@@ -316,21 +316,31 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, const Ctx *__res
             s_phase_cls = pc;
         }
         __syncthreads();
+        // flop counters of this task in call-local scalars (registers; an element of fl[] passed by
+        // reference was reloaded and stored through local memory in every inner-loop iteration)
+        double f1 = 0.0, f2 = 0.0;
+        int c1 = FC_ASM, c2 = FC_TRUNC;
         switch (tk.type) {
-        case TK_FILL: task_fill(ci, tk, fl[FC_ASM]); break;
-        case TK_ACA: task_aca(ci, tk, tscr, smem, red, redv, redi, fl[FC_ASM], fl[FC_TRUNC], gg); break;
+        case TK_FILL: task_fill(ci, tk, f1); break;
+        case TK_ACA: task_aca(ci, tk, tscr, smem, red, redv, redi, f1, f2, gg); break;
         case TK_TAPP:
         case TK_POTRF:
-        case TK_TRSM: task_tile(ci, tk, smem, fl[FC_TILE]); break;
-        case TK_RAPP: task_rapp(ci, tk, tscr, smem, red, redv, redi, fl[FC_TRUNC], gg); break;
-        case TK_SEG: task_seg(ci, tk, smem, fl[FC_SOLVE]); break;
-        case TK_PROJ: task_proj(ci, tk, smem, fl[FC_SOLVE]); break;
-        case TK_PRR: task_prr(ci, tk, fl[FC_PROD]); break;
-        case TK_PHWP: task_phwp(ci, tk, fl[FC_PROD]); break;
-        case TK_PHWR: task_phwr(ci, tk, smem, fl[FC_PROD]); break;
-        case TK_BSEG: task_bseg(ci, tk, smem, fl[FC_SOLVE]); break;
-        case TK_BPROJ: task_bproj(ci, tk, fl[FC_SOLVE]); break;
+        case TK_TRSM: task_tile(ci, tk, smem, f1); c1 = FC_TILE; break;
+        case TK_RAPP: task_rapp(ci, tk, tscr, smem, red, redv, redi, f1, gg); c1 = FC_TRUNC; break;
+        case TK_SEG: task_seg(ci, tk, smem, f1); c1 = FC_SOLVE; break;
+        case TK_PROJ: task_proj(ci, tk, smem, f1); c1 = FC_SOLVE; break;
+        case TK_PRR: task_prr(ci, tk, f1); c1 = FC_PROD; break;
+        case TK_PHWP: task_phwp(ci, tk, f1); c1 = FC_PROD; break;
+        case TK_PHWR: task_phwr(ci, tk, smem, f1); c1 = FC_PROD; break;
+        case TK_BSEG: task_bseg(ci, tk, smem, f1); c1 = FC_SOLVE; break;
+        case TK_BPROJ: task_bproj(ci, tk, f1); c1 = FC_SOLVE; break;
         default: break;
+        }
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < FC_N; ++k) {
+                if (k == c1) fl[k] += f1;
+                if (k == c2 && tk.type == TK_ACA) fl[k] += f2;
+            }
         }
         __threadfence();
         __syncthreads();
@@ -1340,6 +1350,9 @@ static void plan_env_overrides(PlanOpts &o)
     if (const char *e = std::getenv("HCOV_RCHUNK")) { const int v = std::atoi(e); if (v >= 1 && v <= 16) o.rchunk = v; }
     if (const char *e = std::getenv("HCOV_TCHUNK")) { const int v = std::atoi(e); if (v >= 1 && v <= 64) o.chunk = v; }
     if (const char *e = std::getenv("HCOV_GANG1_BELOW")) o.gang1_below = std::atoll(e);
+    if (const char *e = std::getenv("HCOV_GANG_ROWS")) o.gang_rows = std::atoll(e);
+    if (const char *e = std::getenv("HCOV_GANG_MAX_SMALL")) o.gang_max_small = std::atoi(e);
+    if (const char *e = std::getenv("HCOV_RAPP512")) o.rapp512 = std::atoi(e);
 }
 
 hcov_status hcov_build_tree_host_ex(const double *s_host, int64_t n, const hcov_tree_opts *opts, hcov_tree *out)

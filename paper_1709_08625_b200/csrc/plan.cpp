@@ -22,6 +22,9 @@ namespace {
 
 // blocks below this size (and >= HCOV_GANG_MIN) are "gangs" of one CTA (PlanOpts.gang1_below)
 thread_local int64_t t_gang1_below = 0;
+// gang shape (PlanOpts): rows per member, largest gang below m = 65,536, RAPP gang of m = 512
+thread_local int64_t t_gang_rows = 256;
+thread_local int32_t t_gang_max_small = 4, t_rapp512 = 4;
 
 // gang size of an ACA / RAPP task of a low-rank block of size m (0 = a single CTA, queue 0)
 inline int32_t gang_of(int64_t m)
@@ -30,8 +33,8 @@ inline int32_t gang_of(int64_t m)
     if (m < t_gang1_below) return 1;
     // gangs of up to 4 CTAs (faster to form, fewer idle members in the serial phases); 8 only for
     // the largest blocks, which bounds a member's rows (and the per-CTA scratch) at m/8
-    const int64_t gmax = m >= 65536 ? HCOV_GANG : 4;
-    return (int32_t)std::min<int64_t>(gmax, std::max<int64_t>(2, m / 256));
+    const int64_t gmax = m >= 65536 ? HCOV_GANG : t_gang_max_small;
+    return (int32_t)std::min<int64_t>(gmax, std::max<int64_t>(2, m / t_gang_rows));
 }
 // RAPP gangs of blocks below 65,536 rows are side-split (DTask.pad = 1): half the members factor
 // the X panel, half the Y panel (one QR per member instead of two; engine.cuh gang_compress_split)
@@ -39,7 +42,7 @@ inline bool rapp_split(int64_t m) { return m >= HCOV_GANG_MIN && m >= t_gang1_be
 inline int32_t rapp_gang_of(int64_t m)
 {
     if (!rapp_split(m)) return gang_of(m);
-    return m <= 512 ? 4 : HCOV_GANG;
+    return m <= 512 ? t_rapp512 : HCOV_GANG;
 }
 
 inline int64_t heap_id(int l, int64_t c) { return ((int64_t)1 << l) - 1 + c; }
@@ -514,6 +517,9 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt, const P
             if (!std::isfinite(s[k])) return 1;
     P.opt = opt;
     t_gang1_below = opt.gang1_below;
+    t_gang_rows = std::max<int64_t>(32, opt.gang_rows);
+    t_gang_max_small = std::max(2, std::min(HCOV_GANG, opt.gang_max_small));
+    t_rapp512 = std::max(2, std::min(HCOV_GANG, opt.rapp512)) & ~1;
     P.opt.dense_below = std::max(opt.dense_below, HCOV_LEAF);
     P.opt.chunk = std::max(1, opt.chunk);
     P.opt.fill_tiles = std::max(1, opt.fill_tiles);

@@ -16,6 +16,9 @@ struct PlanOpts {
     int fill_tiles = 8;     // tiles per FILL task
     int64_t big_m = HCOV_DENSE_MAX;   // larger low-rank blocks: chunked recompression, capacity 2 kcap
     int dim = 2;            // 2-D locations, or 3 (the 3-D variant)
+    int64_t gang_rows = 256;   // rows per gang member (ACA / non-split RAPP gangs: G = m / gang_rows)
+    int gang_max_small = 4;    // largest such gang below m = 65,536
+    int rapp512 = 4;           // side-split RAPP gang of the m = 512 blocks (even)
     int64_t gang1_below = 0;   // low-rank blocks with HCOV_GANG_MIN <= m < gang1_below run their ACA /
                                // RAPP tasks as one-CTA gangs (in-CTA TSQR, no inter-CTA barriers)
     bool factor_trunc = false;  // SPD-preserving mode (R27): per low-rank block, the last
