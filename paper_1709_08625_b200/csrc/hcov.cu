@@ -1136,15 +1136,17 @@ hcov_status engine_run_batch(hcov_hmat *hs, int nb, int md, cudaStream_t st)
     static const int mask[HCOV_MODES] = {7, 1, 2, 4, 8};
     const int64_t ntk = (int64_t)P.tasks.size();
     if (((int64_t)nb * ntk) >= ((int64_t)1 << (31 - QE_SHIFT))) return HCOV_ERR_INVALID_ARG;
-    for (int i = 0; i < nb; ++i) {
+    for (int i = 0; i < nb; ++i)
         if (hs[i]->t != t || hs[i]->kcap_alloc != hs[0]->kcap_alloc) return HCOV_ERR_INVALID_ARG;
+    // the engine's scratch first: the W / P pools of a first run take all the free memory left
+    hcov_status es = engine_alloc(t, hs[0]->kcap_alloc, nb);
+    if (es) return es;
+    for (int i = 0; i < nb; ++i) {
         if (md == 0 || md == 2 || md == 3) {
             hcov_status ps = pools_alloc(hs[i]);
             if (ps) return ps;
         }
     }
-    hcov_status es = engine_alloc(t, hs[0]->kcap_alloc, nb);
-    if (es) return es;
     Engine &E = t->eng;
     std::vector<Ctx> cx(nb);
     for (int i = 0; i < nb; ++i) {

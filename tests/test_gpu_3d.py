@@ -15,11 +15,12 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("nu,ell", [(0.5, 0.2), (1.0, 0.1), (1.5, 0.15)])
 def test_3d_parity_vs_oracle(nu, ell):
-    """3-D eps-ranks are higher than 2-D ones (they grow like |log eps|^(d+1)): measured on this
-    point set's admissible blocks (dense SVD), max rank 61-72 at eps = 1e-8 but 35-42 at 1e-6, so
-    the 3-D parity runs at eps = 1e-6 with rank capacity 64 (the largest) and no cap.  Bar: the
-    log-linear interpolation of north_star's two bars (1e-6 at eps = 1e-8, 1e-3 at eps = 1e-4) at
-    eps = 1e-6, i.e. 10^-4.5 ~ 3e-5."""
+    """3-D eps-ranks are higher than 2-D ones (they grow like |log eps|^(d+1)).  Measured on this
+    point set's admissible blocks (dense SVD): max rank 61-72 at eps = 1e-8, 48-57 at 1e-7, 35-42
+    at 1e-6; the method also needs the ACA (eps/10) and the near-lossless intermediate states
+    (eps * 1e-2, R22) within the largest rank capacity (64), so the 3-D parity runs at eps = 1e-5
+    (intermediate 1e-7: <= 57).  Bar: the log-linear interpolation of north_star's two bars (1e-6 at
+    eps = 1e-8, 1e-3 at eps = 1e-4) at eps = 1e-5: 10^-3.75 ~ 1.8e-4."""
     n = 3000
     s = synth.uniform_points_3d(n, 31)
     th = (1.0, ell, nu, 1e-6)
@@ -27,11 +28,12 @@ def test_3d_parity_vs_oracle(nu, ell):
     ref = oracle.loglik_dense(s, Z, *th)
     T = H.Tree(torch.from_numpy(s).cuda())
     assert T.info()["dim"] == 3 and T.info()["tree_on_device"] == 1
-    r = H.eval_loglik(T, th, torch.from_numpy(Z).cuda(), 1e-6, 0, 64)
-    print(f"3-D nu={nu} ell={ell}: rel {abs(r['loglik'] - ref[0]) / abs(ref[0]):.2e} max_rank {r['max_rank']}")
+    r = H.eval_loglik(T, th, torch.from_numpy(Z).cuda(), 1e-5, 0, 64)
+    print(f"3-D nu={nu} ell={ell}: status {r['status']} rel {abs(r['loglik'] - ref[0]) / abs(ref[0]):.2e} "
+          f"max_rank {r['max_rank']} acc_loss {r['acc_loss']} interm_cuts {r['interm_cuts']}")
     assert r["status"] == 0, r
-    assert abs(r["loglik"] - ref[0]) <= 3e-5 * abs(ref[0]), (r, ref)
-    assert abs(r["logdet"] - ref[1]) <= 3e-5 * abs(ref[1])
+    assert abs(r["loglik"] - ref[0]) <= 1.8e-4 * abs(ref[0]), (r, ref)
+    assert abs(r["logdet"] - ref[1]) <= 1.8e-4 * abs(ref[1])
 
 
 def test_3d_entries_vs_oracle():

@@ -19,15 +19,16 @@ T = H.Tree(torch.from_numpy(s).cuda())
 xi = torch.from_numpy(synth.xi(n, cfg.seed_xi)).cuda()
 Z = None
 for eg in (1e-7, 3e-7, 1e-6):
+    g = H.HMatrix(T, th, eg, 20)
     try:
-        g = H.HMatrix(T, th, eg, 20)
         g.cholesky()
         Z = g.sample(xi)
-        del g
         break
     except H.HcovError as e:
         if e.code != 4:
             raise
+    finally:
+        del g
 assert Z is not None
 for _ in range(2):
     r = H.eval_loglik(T, th, Z, 1e-6, 20)
