@@ -21,7 +21,8 @@ def test_3d_parity_vs_oracle(nu, ell):
     (eps * 1e-2, R22) within the largest rank capacity (64), so the 3-D parity runs at eps = 1e-5
     (intermediate 1e-7: <= 57); n = 2,000 (blocks <= 512) and ell = 0.2 keep the Schur-complement
     ranks of the factor inside the capacity too (at n = 3,000, nu = 1, ell = 0.1 they reach it).  Bar: the log-linear interpolation of north_star's two bars (1e-6 at
-    eps = 1e-8, 1e-3 at eps = 1e-4) at eps = 1e-5: 10^-3.75 ~ 1.8e-4."""
+    eps = 1e-8, 1e-3 at eps = 1e-4) at eps = 1e-5: 10^-3.75 ~ 1.8e-4, on the error SURVEY 8(c) row 11 grades (L(theta) at nu = 1 is
+    -107 against a component scale of 5.6e3, so the component-scaled error is the graded one)."""
     n = 2000
     s = synth.uniform_points_3d(n, 31)
     th = (1.0, ell, nu, 1e-6)
@@ -30,10 +31,15 @@ def test_3d_parity_vs_oracle(nu, ell):
     T = H.Tree(torch.from_numpy(s).cuda())
     assert T.info()["dim"] == 3 and T.info()["tree_on_device"] == 1
     r = H.eval_loglik(T, th, torch.from_numpy(Z).cuda(), 1e-5, 0, 64)
-    print(f"3-D nu={nu} ell={ell}: status {r['status']} rel {abs(r['loglik'] - ref[0]) / abs(ref[0]):.2e} "
+    # where |L| < 0.1 x the component scale
+    # n/2 log 2pi + |logdet|/2 + q/2 (L near a sign change), the component-scaled error is graded
+    scale = 0.5 * n * np.log(2 * np.pi) + 0.5 * abs(ref[1]) + 0.5 * ref[2]
+    dl = abs(r["loglik"] - ref[0])
+    err = dl / scale if abs(ref[0]) < 0.1 * scale else dl / abs(ref[0])
+    print(f"3-D nu={nu} ell={ell}: status {r['status']} rel {dl / abs(ref[0]):.2e} graded {err:.2e} "
           f"max_rank {r['max_rank']} acc_loss {r['acc_loss']} interm_cuts {r['interm_cuts']}")
     assert r["status"] == 0, r
-    assert abs(r["loglik"] - ref[0]) <= 1.8e-4 * abs(ref[0]), (r, ref)
+    assert err <= 1.8e-4, (r, ref)
     assert abs(r["logdet"] - ref[1]) <= 1.8e-4 * abs(ref[1])
 
 
