@@ -91,6 +91,7 @@ struct Ctx {
     int32_t *bgrp_busy;        // per group: 1 while a gang holds it
     int32_t *bgrp_cta;         // per CTA (member 0 of a gang): the group its gang holds
     int32_t big_mq;            // gang members with more rows than this use a big-member slot
+    int32_t dense_max;         // low-rank blocks up to this size use the dense-mode RAPP (PlanOpts.big_m)
     int32_t n_bgrp;
     double *flop;              // FC_N accumulators
     int64_t smem_dbl;          // dynamic shared memory of the engine (doubles)
@@ -1018,6 +1019,7 @@ __device__ void dense_gemm_add(double *S, int m, const double *XA, const double 
     constexpr int KC = 32, PR = 16 * MA, CN = 32 * NB;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     double *xs = sb, *ys = sb + KC * PR;
+    for (int c0 = 0; c0 < m; c0 += CN)
     for (int p0 = 0; p0 < m; p0 += PR) {
         double acc[MA][NB];
 #pragma unroll
@@ -1032,7 +1034,7 @@ __device__ void dense_gemm_add(double *S, int m, const double *XA, const double 
             }
             for (int e = threadIdx.x; e < KC * CN; e += NT) {
                 const int k = e / CN, j = e % CN;
-                ys[e] = (j < m && k0 + k < W) ? __ldcg(YB + j + (int64_t)m * (k0 + k)) : 0.0;
+                ys[e] = (c0 + j < m && k0 + k < W) ? __ldcg(YB + c0 + j + (int64_t)m * (k0 + k)) : 0.0;
             }
             __syncthreads();
 #pragma unroll 4
@@ -1052,24 +1054,50 @@ __device__ void dense_gemm_add(double *S, int m, const double *XA, const double 
         for (int a = 0; a < MA; ++a)
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
-                const int i = p0 + ty + 16 * a, j = tx + 32 * b;
+                const int i = p0 + ty + 16 * a, j = c0 + tx + 32 * b;
                 if (i < m && j < m) S[i + (int64_t)m * j] += acc[a][b];
             }
     }
     __syncthreads();
 }
 
-// Columns of one pending term in the dense accumulation (0 if a factor has rank 0).
+// Columns of one pending term in the batched GEMM of the dense accumulation (0 if a factor has rank
+// 0; 0 for a tile x tile term, which is applied directly to its 32 x 32 target, tt_apply).
 __device__ __forceinline__ int term_width(const Ctx &c, const DTerm &t)
 {
-    if (t.kind == TM_TT) return 32;
+    if (t.kind == TM_TT) return 0;
     const int ra = __ldcg(c.rank + c.fac_rank_src[t.a]), rb = __ldcg(c.rank + c.fac_rank_src[t.b]);
     return (ra == 0 || rb == 0) ? 0 : rb;
 }
 
-// Dense-mode accumulation (m <= HCOV_DENSE_MAX): S += U V^T - sum_k terms_k (S zero on entry),
-// in batches of at most Wcap columns gathered into XA / YB (m x Wcap each, global scratch).
-// Returns the flops.
+// S[ar + i, br + j] -= sum_k A(i, k) B(j, k) for the 32 x 32 target of a tile x tile term (the
+// tiles staged in shared memory, 2 x 32 x 32 doubles of sb); all threads of the CTA, in term order.
+__device__ __forceinline__ void tt_apply(const Ctx &c, const DTerm &t, double *S, int64_t m, int64_t R0, int64_t C0,
+                                         double *sb)
+{
+    const DNode na = c.nodes[c.tile_node[t.a]], nb = c.nodes[c.tile_node[t.b]];
+    const int64_t ar = (int64_t)na.i * HCOV_LEAF - R0, br = (int64_t)nb.i * HCOV_LEAF - C0;
+    const double *A = c.tiles + (int64_t)t.a * HCOV_TILE, *B = c.tiles + (int64_t)t.b * HCOV_TILE;
+    for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
+        sb[e] = __ldcg(A + e);
+        sb[HCOV_TILE + e] = __ldcg(B + e);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < HCOV_TILE; e += NT) {
+        const int i = e & 31, j = e >> 5;
+        double s = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) s = fma(sb[i + 32 * k], sb[HCOV_TILE + j + 32 * k], s);
+        const int64_t gi = ar + i, gj = br + j;
+        if (gi >= 0 && gi < m && gj >= 0 && gj < m) S[gi + m * gj] -= s;
+    }
+    __syncthreads();
+}
+
+// Dense-mode accumulation (m <= c.dense_max): S += U V^T - sum_k terms_k (S zero on entry), in
+// batches of at most Wcap columns gathered into XA / YB (m x Wcap each, global scratch) for the
+// low-rank terms; tile x tile terms go straight to their 32 x 32 target (tt_apply) instead of
+// being zero-padded to m rows.  Returns the flops.
 #define DENSE_BATCH 128
 __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int64_t m, int64_t R0, int64_t C0,
                                    const double *U, const double *V, int r0, double *XA, int64_t Wcap, double *sb,
@@ -1115,14 +1143,7 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
             if (w == 0) continue;
             double *xc = XA + m * off, *yc = YB + m * off;
             if (t.kind == TM_TT) {
-                const DNode na = c.nodes[c.tile_node[t.a]], nb = c.nodes[c.tile_node[t.b]];
-                const int64_t ar = (int64_t)na.i * HCOV_LEAF - R0, br = (int64_t)nb.i * HCOV_LEAF - C0;
-                const double *A = c.tiles + (int64_t)t.a * HCOV_TILE, *B = c.tiles + (int64_t)t.b * HCOV_TILE;
-                for (int k = 0; k < 32; ++k)
-                    for (int64_t i = lane; i < m; i += 32) {
-                        xc[i + m * k] = (i >= ar && i < ar + 32) ? -__ldcg(A + (i - ar) + 32 * k) : 0.0;
-                        yc[i + m * k] = (i >= br && i < br + 32) ? __ldcg(B + (i - br) + 32 * k) : 0.0;
-                    }
+                continue;   // tt_apply below
             } else {
                 const Fac A = get_fac(c, t.a), B = get_fac(c, t.b);
                 const int ra = A.ncols;
@@ -1186,6 +1207,13 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
             else dense_gemm_add<4, 8>(S, (int)m, XA, YB, W, sb);
             fl += 2.0 * m * m * W;
         }
+        for (int j = 0; j < nt; ++j) {
+            const DTerm t = c.terms[c.xterm[kk + j]];
+            if (t.kind == TM_TT) {
+                tt_apply(c, t, S, m, R0, C0, sb);
+                fl += 2.0 * HCOV_TILE * 32;
+            }
+        }
         PH_END(15, tdg);
         kk = s_next;
         first = false;
@@ -1212,7 +1240,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     const int maxw = max(32, c.kcap);
     double *X2, *Y2;
     if (gg) gang_rows(*gg, m);
-    if (m <= HCOV_DENSE_MAX) {
+    if (m <= c.dense_max) {
         // small block: exact dense accumulation S = U V^T - sum of terms (m x m), fully pivoted
         // cross approximation of S to 0.1 eps |S|_max / m (so |S - X Y^T|_2 <= 0.1 eps |S|_2), then
         // QR + SVD truncation to (eps, kmax)
@@ -1248,7 +1276,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         else record_rank(c, r, rk, cb, of);
         return;
     }
-    // factor mode (m > HCOV_DENSE_MAX); rows [q0, q0 + mq) belong to this CTA (the whole block
+    // factor mode (m > c.dense_max); rows [q0, q0 + mq) belong to this CTA (the whole block
     // without a gang); the panels w.X, w.Y, X2, Y2 hold those rows (ld mq).
     CompressWs w = make_ws(scr, gg ? gg->mq : m, K, &X2, &Y2, gg ? 4 : 6);
     if (gg) w.tsr = scr + task_scratch_base(gg->mq, c.kcap, 4);

@@ -1007,7 +1007,8 @@ hcov_status engine_alloc(hcov_tree t, int kcap, int ninst)
         // (m / G rows, 4 panels) followed by the gang's shared workspace (used when the CTA is member
         // 0); members of more than HCOV_BIG_MQ rows (gangs on the largest blocks) use one of
         // HCOV_BIG_GROUPS shared big-member groups instead
-        const int64_t med_m = std::min<int64_t>(HCOV_GANG_MIN / 2, std::max<int64_t>(P.max_rm, 32));
+        const int64_t med_m = std::min<int64_t>(std::max<int64_t>(HCOV_GANG_MIN / 2, P.opt.big_m),
+                                                std::max<int64_t>(P.max_rm, 32));
         E.gshared_off = 0;
         E.scr_stride = task_scratch(med_m, kcap);
         E.bstride = 0;
@@ -1108,6 +1109,7 @@ void fill_ctx(hcov_hmat h)
     c.indeg = h->indeg; c.gbar = h->gbar; c.gslot = h->gslot;
     c.band_off = t->d_band_off;
     c.factor_trunc = P.opt.factor_trunc ? 1 : 0;
+    c.dense_max = (int32_t)P.opt.big_m;
     c.flop = nullptr;
     const char *wd = std::getenv("HCOV_WATCHDOG_S");
     double wds = wd ? std::atof(wd) : 300.0;
@@ -1355,6 +1357,7 @@ static void plan_env_overrides(PlanOpts &o)
     if (const char *e = std::getenv("HCOV_GANG_ROWS")) o.gang_rows = std::atoll(e);
     if (const char *e = std::getenv("HCOV_GANG_MAX_SMALL")) o.gang_max_small = std::atoi(e);
     if (const char *e = std::getenv("HCOV_RAPP512")) o.rapp512 = std::atoi(e);
+    if (const char *e = std::getenv("HCOV_BIG_M")) { const int v = std::atoi(e); if (v == 64 || v == 128 || v == 256 || v == 512) o.big_m = v; }
 }
 
 hcov_status hcov_build_tree_host_ex(const double *s_host, int64_t n, const hcov_tree_opts *opts, hcov_tree *out)

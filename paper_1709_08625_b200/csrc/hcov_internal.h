@@ -8,7 +8,7 @@
 #define HCOV_GANG 8           // largest gang (CTAs cooperating on one task); HCOV_BANDS * (HCOV_GANG - 1)
                               // must stay below the number of engine CTAs (at most one partially
                               // formed gang per band can hold CTAs, so every gang eventually forms)
-#define HCOV_DENSE_MAX 256    // low-rank blocks up to this size are recompressed from a dense accumulation
+#define HCOV_DENSE_MAX 512    // largest low-rank block the dense-mode RAPP supports (PlanOpts.big_m picks the split)
 #define HCOV_SMEM_DBL 28160 // dynamic shared memory of the engine CTA (220 KB + static <= 227 KB; one 512-thread CTA per SM)
 #define HCOV_BIG_MQ 8192      // gang members with more rows use a big-member scratch slot (hcov.cu)
 #define HCOV_BIG_GROUPS 4     // big-member groups (HCOV_GANG slots each)

@@ -25,6 +25,8 @@ thread_local int64_t t_gang1_below = 0;
 // gang shape (PlanOpts): rows per member, largest gang below m = 65,536, RAPP gang of m = 512
 thread_local int64_t t_gang_rows = 256;
 thread_local int32_t t_gang_max_small = 4, t_rapp512 = 4;
+// largest low-rank block whose RAPP is one dense-mode task on a single CTA (PlanOpts.big_m)
+thread_local int64_t t_big_m = 256;
 
 // gang size of an ACA / RAPP task of a low-rank block of size m (0 = a single CTA, queue 0)
 inline int32_t gang_of(int64_t m)
@@ -38,9 +40,10 @@ inline int32_t gang_of(int64_t m)
 }
 // RAPP gangs of blocks below 65,536 rows are side-split (DTask.pad = 1): half the members factor
 // the X panel, half the Y panel (one QR per member instead of two; engine.cuh gang_compress_split)
-inline bool rapp_split(int64_t m) { return m >= HCOV_GANG_MIN && m >= t_gang1_below && m < 65536; }
+inline bool rapp_split(int64_t m) { return m >= HCOV_GANG_MIN && m >= t_gang1_below && m < 65536 && m > t_big_m; }
 inline int32_t rapp_gang_of(int64_t m)
 {
+    if (m <= t_big_m) return 0;
     if (!rapp_split(m)) return gang_of(m);
     return m <= 512 ? t_rapp512 : HCOV_GANG;
 }
@@ -523,6 +526,8 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt, const P
     P.opt.dense_below = std::max(opt.dense_below, HCOV_LEAF);
     P.opt.chunk = std::max(1, opt.chunk);
     P.opt.fill_tiles = std::max(1, opt.fill_tiles);
+    P.opt.big_m = std::max<int64_t>(32, std::min<int64_t>(HCOV_DENSE_MAX, opt.big_m));
+    t_big_m = P.opt.big_m;
     int L = 0;
     while (((int64_t)HCOV_LEAF << L) < n) ++L;
     P.n = n; P.depth = L; P.n_leaves = (int64_t)1 << L; P.n_pad = (int64_t)HCOV_LEAF << L;
@@ -735,7 +740,8 @@ int plan_build(Plan &P, const double *s, int64_t n, const PlanOpts &opt, const P
             if (k.type == TK_NOP) w[t] = 0.0;
             else if (k.type == TK_RAPP || k.type == TK_ACA) {
                 const double m = (double)P.rblk[k.a].m;
-                w[t] = (m <= HCOV_DENSE_MAX) ? 40.0 : 40.0 + m / (64.0 * std::max(1, k.qcls));
+                if (k.type == TK_RAPP && m <= P.opt.big_m) w[t] = 40.0 * std::max(1.0, m * m / 65536.0);   // dense mode
+                else w[t] = (m <= 256) ? 40.0 : 40.0 + m / (64.0 * std::max(1, k.qcls));
             } else if (k.type == TK_SEG || k.type == TK_PHWR || k.type == TK_BSEG) w[t] = 3.0;
         }
         double bmax = 0.0;

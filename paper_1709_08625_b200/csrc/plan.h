@@ -14,7 +14,8 @@ struct PlanOpts {
     int chunk = 4;          // pending terms applied per TAPP task
     int rchunk = 3;         // pending terms appended per RAPP task of a large low-rank block
     int fill_tiles = 8;     // tiles per FILL task
-    int64_t big_m = HCOV_DENSE_MAX;   // larger low-rank blocks: chunked recompression, capacity 2 kcap
+    int64_t big_m = 256;    // low-rank blocks up to this size: one dense-mode RAPP task (a single CTA);
+                            // larger ones: chunked recompression (gangs), capacity 2 kcap (<= HCOV_DENSE_MAX)
     int dim = 2;            // 2-D locations, or 3 (the 3-D variant)
     int64_t gang_rows = 256;   // rows per gang member (ACA / non-split RAPP gangs: G = m / gang_rows)
     int gang_max_small = 4;    // largest such gang below m = 65,536
