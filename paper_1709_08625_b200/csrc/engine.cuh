@@ -92,6 +92,9 @@ struct Ctx {
     int32_t *bgrp_cta;         // per CTA (member 0 of a gang): the group its gang holds
     int32_t big_mq;            // gang members with more rows than this use a big-member slot
     int32_t dense_max;         // low-rank blocks up to this size use the dense-mode RAPP (PlanOpts.big_m)
+    int32_t dense_dmma;        // dense-mode S += XA YB^T on the FP64 tensor cores (HCOV_DENSE_DMMA, default 1)
+    int32_t term_min;          // a pending term A K B^T enters a panel with min(rank A, rank B) columns:
+                               // [-A K, B] (rank B columns) or [-A, B K^T] (rank A), HCOV_TERM_MIN, default 1
     int32_t n_bgrp;
     double *flop;              // FC_N accumulators
     int64_t smem_dbl;          // dynamic shared memory of the engine (doubles)
@@ -280,7 +283,10 @@ __host__ __device__ inline int aca_kmax(int64_t m, int kcap)
     int64_t k = 2 * (int64_t)kcap + 32;
     return (int)(k < m ? k : m);
 }
-__host__ __device__ inline int kbuf_of(int kcap) { return 3 * kcap + 32; }
+#ifndef HCOV_KBUF_MULT
+#define HCOV_KBUF_MULT 3   // panel width of a chunked accumulation: HCOV_KBUF_MULT kcap + 32 columns
+#endif
+__host__ __device__ inline int kbuf_of(int kcap) { return HCOV_KBUF_MULT * kcap + 32; }
 // In-CTA TSQR of a member's rows (> 256): chunks of <= 256 rows, per side nc x K taus and nc
 // node slots of (2 K x K panel + K taus).
 __host__ __device__ inline int ts_nchunks(int64_t mq) { return (int)((mq + 255) / 256); }
@@ -413,9 +419,10 @@ __device__ __forceinline__ void gang_sync(Gang &gg)
         const int target = gg.nb * gg.G;
         __threadfence();
         atomicAdd(gg.bar, 1);
+        unsigned spin = 0;
         while (*bar < target) {
-            if (*abort) break;
-            __nanosleep(64);
+            if ((++spin & 63u) == 0 && *abort) break;
+            __nanosleep(32);
         }
         __threadfence();
     }
@@ -1061,13 +1068,74 @@ __device__ void dense_gemm_add(double *S, int m, const double *XA, const double 
     __syncthreads();
 }
 
+// S (m x m, ld m) += XA YB^T on the FP64 tensor cores (the U V^T low-rank-update product of the
+// dense-mode accumulation; north_star: DMMA for the truly dense contractions).  XA, YB: m x W (ld m,
+// global scratch).  CTA tile (8 WM WGM) x (8 WN WGN), warp grid WGM x WGN (= NWARP warps), every
+// warp WM x WN mma.sync.m8n8k4.f64 blocks; k staged through shared memory in chunks of 32, row
+// stride (tile + 4) doubles so the four k of a fragment load fall into disjoint banks.
+// sb: 32 (TM + TN + 8) doubles.
+template <int WM, int WN, int WGM, int WGN>
+__device__ void dense_gemm_add_dmma(double *S, int m, const double *XA, const double *YB, int W, double *sb)
+{
+    static_assert(WGM * WGN == NWARP, "warp grid must cover the CTA");
+    constexpr int KC = 32, TM = 8 * WM * WGM, TN = 8 * WN * WGN, LX = TM + 4, LY = TN + 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp % WGM, wn = warp / WGM;
+    const int g = lane >> 2, q = lane & 3;
+    double *xs = sb, *ys = sb + KC * LX;
+    for (int c0 = 0; c0 < m; c0 += TN)
+    for (int p0 = 0; p0 < m; p0 += TM) {
+        double acc[WM][WN][2];
+#pragma unroll
+        for (int u = 0; u < WM; ++u)
+#pragma unroll
+            for (int v = 0; v < WN; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+        for (int k0 = 0; k0 < W; k0 += KC) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < KC * TM; e += NT) {
+                const int k = e / TM, i = e % TM;
+                xs[k * LX + i] = (p0 + i < m && k0 + k < W) ? __ldcg(XA + (p0 + i) + (int64_t)m * (k0 + k)) : 0.0;
+            }
+            for (int e = threadIdx.x; e < KC * TN; e += NT) {
+                const int k = e / TN, j = e % TN;
+                ys[k * LY + j] = (c0 + j < m && k0 + k < W) ? __ldcg(YB + (c0 + j) + (int64_t)m * (k0 + k)) : 0.0;
+            }
+            __syncthreads();
+            const int kc = min(KC, (W - k0 + 3) & ~3);
+            const double *xw = xs + 8 * WM * wm + g, *yw = ys + 8 * WN * wn + g;
+#pragma unroll 2
+            for (int kk = 0; kk < kc; kk += 4) {
+                double a[WM], b[WN];
+#pragma unroll
+                for (int u = 0; u < WM; ++u) a[u] = xw[(kk + q) * LX + 8 * u];
+#pragma unroll
+                for (int v = 0; v < WN; ++v) b[v] = yw[(kk + q) * LY + 8 * v];
+#pragma unroll
+                for (int u = 0; u < WM; ++u)
+#pragma unroll
+                    for (int v = 0; v < WN; ++v) dmma_8x8x4(acc[u][v][0], acc[u][v][1], a[u], b[v]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < WM; ++u)
+#pragma unroll
+            for (int v = 0; v < WN; ++v) {
+                const int i = p0 + 8 * (WM * wm + u) + g, j = c0 + 8 * (WN * wn + v) + 2 * q;
+                if (i < m && j < m) S[i + (int64_t)m * j] += acc[u][v][0];
+                if (i < m && j + 1 < m) S[i + (int64_t)m * (j + 1)] += acc[u][v][1];
+            }
+    }
+    __syncthreads();
+}
+
 // Columns of one pending term in the batched GEMM of the dense accumulation (0 if a factor has rank
 // 0; 0 for a tile x tile term, which is applied directly to its 32 x 32 target, tt_apply).
 __device__ __forceinline__ int term_width(const Ctx &c, const DTerm &t)
 {
     if (t.kind == TM_TT) return 0;
     const int ra = __ldcg(c.rank + c.fac_rank_src[t.a]), rb = __ldcg(c.rank + c.fac_rank_src[t.b]);
-    return (ra == 0 || rb == 0) ? 0 : rb;
+    if (ra == 0 || rb == 0) return 0;
+    return (t.core >= 0 && c.term_min && ra < rb) ? ra : rb;
 }
 
 // S[ar + i, br + j] -= sum_k A(i, k) B(j, k) for the 32 x 32 target of a tile x tile term (the
@@ -1146,43 +1214,58 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
                 continue;   // tt_apply below
             } else {
                 const Fac A = get_fac(c, t.a), B = get_fac(c, t.b);
-                const int ra = A.ncols;
+                const int ra = A.ncols, rbn = B.ncols;
                 const int64_t r_lo = max(R0, A.row0), r_hi = min(R0 + m, A.row0 + A.nrows);
                 const int64_t c_lo = max(C0, B.row0), c_hi = min(C0 + m, B.row0 + B.nrows);
                 const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcore * c.kcore : nullptr;
-                // the core K (ra x w) staged in this warp's slice of shared memory: kb[a + ra b]
+                // the core K (ra x rbn) staged in this warp's slice of shared memory: kb[a + ra b]
                 double *kb = sb + (int64_t)warp * kbw;
-                const bool kstaged = Kc && ra * w <= kbw;
+                const bool kstaged = Kc && ra * rbn <= kbw;
                 if (kstaged) {
-                    for (int e = lane; e < ra * w; e += 32) kb[e] = __ldcg(Kc + (e % ra) + (int64_t)c.kcore * (e / ra));
+                    for (int e = lane; e < ra * rbn; e += 32) kb[e] = __ldcg(Kc + (e % ra) + (int64_t)c.kcore * (e / ra));
                     __syncwarp();
                 }
+                // the product side: [-A K, B] (w = rbn columns) or, when A has the lower rank,
+                // [-A, B K^T] (w = ra columns; term_width).  F: the factor multiplied by the core
+                // (nin columns), M(l, o) = km[l sl + o so] the core as seen from F.
+                const bool swp = Kc && w < rbn;
+                const int nin = swp ? rbn : ra;
+                const double *km = kstaged ? kb : Kc;
+                const int64_t kld = kstaged ? ra : c.kcore;
+                const int64_t sl = swp ? kld : 1, so = swp ? 1 : kld;
+                const double sgn = swp ? 1.0 : -1.0;
                 for (int64_t i = lane; i < m; i += 32) {
                     const int64_t gi = R0 + i, gj = C0 + i;
                     const bool inr = gi >= r_lo && gi < r_hi, inc = gj >= c_lo && gj < c_hi;
-                    const double *Ar = A.p + (gi - A.row0);
-                    if (!inr) {
-                        for (int b = 0; b < w; ++b) xc[i + m * b] = 0.0;
+                    const double *Ar = A.p + (gi - A.row0), *Br = B.p + (gj - B.row0);
+                    double *pc = swp ? yc : xc;          // the product panel, the plain-copy panel
+                    double *cc = swp ? xc : yc;
+                    const bool inp = swp ? inc : inr, inq = swp ? inr : inc;
+                    const double *Fr = swp ? Br : Ar, *Gr = swp ? Ar : Br;
+                    const int64_t fld = swp ? B.ld : A.ld, gld = swp ? A.ld : B.ld;
+                    const double csg = swp ? -1.0 : 1.0;  // sign of the copied panel (X carries the minus)
+                    if (!inp) {
+                        for (int b = 0; b < w; ++b) pc[i + m * b] = 0.0;
                     } else if (!Kc) {
-                        for (int b = 0; b < w; ++b) xc[i + m * b] = -__ldcg(Ar + A.ld * b);
+                        for (int b = 0; b < w; ++b) pc[i + m * b] = -__ldcg(Fr + fld * b);
                     } else {
                         for (int b0 = 0; b0 < w; b0 += 8) {
                             double acc[8];
 #pragma unroll
                             for (int bb = 0; bb < 8; ++bb) acc[bb] = 0.0;
-                            for (int a0 = 0; a0 < ra; a0 += 4) {
+                            for (int a0 = 0; a0 < nin; a0 += 4) {
                                 double xa[4];
 #pragma unroll
-                                for (int u = 0; u < 4; ++u) xa[u] = (a0 + u < ra) ? __ldcg(Ar + A.ld * (a0 + u)) : 0.0;
+                                for (int u = 0; u < 4; ++u) xa[u] = (a0 + u < nin) ? __ldcg(Fr + fld * (a0 + u)) : 0.0;
 #pragma unroll
                                 for (int u = 0; u < 4; ++u) {
                                     const int a = a0 + u;
-                                    if (a < ra) {
+                                    if (a < nin) {
 #pragma unroll
                                         for (int bb = 0; bb < 8; ++bb)
                                             if (b0 + bb < w) {
-                                                const double kv = kstaged ? kb[a + ra * (b0 + bb)]
-                                                                          : __ldcg(Kc + a + (int64_t)c.kcore * (b0 + bb));
+                                                const double kv = kstaged ? km[a * sl + (b0 + bb) * so]
+                                                                          : __ldcg(km + a * sl + (b0 + bb) * so);
                                                 acc[bb] = fma(xa[u], kv, acc[bb]);
                                             }
                                     }
@@ -1190,19 +1273,22 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
                             }
 #pragma unroll
                             for (int bb = 0; bb < 8; ++bb)
-                                if (b0 + bb < w) xc[i + m * (b0 + bb)] = -acc[bb];
+                                if (b0 + bb < w) pc[i + m * (b0 + bb)] = sgn * acc[bb];
                         }
                     }
                     for (int b = 0; b < w; ++b)
-                        yc[i + m * b] = inc ? __ldcg(B.p + (gj - B.row0) + B.ld * b) : 0.0;
+                        cc[i + m * b] = inq ? csg * __ldcg(Gr + gld * b) : 0.0;
                 }
-                if (Kc) fl += 2.0 * (r_hi - r_lo) * ra * w;
+                if (Kc) fl += 2.0 * (swp ? c_hi - c_lo : r_hi - r_lo) * ra * rbn;
             }
         }
         __syncthreads();
         PH_BEGIN(tdg);
         if (W > 0) {
-            if (m <= 64) dense_gemm_add<4, 2>(S, (int)m, XA, YB, W, sb);
+            if (c.dense_dmma) {
+                if (m <= 64) dense_gemm_add_dmma<2, 2, 4, 4>(S, (int)m, XA, YB, W, sb);
+                else dense_gemm_add_dmma<4, 4, 4, 4>(S, (int)m, XA, YB, W, sb);
+            } else if (m <= 64) dense_gemm_add<4, 2>(S, (int)m, XA, YB, W, sb);
             else if (m <= 128) dense_gemm_add<8, 4>(S, (int)m, XA, YB, W, sb);
             else dense_gemm_add<4, 8>(S, (int)m, XA, YB, W, sb);
             fl += 2.0 * m * m * W;
@@ -1245,7 +1331,7 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
         // cross approximation of S to 0.1 eps |S|_max / m (so |S - X Y^T|_2 <= 0.1 eps |S|_2), then
         // QR + SVD truncation to (eps, kmax)
         // S lives in shared memory when it leaves room for the GEMM staging (m <= 128)
-        const int64_t stage = m <= 64 ? 32 * 128 : m <= 128 ? 32 * 256 : 32 * 320;   // dense_gemm_add staging
+        const int64_t stage = m <= 64 ? 32 * 136 : m <= 128 ? 32 * 264 : 32 * 320;   // dense_gemm_add(_dmma) staging
         const bool s_sm = m * m + stage <= c.smem_dbl;
         double *S = s_sm ? smem : scr;
         double *gs = s_sm ? smem + m * m : smem;
@@ -1298,10 +1384,15 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
     for (int kk = tk.b; kk < tk.c; ++kk) {
         const DTerm t = c.terms[c.xterm[kk]];
         int width;
+        bool swp = false;   // LR term with rank A < rank B: appended as [-A, B K^T] (rank A columns)
         if (t.kind == TM_TT) width = 32;
-        else width = __ldcg(c.rank + c.fac_rank_src[t.b]);
+        else {
+            width = __ldcg(c.rank + c.fac_rank_src[t.b]);
+            const int wa = __ldcg(c.rank + c.fac_rank_src[t.a]);
+            if (wa == 0) continue;
+            if (t.core >= 0 && c.term_min && wa < width) { width = wa; swp = true; }
+        }
         if (width == 0) continue;
-        if (t.kind == TM_LR && __ldcg(c.rank + c.fac_rank_src[t.a]) == 0) continue;
         if (cur + width > K) {
             int icb = 0, iof = 0, rk;
             if (split)
@@ -1342,24 +1433,31 @@ __device__ void task_rapp(const Ctx &c, const DTask &tk, double *scr, double *sm
             const int64_t c_lo = max(C0 + q0, B.row0), c_hi = min(C0 + q0 + mq, B.row0 + B.nrows);
             const double *Kc = (t.core >= 0) ? c.cores + (int64_t)t.core * c.kcore * c.kcore : nullptr;
             if (doX && r_hi > r_lo) {
-                if (Kc) {   // xc = -A K  (columns b < rb), staged GEMM
+                if (Kc && !swp) {   // xc = -A K  (columns b < rb), staged GEMM
                     cta_gemm_nt(xc + (r_lo - R0 - q0), mq, r_hi - r_lo, rb, ra, A.p + (r_lo - A.row0), A.ld, Kc, c.kcore,
                                 1, -1.0, smem);
                     fl += 2.0 * (r_hi - r_lo) * ra * rb;
                 } else {
-                    for (int64_t e = threadIdx.x; e < (r_hi - r_lo) * (int64_t)rb; e += NT) {
+                    for (int64_t e = threadIdx.x; e < (r_hi - r_lo) * (int64_t)width; e += NT) {
                         int64_t i = e % (r_hi - r_lo);
                         int b = (int)(e / (r_hi - r_lo));
                         xc[(r_lo - R0 - q0) + i + mq * b] = -__ldcg(A.p + (r_lo - A.row0) + i + A.ld * b);
                     }
                 }
             }
-            if (doY && c_hi > c_lo)
-                for (int64_t e = threadIdx.x; e < (c_hi - c_lo) * (int64_t)rb; e += NT) {
-                    int64_t i = e % (c_hi - c_lo);
-                    int b = (int)(e / (c_hi - c_lo));
-                    yc[(c_lo - C0 - q0) + i + mq * b] = __ldcg(B.p + (c_lo - B.row0) + i + B.ld * b);
+            if (doY && c_hi > c_lo) {
+                if (swp) {   // yc = B K^T  (columns a < ra), staged GEMM
+                    cta_gemm_nt(yc + (c_lo - C0 - q0), mq, c_hi - c_lo, ra, rb, B.p + (c_lo - B.row0), B.ld, Kc, 1,
+                                c.kcore, 1.0, smem);
+                    fl += 2.0 * (c_hi - c_lo) * ra * rb;
+                } else {
+                    for (int64_t e = threadIdx.x; e < (c_hi - c_lo) * (int64_t)rb; e += NT) {
+                        int64_t i = e % (c_hi - c_lo);
+                        int b = (int)(e / (c_hi - c_lo));
+                        yc[(c_lo - C0 - q0) + i + mq * b] = __ldcg(B.p + (c_lo - B.row0) + i + B.ld * b);
+                    }
                 }
+            }
         }
         __syncthreads();
         PH_END(14, tap);

@@ -140,6 +140,12 @@ __device__ __forceinline__ unsigned long long gtimer()
     return t;
 }
 __device__ __forceinline__ int ld_volatile(const int32_t *p) { return *(volatile const int32_t *)p; }
+__device__ __forceinline__ uint4 ld_volatile_v4(const uint32_t *p)
+{
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
 
 
 // Queue entries: (global task id << QE_SHIFT) | gang member, global task id = instance * ntasks +
@@ -212,7 +218,27 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_engine(Ctx c, const Ctx *__res
                 if (ld_volatile((const int32_t *)c.qctl + QC_DONE0) >= c.nq[0]) break;
                 if (ld_volatile((const int32_t *)c.qctl + QC_ABORT)) break;
                 bool got = false;
-                for (int b = HCOV_BANDS - 1; b >= 0 && !got; --b) {
+                // one pass of independent 16-byte loads over the band heads and tails (the per-band
+                // head -> entry chain of dependent L2 loads made an idle scan ~16 x 2 L2 latencies)
+                static_assert(HCOV_BANDS == 16, "vectorised band scan");
+                unsigned nonempty = 0;
+                {
+                    uint4 hv[4], tv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) hv[i] = ld_volatile_v4(c.qctl + QC_BHEAD + 4 * i);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) tv[i] = ld_volatile_v4(c.qctl + QC_BTAIL + 4 * i);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        nonempty |= (hv[i].x < tv[i].x ? 1u : 0u) << (4 * i);
+                        nonempty |= (hv[i].y < tv[i].y ? 1u : 0u) << (4 * i + 1);
+                        nonempty |= (hv[i].z < tv[i].z ? 1u : 0u) << (4 * i + 2);
+                        nonempty |= (hv[i].w < tv[i].w ? 1u : 0u) << (4 * i + 3);
+                    }
+                }
+                while (nonempty && !got) {
+                    const int b = 31 - __clz(nonempty);
+                    nonempty &= ~(1u << b);
                     const int64_t base = (int64_t)c.band_off[b] * ninst;
                     const uint32_t cap = (uint32_t)((c.band_off[b + 1] - c.band_off[b]) * ninst);
                     while (true) {
@@ -1110,6 +1136,12 @@ void fill_ctx(hcov_hmat h)
     c.band_off = t->d_band_off;
     c.factor_trunc = P.opt.factor_trunc ? 1 : 0;
     c.dense_max = (int32_t)P.opt.big_m;
+    {
+        const char *dm = std::getenv("HCOV_DENSE_DMMA");   // A/B switch: scalar DFMA accumulation when 0
+        c.dense_dmma = (dm && *dm == '0') ? 0 : 1;
+        const char *tm = std::getenv("HCOV_TERM_MIN");     // A/B switch: terms always rank-B wide when 0
+        c.term_min = (tm && *tm == '0') ? 0 : 1;
+    }
     c.flop = nullptr;
     const char *wd = std::getenv("HCOV_WATCHDOG_S");
     double wds = wd ? std::atof(wd) : 300.0;

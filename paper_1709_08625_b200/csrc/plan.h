@@ -12,7 +12,8 @@ struct PlanOpts {
     double eta = 2.0;
     int dense_below = 32;   // admissible blocks of cluster size <= dense_below are dense tiles
     int chunk = 4;          // pending terms applied per TAPP task
-    int rchunk = 3;         // pending terms appended per RAPP task of a large low-rank block
+    int rchunk = 4;         // pending terms appended per RAPP task of a large low-rank block (4 since the
+                            // terms enter with min(rank A, rank B) columns; 3 before)
     int fill_tiles = 8;     // tiles per FILL task
     int64_t big_m = 256;    // low-rank blocks up to this size: one dense-mode RAPP task (a single CTA);
                             // larger ones: chunked recompression (gangs), capacity 2 kcap (<= HCOV_DENSE_MAX)
