@@ -1248,6 +1248,29 @@ __device__ double dense_accumulate(const Ctx &c, const DTask &tk, double *S, int
                         for (int b = 0; b < w; ++b) pc[i + m * b] = 0.0;
                     } else if (!Kc) {
                         for (int b = 0; b < w; ++b) pc[i + m * b] = -__ldcg(Fr + fld * b);
+                    } else if (kstaged && nin <= 24) {
+                        // the row of F in registers first: nin independent L2 loads in flight (one
+                        // latency per row; inside the a-loop below they were exposed four at a time,
+                        // once per block of 8 output columns)
+                        double fa[24];
+#pragma unroll
+                        for (int a = 0; a < 24; ++a) fa[a] = (a < nin) ? __ldcg(Fr + fld * a) : 0.0;
+                        for (int b0 = 0; b0 < w; b0 += 8) {
+                            double acc[8];
+#pragma unroll
+                            for (int bb = 0; bb < 8; ++bb) acc[bb] = 0.0;
+#pragma unroll
+                            for (int a = 0; a < 24; ++a) {
+                                if (a < nin) {
+#pragma unroll
+                                    for (int bb = 0; bb < 8; ++bb)
+                                        if (b0 + bb < w) acc[bb] = fma(fa[a], km[a * sl + (b0 + bb) * so], acc[bb]);
+                                }
+                            }
+#pragma unroll
+                            for (int bb = 0; bb < 8; ++bb)
+                                if (b0 + bb < w) pc[i + m * (b0 + bb)] = sgn * acc[bb];
+                        }
                     } else {
                         for (int b0 = 0; b0 < w; b0 += 8) {
                             double acc[8];

@@ -1250,6 +1250,8 @@ __device__ int aca_full(double *S, int64_t m, double *X, double *Y, int Kmax, do
     double bv = 0.0, ss = 0.0;
     int64_t bi = 0;
     const int64_t mm = m * m;
+    const int mi = (int)m, mmi = (int)mm;   // m <= HCOV_DENSE_MAX (512)
+    const int sh = ((mi & (mi - 1)) == 0) ? 31 - __clz(mi) : -1;
     for (int64_t e = threadIdx.x; e < mm; e += NT) {
         const double v = S[e], a = fabs(v);
         ss += v * v;
@@ -1270,13 +1272,15 @@ __device__ int aca_full(double *S, int64_t m, double *X, double *Y, int Kmax, do
         __syncthreads();
         bv = 0.0; bi = 0; ss = 0.0;
         const double *xk = X + m * k, *yk = Y + m * k;
-        for (int64_t e = threadIdx.x; e < mm; e += NT) {
-            const int64_t j = e / m, i = e - j * m;
+        // (i, j) of entry e in 32-bit arithmetic, by a shift when m is a power of two (every cluster
+        // size is): the 64-bit division per entry was a sizeable part of this pass
+        for (int e = threadIdx.x; e < mmi; e += NT) {
+            const int j = sh >= 0 ? (e >> sh) : e / mi, i = e - j * mi;
             const double v = S[e] - xk[i] * yk[j];
             S[e] = v;
             ss += v * v;
             const double a = fabs(v);
-            if (vi_better(a, e, bv, bi)) { bv = a; bi = e; }
+            if (vi_better(a, (int64_t)e, bv, bi)) { bv = a; bi = e; }
         }
         b = block_argmax(bv, bi, redv, redi);
         fro = sqrt(block_sum(ss, red));
